@@ -1,0 +1,301 @@
+/*
+ * fastmap_b200.h -- C ABI of the B200-native FastMap hot path.
+ *
+ * This is the drop-in boundary for the two gradient-descent stages of the
+ * FastMap reference package (/root/reference/pkg/src/fastmap):
+ *
+ *   epipolar adjustment   ref/epipolar.py:46-319   (precompute_weights,
+ *                          current_residuals, epipolar_loss,
+ *                          quadratic_loss_and_grad, irls_refine)
+ *   global translation    ref/translation.py:112-186 (translation_loss_and_grad,
+ *                          align_centers, per_node_residuals, canonicalize,
+ *                          multi_init_align)
+ *   optimizer / 6D rot    ref/optim.py:11-110       (Adam, rot6d_to_matrix,
+ *                          rot6d_jacobian), ref/model.py:112-116 project_to_so3
+ *
+ * Conventions
+ *   - Every array argument is a DEVICE pointer unless the name says host_.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as void*,
+ *     NULL = legacy default stream).  No call synchronises the device except
+ *     where documented (the *_create helpers).
+ *   - Return value is an fm_status.  On failure fm_last_error() returns a
+ *     thread-local message.  Asynchronous numerical errors (non-finite loss /
+ *     gradient, degenerate 6D rotations) are reported through a device int32
+ *     `flag` word which holds the FIRST fm_status code raised; the host maps it
+ *     to the same Python exception the reference raises.
+ *   - fp64 parameters, fp32 point coordinates.  The packed parameter vector
+ *     has the reference layout [rot6d (n x 6) | centers (n x 3) | log_focal (C)]
+ *     (ref/epipolar.py:95-106).
+ *   - No torch types: plain pointers and sizes only.
+ */
+#ifndef FASTMAP_B200_H
+#define FASTMAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FM_ABI_VERSION 1
+
+typedef enum fm_status {
+  FM_OK = 0,
+  FM_ERR_INVALID = 1,           /* bad arguments              -> ValueError            */
+  FM_ERR_CUDA = 2,              /* CUDA runtime failure       -> RuntimeError          */
+  FM_ERR_NONFINITE_LOSS = 3,    /* ref/epipolar.py:306-307    -> FloatingPointError    */
+  FM_ERR_NONFINITE_GRAD = 4,    /* ref/optim.py:28-29         -> FloatingPointError    */
+  FM_ERR_ROT6D_ZERO = 5,        /* ref/optim.py:50-51         -> ValueError            */
+  FM_ERR_ROT6D_COLLINEAR = 6,   /* ref/optim.py:55-56         -> ValueError            */
+  FM_ERR_NO_ACTIVE = 7,         /* ref/epipolar.py:147-148    -> ValueError            */
+  FM_ERR_ALL_PRUNED = 8,        /* ref/epipolar.py:289-290    -> ValueError            */
+  FM_ERR_NONFINITE_TRANSLATION = 9 /* ref/translation.py:149-150 -> FloatingPointError */
+} fm_status;
+
+/* ------------------------------------------------------------------------ */
+/* library                                                                  */
+/* ------------------------------------------------------------------------ */
+
+int fm_abi_version(void);
+const char* fm_last_error(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int fm_device_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* point-pair store (the per-point data of all EpipolarPair objects)         */
+/* ------------------------------------------------------------------------ */
+/*
+ * Structure of arrays (one (x, y) column per image side, 16 B per point pair),
+ * image pairs sorted by (img_i, img_j) (the order of ref/tracks.py:104).  Pair n owns slots [pair_off[n], pair_off[n]+pair_len[n]);
+ * pair_off[n] is a multiple of 4 so every 128-bit load belongs to one pair.
+ * Padding slots hold zeros and a cleared active bit.  n_slots is a multiple of
+ * 128.  The per-point data replaces EpipolarPair.x1/x2/active
+ * (ref/epipolar.py:19-36); `terms` is never materialised.
+ *
+ * A pass is split into work items of at most `chunk` slots (multiple of 128);
+ * item k belongs to pair item_pair[k]; pair n owns items
+ * [pair_item_off[n], pair_item_off[n+1]).
+ */
+typedef struct fm_point_store {
+  int64_t n_pairs;
+  int64_t n_slots;
+  int64_t n_items;
+  int64_t chunk;
+  const int64_t* pair_off;      /* [n_pairs+1] */
+  const int32_t* pair_len;      /* [n_pairs]   */
+  const int32_t* pair_item_off; /* [n_pairs+1] */
+  const int32_t* item_pair;     /* [n_items]   */
+  const float* x1;              /* [n_slots][2] image-i normalized (x, y), fp32 */
+  const float* x2;              /* [n_slots][2] image-j normalized (x, y), fp32 */
+  const float* x1z;             /* [n_slots] or NULL => homogeneous z == 1 (pipeline case) */
+  const float* x2z;
+  uint32_t* active;             /* [n_slots/32] bit s%32 of word s/32 = slot s active */
+} fm_point_store;
+
+/* Pass mode bits (combine with |). */
+#define FM_PASS_PRUNE        1u   /* active &= |r| <= threshold  (ref/epipolar.py:283) */
+#define FM_PASS_L1           2u   /* l1[n] = sum |r| over pre-prune active (ref :156-160) */
+#define FM_PASS_MOMENTS      4u   /* W moments over post-prune active (ref :46-59)      */
+#define FM_PASS_IRLS         8u   /* weights 1/max(|r|,1e-6) from the pass' own residual */
+#define FM_PASS_ALL_POINTS  16u   /* ignore the mask (current_residuals, ref :251-255)  */
+#define FM_PASS_RES_OUT     32u   /* residual[s] = |r| for every slot                   */
+#define FM_PASS_RES_IN      64u   /* weights 1/max(|res_in[s]|,1e-6) (precompute_weights) */
+#define FM_PASS_F64        128u   /* fp64 moment accumulation (API precision)           */
+#define FM_PASS_SKIP_DROPPED 256u /* skip pairs with prev_active[n] == 0                */
+
+/*
+ * Per-pair outputs of a point pass (SoA, index [k * n_pairs + n]).
+ * W = sum_m w_m t_m t_m^T with t_m = flatten(x2 x1^T) has Kronecker structure:
+ * W[(p,r),(q,s)] = mom[sym(p,q)*6 + sym(r,s)], sym in (00,01,02,11,12,22), so
+ * 36 moments describe it exactly.  IRLS passes also emit the linearisation
+ * terms vgrad = sum w r0 t and s0 = sum w r0^2 of the shifted quadratic model
+ * (see DESIGN.md "shifted quadratic model").
+ */
+typedef struct fm_pass_out {
+  float* mom32;       /* [36][n_pairs] or NULL */
+  double* mom64;      /* [36][n_pairs] or NULL (FM_PASS_F64) */
+  float* vgrad;       /* [9][n_pairs]  or NULL */
+  double* s0;         /* [n_pairs]     or NULL */
+  double* l1;         /* [n_pairs]     or NULL */
+  int32_t* n_active;  /* [n_pairs]     or NULL; post-prune active count */
+  double* residual;   /* [n_slots]     or NULL; FM_PASS_RES_OUT */
+} fm_pass_out;
+
+size_t fm_point_pass_scratch_bytes(const fm_point_store* store);
+
+/*
+ * One fused sweep over all point pairs: residual r = x2^T Ghat_n x1 (fp64),
+ * optional prune, L1 partials, IRLS-weighted W moments and linearisation
+ * terms.  ghat = [9][n_pairs] fp64 (row-major Ghat_n), may be NULL when the
+ * mode needs no residual.  res_in = [n_slots] fp64 for FM_PASS_RES_IN.
+ * prev_active = [n_pairs] for FM_PASS_SKIP_DROPPED.
+ */
+int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold,
+                  const double* ghat, const double* res_in,
+                  const int32_t* prev_active, const fm_pass_out* out,
+                  void* scratch, size_t scratch_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* image-pair graph of the epipolar adjustment                               */
+/* ------------------------------------------------------------------------ */
+/*
+ * Pairs in store order.  pair_i/pair_j are DENSE image indices (positions in
+ * the sorted image_ids of ref/epipolar.py:271); pair_ci/pair_cj are camera ids
+ * (ref/epipolar.py:167-168, not remapped).  Incidence lists make the per-image
+ * and per-camera gradient reductions deterministic gathers (no float atomics):
+ * entries are (pair << 1) | side, side 0 = the image/camera is the pair's i.
+ * Camera lists are cut into chunks of <= 4096 incidences: chunk k covers
+ * cam_inc[cam_chunk_lo[k] .. cam_chunk_lo[k+1]) and belongs to camera
+ * cam_chunk_cam[k]; camera c owns chunks [cam_chunk_off[c], cam_chunk_off[c+1]).
+ */
+typedef struct fm_pair_graph {
+  int32_t n_images;
+  int32_t n_cameras;
+  int32_t refine_focal;
+  int32_t n_cam_chunks;
+  int64_t n_pairs;
+  const int32_t* pair_i;
+  const int32_t* pair_j;
+  const int32_t* pair_ci;
+  const int32_t* pair_cj;
+  const int32_t* img_off;       /* [n_images+1] */
+  const int32_t* img_inc;
+  const int32_t* cam_off;       /* [n_cameras+1] */
+  const int32_t* cam_inc;
+  const int32_t* cam_chunk_lo;  /* [n_cam_chunks+1] */
+  const int32_t* cam_chunk_cam; /* [n_cam_chunks]   */
+  const int32_t* cam_chunk_off; /* [n_cameras+1]    */
+} fm_pair_graph;
+
+/* Quadratic model kinds */
+#define FM_QUAD_SHIFTED32 0  /* hot path: mom32 + vgrad + s0 about ghat0           */
+#define FM_QUAD_W64       1  /* caller-given dense W, row-major [81][n_pairs]       */
+#define FM_QUAD_MOM64     2  /* Kronecker moments in fp64 [36][n_pairs], no shift   */
+
+typedef struct fm_quad_model {
+  int32_t kind;
+  const float* mom32;
+  const float* vgrad;
+  const double* s0;
+  const double* ghat0;   /* [9][n_pairs] linearisation point */
+  const double* w81;
+  const double* mom64;
+} fm_quad_model;
+
+size_t fm_epi_scratch_bytes(const fm_pair_graph* g);
+
+/* ghat[9][n_pairs] of the current state (ref/epipolar.py:109-138). */
+int fm_epi_pair_ghat(const fm_pair_graph* g, const double* params, double* ghat,
+                     int32_t* flag, void* scratch, size_t scratch_bytes, void* stream);
+
+/*
+ * Loss (2/Z) sum ghat^T W ghat and packed gradient (ref/epipolar.py:172-232).
+ * scale = 2/Z.  loss_out: one device double.  grad_out: packed, length
+ * 9*n_images + (refine_focal ? n_cameras : 0).
+ */
+int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q,
+                     const double* params, double scale, double* loss_out,
+                     double* grad_out, int32_t* flag, void* scratch,
+                     size_t scratch_bytes, void* stream);
+
+/*
+ * n_steps fused Adam steps of the quadratic model (the inner loop of
+ * ref/epipolar.py:302-308): per step loss/grad + non-finite checks + Adam
+ * (ref/optim.py:24-36) on the packed params; t counts from t0+1.
+ * use_graph != 0 captures the step sequence in a CUDA graph (cached per
+ * argument set) and replays it.
+ */
+int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q,
+                      double* params, double* adam_m, double* adam_v,
+                      int64_t t0, int32_t n_steps, double lr, double beta1,
+                      double beta2, double eps, double scale, int32_t* flag,
+                      int32_t use_graph, void* scratch, size_t scratch_bytes,
+                      void* stream);
+
+/* Drop every CUDA graph cached by fm_epi_adam_steps (use_graph != 0). */
+void fm_release_cached_graphs(void);
+
+/* rot6d -> SO(3) (ref/optim.py:39-59); project != 0 additionally applies the
+ * polar projection of ref/model.py:112-116.  R_out [n][9] row-major. */
+int fm_rot6d_to_matrix(const double* rot6d, int64_t n, int32_t project,
+                       double* R_out, int32_t* flag, void* stream);
+
+/* Jacobian of rot6d_to_matrix, [n][9][6] (ref/optim.py:68-110). */
+int fm_rot6d_jacobian(const double* rot6d, int64_t n, double* J_out,
+                      void* stream);
+
+/* Batched polar projection of arbitrary 3x3 matrices onto SO(3)
+ * (ref/model.py:112-116). */
+int fm_project_to_so3(const double* M, int64_t n, double* R_out, void* stream);
+
+/* E = [t]x R_j R_i^T, t = -R_j (o_j - o_i)  (ref/epipolar.py:62-70). */
+int fm_compose_essential(const double* R_i, const double* R_j,
+                         const double* o_i, const double* o_j, int64_t n,
+                         double* E_out, void* stream);
+
+/* One Adam step on a flat fp64 vector (ref/optim.py:24-36).  t >= 1. */
+int fm_adam_step(double* params, double* adam_m, double* adam_v,
+                 const double* grad, int64_t n, int64_t t, double lr,
+                 double beta1, double beta2, double eps, int32_t* flag,
+                 void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* global translation (direction graph)                                      */
+/* ------------------------------------------------------------------------ */
+/*
+ * DirectionGraph (ref/translation.py:104-109) plus a node incidence list
+ * node_inc[node_off[v] .. node_off[v+1]) of (edge << 1) | side, side 0 = v is
+ * the edge's i, sorted by edge.  Centres of B independent runs are stored
+ * node-major [n][B][3] fp64 so one gather serves all runs.
+ */
+typedef struct fm_dir_graph {
+  int32_t n_nodes;
+  int64_t n_edges;
+  const int32_t* edge_i;
+  const int32_t* edge_j;
+  const double* dirs;       /* [n_edges][3] unit world directions */
+  const int32_t* node_off;  /* [n_nodes+1] */
+  const int32_t* node_inc;
+} fm_dir_graph;
+
+size_t fm_tr_scratch_bytes(int32_t n_nodes, int64_t n_edges, int32_t n_runs);
+
+/* Mean per-edge L1 direction loss and gradient, per run
+ * (ref/translation.py:112-125).  loss_out [B], grad_out [n][B][3]. */
+int fm_tr_loss_grad(const fm_dir_graph* g, const double* centers, int32_t n_runs,
+                    double* loss_out, double* grad_out, void* scratch,
+                    size_t scratch_bytes, void* stream);
+
+/*
+ * B independent Adam descents of the L1 direction loss, in lock-step
+ * (ref/translation.py:137-152 for each run).  centers [n][B][3] in/out.
+ * loss_out[b] = loss evaluated at the last step (before its update), as the
+ * reference returns it.  Adam state is fresh (t = 1..steps).
+ */
+int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t n_runs,
+                int32_t steps, double lr, double beta1, double beta2,
+                double eps, double* loss_out, int32_t* flag, void* scratch,
+                size_t scratch_bytes, void* stream);
+
+/* canonicalize each run in place (ref/translation.py:128-134). */
+int fm_tr_canonicalize(double* centers, int32_t n_nodes, int32_t n_runs,
+                       void* scratch, size_t scratch_bytes, void* stream);
+
+/* Mean incident-edge L1 residual per node and run, out [n][B]
+ * (ref/translation.py:155-166). */
+int fm_tr_node_residuals(const fm_dir_graph* g, const double* centers,
+                         int32_t n_runs, double* out, void* stream);
+
+/* Multi-init merge (ref/translation.py:178-184): canonicalize every run,
+ * per-node argmin of the mean incident residual (ties -> lowest run), gather.
+ * centers [n][B][3] is canonicalized in place; merged [n][3]; choice [n]. */
+int fm_tr_merge(const fm_dir_graph* g, double* centers, int32_t n_runs,
+                double* merged, int32_t* choice, void* scratch,
+                size_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTMAP_B200_H */

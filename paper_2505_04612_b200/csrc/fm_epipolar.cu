@@ -1,0 +1,682 @@
+// Image-pair level of the epipolar adjustment: per-pair Frobenius-normalised
+// essential/fundamental matrices, the quadratic loss and its gradient in the
+// packed [rot6d | centers | log_focal] parameters, deterministic per-image and
+// per-camera reductions, and the fused Adam step loop
+// (ref/epipolar.py:109-138, :172-248, :302-308; ref/optim.py:24-36).
+//
+// Per step: O(image pairs) work, independent of the number of point pairs
+// (the paper's claim, ref/epipolar.py:3-7).  All fp64.  A step is
+//   pair_grad   (thread / image pair)  -> per-pair dL/dR_i, dL/dR_j, dL/dc, dL/dphi
+//   image_adam  (warp / image)         -> gather over the image's incidences in
+//                                         fixed order, 6D VJP, Adam, new R
+//   cam_chunk   (block / chunk)        -> fixed-order partial focal sums
+//   cam_adam    (thread / camera)      -> focal gradient, Adam
+// and is replayed from a CUDA graph in the hot loop.
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+#include <cmath>
+
+#include "fm_common.cuh"
+
+namespace fm {
+
+namespace {
+
+constexpr int kPG = 24;          // per-pair gradient record: gRi 9, gRj 9, gdc 3, gphi_i, gphi_j, loss
+constexpr int kMaxSteps = 4096;  // steps per fm_epi_adam_steps call (bias-correction table)
+constexpr int kCamBlock = 128;
+
+struct EpiScratch {
+  double* R;      // [N][9]
+  double* pg;     // [kPG][P]
+  double* cpart;  // [n_cam_chunks]
+  double* lpart;  // [loss blocks]
+  double* sched;  // [2 + 2*kMaxSteps]: lr, scale, bc1[], bc2[]
+};
+
+int loss_blocks(int64_t P) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(P, 1024), 1), 1024); }
+
+size_t scratch_need(const fm_pair_graph& g) {
+  size_t b = 0;
+  b += scratch_round((size_t)g.n_images * 9 * sizeof(double));
+  b += scratch_round((size_t)g.n_pairs * kPG * sizeof(double));
+  b += scratch_round((size_t)std::max(g.n_cam_chunks, 1) * sizeof(double));
+  b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
+  b += scratch_round((size_t)(2 + 2 * kMaxSteps) * sizeof(double));
+  return b + 256;
+}
+
+bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
+  Scratch sc(p, n);
+  s.R = sc.take<double>((size_t)g.n_images * 9);
+  s.pg = sc.take<double>((size_t)g.n_pairs * kPG);
+  s.cpart = sc.take<double>((size_t)std::max(g.n_cam_chunks, 1));
+  s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
+  s.sched = sc.take<double>((size_t)(2 + 2 * kMaxSteps));
+  return p != nullptr && sc.ok();
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void image_rot_kernel(const double* __restrict__ params, int n, double* __restrict__ R,
+                                 int32_t* flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double Rk[9];
+  const int code = rot6d_to_R(params + 6 * k, Rk);
+  if (code) raise_flag(flag, code);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) R[9 * k + q] = Rk[q];
+}
+
+// Forward geometry of one image pair (ref/epipolar.py:109-138).
+struct PairFwd {
+  double Ri[9], Rj[9], dc[3], t[3], Rrel[9], E[9], G[9], gh[9];
+  double nrm, di, dj;
+};
+
+__device__ __forceinline__ void pair_forward(const fm_pair_graph& g, const double* params,
+                                             const double* R, int64_t n, PairFwd& f) {
+  const int i = g.pair_i[n], j = g.pair_j[n];
+  const int N = g.n_images;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    f.Ri[q] = R[9 * i + q];
+    f.Rj[q] = R[9 * j + q];
+  }
+  const double* ci = params + 6 * N + 3 * i;
+  const double* cj = params + 6 * N + 3 * j;
+  essential(f.Ri, f.Rj, ci, cj, f.dc, f.t, f.Rrel, f.E);
+  if (g.refine_focal) {
+    f.di = exp(-params[9 * N + g.pair_ci[n]]);
+    f.dj = exp(-params[9 * N + g.pair_cj[n]]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        f.G[a * 3 + b] = (a < 2 ? f.dj : 1.0) * f.E[a * 3 + b] * (b < 2 ? f.di : 1.0);
+  } else {
+    f.di = f.dj = 1.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) f.G[q] = f.E[q];
+  }
+  double ss = 0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) ss += f.G[q] * f.G[q];
+  f.nrm = fmax(sqrt(ss), 1e-15);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) f.gh[q] = f.G[q] / f.nrm;
+}
+
+__global__ void pair_ghat_kernel(const fm_pair_graph g, const double* __restrict__ params,
+                                 const double* __restrict__ R, double* __restrict__ ghat) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= g.n_pairs) return;
+  PairFwd f;
+  pair_forward(g, params, R, n, f);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) ghat[q * g.n_pairs + n] = f.gh[q];
+}
+
+// u = W x for the Kronecker-structured W given by 36 moments:
+// (W x)[p][r] = sum_{q,s} mom[sym(p,q)][sym(r,s)] x[q][s]
+template <typename T>
+__device__ __forceinline__ void mom_apply(const T* __restrict__ mom, int64_t P, int64_t n,
+                                          const double* x, double* u) {
+  double m[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) m[k] = (double)mom[k * P + n];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double acc = 0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) acc = fma(m[sym3(p, q) * 6 + sym3(r, s)], x[q * 3 + s], acc);
+      u[p * 3 + r] = acc;
+    }
+}
+
+// Loss term and full backward of one pair (ref/epipolar.py:172-232).
+template <int KIND>
+__global__ void pair_grad_kernel(const fm_pair_graph g, const fm_quad_model q,
+                                 const double* __restrict__ params, const double* __restrict__ R,
+                                 const double* __restrict__ sched, double* __restrict__ pg,
+                                 int32_t* flag) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t P = g.n_pairs;
+  if (n >= P) return;
+  if (flag && *flag) return;
+  const double scale = sched[1];
+  PairFwd f;
+  pair_forward(g, params, R, n, f);
+
+  double u[9], Ln;
+  if (KIND == FM_QUAD_SHIFTED32) {
+    // ghat^T W ghat = s0 + 2 d^T v + d^T W d, d = ghat - ghat0, v = W ghat0
+    double d[9], Wd[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) d[k] = f.gh[k] - q.ghat0[k * P + n];
+    mom_apply(q.mom32, P, n, d, Wd);
+    double acc = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const double v = (double)q.vgrad[k * P + n];
+      u[k] = v + Wd[k];
+      acc = fma(d[k], v + u[k], acc);
+    }
+    Ln = q.s0[n] + acc;
+  } else if (KIND == FM_QUAD_MOM64) {
+    mom_apply(q.mom64, P, n, f.gh, u);
+    Ln = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Ln = fma(f.gh[k], u[k], Ln);
+  } else {  // dense caller-given W (row-major 9x9)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      double acc = 0;
+#pragma unroll
+      for (int l = 0; l < 9; ++l) acc = fma(q.w81[(k * 9 + l) * P + n], f.gh[l], acc);
+      u[k] = acc;
+    }
+    Ln = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Ln = fma(f.gh[k], u[k], Ln);
+  }
+  const double loss_n = scale * Ln;
+  // d loss / d ghat = (2/Z) 2 W ghat, then through the normalisation
+  double gg[9], dot = 0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    gg[k] = 2.0 * scale * u[k];
+    dot = fma(f.gh[k], gg[k], dot);
+  }
+  double gG[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) gG[k] = (gg[k] - f.gh[k] * dot) / f.nrm;
+
+  double gE[9], gphi_i = 0, gphi_j = 0;
+  if (g.refine_focal) {
+    double si = 0, sj = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double fa = a < 2 ? f.dj : 1.0, fb = b < 2 ? f.di : 1.0;
+        gE[a * 3 + b] = fa * gG[a * 3 + b] * fb;
+        if (b < 2) si += gG[a * 3 + b] * (fa * f.E[a * 3 + b]);  // (Dj E) columns 0,1
+        if (a < 2) sj += gG[a * 3 + b] * (f.E[a * 3 + b] * fb);  // (E Di) rows 0,1
+      }
+    gphi_i = -f.di * si;
+    gphi_j = -f.dj * sj;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) gE[k] = gG[k];
+  }
+  // E = [t]x R_rel:  M_rel = [t]x^T gE,  Pm = gE R_rel^T
+  const double* t = f.t;
+  double Mrel[9], Pm[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    // [t]x^T = [[0,t2,-t1],[-t2,0,t0],[t1,-t0,0]]
+    Mrel[0 * 3 + c] = t[2] * gE[1 * 3 + c] - t[1] * gE[2 * 3 + c];
+    Mrel[1 * 3 + c] = -t[2] * gE[0 * 3 + c] + t[0] * gE[2 * 3 + c];
+    Mrel[2 * 3 + c] = t[1] * gE[0 * 3 + c] - t[0] * gE[1 * 3 + c];
+  }
+  mat3_mul_bt(gE, f.Rrel, Pm);
+  const double gt[3] = {Pm[7] - Pm[5], Pm[2] - Pm[6], Pm[3] - Pm[1]};
+  // t = -R_j dc
+  double gdc[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) gdc[c] = -(f.Rj[0 * 3 + c] * gt[0] + f.Rj[1 * 3 + c] * gt[1] + f.Rj[2 * 3 + c] * gt[2]);
+  double gRj[9], gRi[9];
+  mat3_mul(Mrel, f.Ri, gRj);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) gRj[a * 3 + b] -= gt[a] * f.dc[b];
+  mat3_mul_at(Mrel, f.Rj, gRi);
+
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    pg[k * P + n] = gRi[k];
+    pg[(9 + k) * P + n] = gRj[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pg[(18 + k) * P + n] = gdc[k];
+  pg[21 * P + n] = gphi_i;
+  pg[22 * P + n] = gphi_j;
+  pg[23 * P + n] = loss_n;
+  if (!isfinite(loss_n)) raise_flag(flag, FM_ERR_NONFINITE_LOSS);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+__device__ __forceinline__ void adam_elem(double& p, double& m, double& v, double g, double lr,
+                                          double b1, double b2, double eps, double bc1, double bc2) {
+  const double mk = __dadd_rn(__dmul_rn(b1, m), __dmul_rn(1.0 - b1, g));
+  const double vk = __dadd_rn(__dmul_rn(b2, v), __dmul_rn(1.0 - b2, __dmul_rn(g, g)));
+  m = mk;
+  v = vk;
+  p = __dsub_rn(p, __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, bc1)), __dadd_rn(sqrt(__ddiv_rn(vk, bc2)), eps)));
+}
+
+struct AdamArgs {
+  double* m;
+  double* v;
+  double b1, b2, eps;
+  const double* sched;  // lr, scale, bc1[kMaxSteps], bc2[kMaxSteps]
+  int step;             // index into the bias-correction table
+};
+
+// Warp per image: fixed-order gather of the image's incidences, 6D VJP, then
+// either the packed gradient (API) or an Adam update + new rotation (hot loop).
+template <bool ADAM>
+__global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
+                                    const double* __restrict__ pg, double* __restrict__ grad,
+                                    double* __restrict__ R, const AdamArgs ad, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int N = g.n_images;
+  if (k >= N) return;
+  if (ADAM && *flag) return;
+  const int64_t P = g.n_pairs;
+  double acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0;
+  const int e0 = g.img_off[k], e1 = g.img_off[k + 1];
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const int inc = g.img_inc[e];
+    const int64_t n = inc >> 1;
+    const int side = inc & 1;
+    const int base = side ? 9 : 0;
+    const double sgn = side ? 1.0 : -1.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += pg[(base + q) * P + n];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) acc[9 + q] += sgn * pg[(18 + q) * P + n];
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = warp_sum(acc[q]);
+  if (lane != 0) return;
+  double* v6 = params + 6 * k;
+  double* c3 = params + 6 * N + 3 * k;
+  double g6[6];
+  rot6d_vjp(v6, acc, g6);
+  if (!ADAM) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) grad[6 * k + q] = g6[q];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) grad[6 * N + 3 * k + q] = acc[9 + q];
+    return;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) ok = ok && isfinite(g6[q]);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) ok = ok && isfinite(acc[9 + q]);
+  if (!ok) {
+    raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  const double lr = ad.sched[0];
+  const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    adam_elem(v6[q], ad.m[6 * k + q], ad.v[6 * k + q], g6[q], lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    adam_elem(c3[q], ad.m[6 * N + 3 * k + q], ad.v[6 * N + 3 * k + q], acc[9 + q], lr, ad.b1,
+              ad.b2, ad.eps, bc1, bc2);
+  double Rk[9];
+  const int code = rot6d_to_R(v6, Rk);
+  if (code) raise_flag(flag, code);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) R[9 * k + q] = Rk[q];
+}
+
+// Block per camera chunk: fixed-order partial sum of focal gradients.
+__global__ void cam_chunk_kernel(const fm_pair_graph g, const double* __restrict__ pg,
+                                 double* __restrict__ cpart, const int32_t* flag) {
+  __shared__ double red[kCamBlock];
+  const int c = blockIdx.x;
+  if (flag && *flag) return;
+  const int64_t P = g.n_pairs;
+  const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
+  double acc = 0;
+  for (int e = lo + threadIdx.x; e < hi; e += kCamBlock) {
+    const int inc = g.cam_inc[e];
+    acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kCamBlock / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cpart[c] = red[0];
+}
+
+template <bool ADAM>
+__global__ void cam_final_kernel(const fm_pair_graph g, double* __restrict__ params,
+                                 const double* __restrict__ cpart, double* __restrict__ grad,
+                                 const AdamArgs ad, int32_t* flag) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n_cameras) return;
+  if (ADAM && *flag) return;
+  double acc = 0;
+  for (int k = g.cam_chunk_off[c]; k < g.cam_chunk_off[c + 1]; ++k) acc += cpart[k];
+  const int idx = 9 * g.n_images + c;
+  if (!ADAM) {
+    grad[idx] = acc;
+    return;
+  }
+  if (!isfinite(acc)) {
+    raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  const double lr = ad.sched[0];
+  const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+  adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+}
+
+// Deterministic two-level sum of the per-pair loss terms.
+__global__ void loss_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  double acc = 0;
+  for (int64_t k = blockIdx.x * 256 + threadIdx.x; k < n; k += (int64_t)gridDim.x * 256) acc += x[k];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void loss_final_kernel(const double* __restrict__ part, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double acc = 0;
+    for (int k = 0; k < nb; ++k) acc += part[k];
+    *out = acc;
+  }
+}
+
+__global__ void set_sched_kernel(double* sched, double lr, double scale) {
+  sched[0] = lr;
+  sched[1] = scale;
+}
+
+int launch_pair_grad(const fm_pair_graph& g, const fm_quad_model& q, const double* params,
+                     const EpiScratch& s, int32_t* flag, cudaStream_t st) {
+  const unsigned blocks = (unsigned)ceil_div(g.n_pairs, 128);
+  switch (q.kind) {
+    case FM_QUAD_SHIFTED32:
+      pair_grad_kernel<FM_QUAD_SHIFTED32><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      break;
+    case FM_QUAD_W64:
+      pair_grad_kernel<FM_QUAD_W64><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      break;
+    case FM_QUAD_MOM64:
+      pair_grad_kernel<FM_QUAD_MOM64><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      break;
+    default:
+      return set_error(FM_ERR_INVALID, "unknown quadratic model kind %d", q.kind);
+  }
+  FM_LAUNCHED(pair_grad_kernel);
+  return FM_OK;
+}
+
+int check_graph(const fm_pair_graph* g) {
+  FM_REQUIRE(g, "null pair graph");
+  FM_REQUIRE(g->n_images >= 0 && g->n_pairs >= 0 && g->n_cameras >= 0, "negative graph sizes");
+  FM_REQUIRE(!g->refine_focal || g->n_cameras > 0, "refine_focal needs n_cameras > 0");
+  return FM_OK;
+}
+
+int check_quad(const fm_quad_model* q) {
+  FM_REQUIRE(q, "null quadratic model");
+  if (q->kind == FM_QUAD_SHIFTED32)
+    FM_REQUIRE(q->mom32 && q->vgrad && q->s0 && q->ghat0, "incomplete shifted model");
+  else if (q->kind == FM_QUAD_W64)
+    FM_REQUIRE(q->w81, "missing dense W");
+  else if (q->kind == FM_QUAD_MOM64)
+    FM_REQUIRE(q->mom64, "missing fp64 moments");
+  else
+    return set_error(FM_ERR_INVALID, "unknown quadratic model kind %d", q->kind);
+  return FM_OK;
+}
+
+// Enqueue n_steps optimizer steps (kernels only, no host work) on `st`.
+int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params, double* m,
+                  double* v, int n_steps, double b1, double b2, double eps, const EpiScratch& s,
+                  int32_t* flag, cudaStream_t st) {
+  const int N = g.n_images;
+  for (int step = 0; step < n_steps; ++step) {
+    int rc = launch_pair_grad(g, q, params, s, flag, st);
+    if (rc) return rc;
+    AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
+    if (N > 0) {
+      image_reduce_kernel<true><<<(unsigned)ceil_div((int64_t)N * 32, 256), 256, 0, st>>>(
+          g, params, s.pg, nullptr, s.R, ad, flag);
+      FM_LAUNCHED(image_reduce_kernel);
+    }
+    if (g.refine_focal && g.n_cameras > 0) {
+      if (g.n_cam_chunks > 0) {
+        cam_chunk_kernel<<<(unsigned)g.n_cam_chunks, kCamBlock, 0, st>>>(g, s.pg, s.cpart, flag);
+        FM_LAUNCHED(cam_chunk_kernel);
+      }
+      cam_final_kernel<true><<<(unsigned)ceil_div(g.n_cameras, 128), 128, 0, st>>>(
+          g, params, s.cpart, nullptr, ad, flag);
+      FM_LAUNCHED(cam_final_kernel);
+    }
+  }
+  return FM_OK;
+}
+
+// --------------------------------------------------------------- graph cache
+struct GraphKey {
+  std::vector<uintptr_t> k;
+  bool operator<(const GraphKey& o) const { return k < o.k; }
+};
+std::mutex g_graph_mu;
+std::map<GraphKey, cudaGraphExec_t> g_graphs;
+
+GraphKey make_key(const fm_pair_graph& g, const fm_quad_model& q, double* params, double* m,
+                  double* v, int n_steps, double b1, double b2, double eps, const EpiScratch& s,
+                  int32_t* flag) {
+  GraphKey key;
+  auto put = [&](const void* p) { key.k.push_back(reinterpret_cast<uintptr_t>(p)); };
+  auto putd = [&](double d) {
+    uintptr_t u = 0;
+    memcpy(&u, &d, sizeof(d));
+    key.k.push_back(u);
+  };
+  key.k.push_back((uintptr_t)g.n_images);
+  key.k.push_back((uintptr_t)g.n_cameras);
+  key.k.push_back((uintptr_t)g.refine_focal);
+  key.k.push_back((uintptr_t)g.n_cam_chunks);
+  key.k.push_back((uintptr_t)g.n_pairs);
+  for (const void* p : {(const void*)g.pair_i, (const void*)g.pair_j, (const void*)g.pair_ci,
+                        (const void*)g.pair_cj, (const void*)g.img_off, (const void*)g.img_inc,
+                        (const void*)g.cam_off, (const void*)g.cam_inc, (const void*)g.cam_chunk_lo,
+                        (const void*)g.cam_chunk_cam, (const void*)g.cam_chunk_off})
+    put(p);
+  key.k.push_back((uintptr_t)q.kind);
+  for (const void* p : {(const void*)q.mom32, (const void*)q.vgrad, (const void*)q.s0,
+                        (const void*)q.ghat0, (const void*)q.w81, (const void*)q.mom64})
+    put(p);
+  put(params);
+  put(m);
+  put(v);
+  key.k.push_back((uintptr_t)n_steps);
+  putd(b1);
+  putd(b2);
+  putd(eps);
+  put(s.R);
+  put(s.sched);
+  put(flag);
+  return key;
+}
+
+}  // namespace
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+size_t fm_epi_scratch_bytes(const fm_pair_graph* g) { return g ? scratch_need(*g) : 0; }
+
+int fm_epi_pair_ghat(const fm_pair_graph* g, const double* params, double* ghat, int32_t* flag,
+                     void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = check_graph(g)) return rc;
+  EpiScratch s;
+  FM_REQUIRE(carve(*g, scratch, scratch_bytes, s), "epipolar scratch too small");
+  cudaStream_t st = as_stream(stream);
+  if (g->n_images > 0) {
+    image_rot_kernel<<<(unsigned)ceil_div(g->n_images, 128), 128, 0, st>>>(params, g->n_images, s.R, flag);
+    FM_LAUNCHED(image_rot_kernel);
+  }
+  if (g->n_pairs > 0) {
+    pair_ghat_kernel<<<(unsigned)ceil_div(g->n_pairs, 128), 128, 0, st>>>(*g, params, s.R, ghat);
+    FM_LAUNCHED(pair_ghat_kernel);
+  }
+  return FM_OK;
+}
+
+int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const double* params,
+                     double scale, double* loss_out, double* grad_out, int32_t* flag, void* scratch,
+                     size_t scratch_bytes, void* stream) {
+  if (int rc = check_graph(g)) return rc;
+  if (int rc = check_quad(q)) return rc;
+  EpiScratch s;
+  FM_REQUIRE(carve(*g, scratch, scratch_bytes, s), "epipolar scratch too small");
+  cudaStream_t st = as_stream(stream);
+  const int N = g->n_images;
+  const int64_t P = g->n_pairs;
+  const size_t n_grad = (size_t)9 * N + (g->refine_focal ? g->n_cameras : 0);
+  set_sched_kernel<<<1, 1, 0, st>>>(s.sched, 0.0, scale);
+  FM_LAUNCHED(set_sched_kernel);
+  if (N > 0) {
+    image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
+    FM_LAUNCHED(image_rot_kernel);
+  }
+  if (P == 0) {
+    FM_CUDA(cudaMemsetAsync(grad_out, 0, n_grad * sizeof(double), st));
+    FM_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(double), st));
+    return FM_OK;
+  }
+  // API semantics: evaluate even if `flag` is already set by the caller
+  if (int rc = launch_pair_grad(*g, *q, params, s, nullptr, st)) return rc;
+  AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, 0};
+  if (N > 0) {
+    image_reduce_kernel<false><<<(unsigned)ceil_div((int64_t)N * 32, 256), 256, 0, st>>>(
+        *g, const_cast<double*>(params), s.pg, grad_out, s.R, none, flag);
+    FM_LAUNCHED(image_reduce_kernel);
+  }
+  if (g->refine_focal && g->n_cameras > 0) {
+    if (g->n_cam_chunks > 0) {
+      cam_chunk_kernel<<<(unsigned)g->n_cam_chunks, kCamBlock, 0, st>>>(*g, s.pg, s.cpart, nullptr);
+      FM_LAUNCHED(cam_chunk_kernel);
+    }
+    cam_final_kernel<false><<<(unsigned)ceil_div(g->n_cameras, 128), 128, 0, st>>>(
+        *g, const_cast<double*>(params), s.cpart, grad_out, none, flag);
+    FM_LAUNCHED(cam_final_kernel);
+  }
+  const int nb = loss_blocks(P);
+  loss_partial_kernel<<<nb, 256, 0, st>>>(s.pg + (size_t)23 * P, P, s.lpart);
+  FM_LAUNCHED(loss_partial_kernel);
+  loss_final_kernel<<<1, 32, 0, st>>>(s.lpart, nb, loss_out);
+  FM_LAUNCHED(loss_final_kernel);
+  return FM_OK;
+}
+
+int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* params,
+                      double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
+                      double beta1, double beta2, double eps, double scale, int32_t* flag,
+                      int32_t use_graph, void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = check_graph(g)) return rc;
+  if (int rc = check_quad(q)) return rc;
+  FM_REQUIRE(flag, "fm_epi_adam_steps needs a device flag word");
+  FM_REQUIRE(n_steps >= 0 && t0 >= 0, "bad step range");
+  EpiScratch s;
+  FM_REQUIRE(carve(*g, scratch, scratch_bytes, s), "epipolar scratch too small");
+  cudaStream_t st = as_stream(stream);
+  if (n_steps == 0) return FM_OK;
+  const int N = g->n_images;
+  if (N > 0) {
+    image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
+    FM_LAUNCHED(image_rot_kernel);
+  }
+  for (int32_t done = 0; done < n_steps;) {
+    const int chunk = std::min<int32_t>(n_steps - done, kMaxSteps);
+    // schedule: lr, 2/Z, and the bias corrections 1 - beta^t computed with the
+    // host pow() exactly as ref/optim.py:34-35 does
+    std::vector<double> sched(2 + 2 * kMaxSteps, 1.0);
+    sched[0] = lr;
+    sched[1] = scale;
+    for (int k = 0; k < chunk; ++k) {
+      const double t = (double)(t0 + done + k + 1);
+      sched[2 + k] = 1.0 - pow(beta1, t);
+      sched[2 + kMaxSteps + k] = 1.0 - pow(beta2, t);
+    }
+    FM_CUDA(cudaMemcpyAsync(s.sched, sched.data(), sched.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, st));
+    if (!use_graph) {
+      if (int rc = enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, st))
+        return rc;
+    } else {
+      GraphKey key = make_key(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag);
+      cudaGraphExec_t exec = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        auto it = g_graphs.find(key);
+        if (it != g_graphs.end()) exec = it->second;
+      }
+      if (!exec) {
+        cudaStream_t cs;
+        FM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        FM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, cs);
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        cudaStreamDestroy(cs);
+        if (rc) {
+          if (graph) cudaGraphDestroy(graph);
+          return rc;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture", __FILE__, __LINE__);
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate", __FILE__, __LINE__);
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        if (g_graphs.size() >= 16) {
+          for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second);
+          g_graphs.clear();
+        }
+        g_graphs[key] = exec;
+      }
+      FM_CUDA(cudaGraphLaunch(exec, st));
+    }
+    done += chunk;
+  }
+  return FM_OK;
+}
+
+void fm_release_cached_graphs(void) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second);
+  g_graphs.clear();
+}
+
+}  // extern "C"

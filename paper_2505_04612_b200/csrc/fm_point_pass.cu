@@ -1,0 +1,637 @@
+// Fused point-pair pass of the epipolar adjustment -- the HBM-bound hot kernel.
+//
+// One sweep over the structure-of-arrays point store replaces, for every
+// active point pair m of image pair n,
+//   current_residuals     r_m = t_m . ghat_n        (ref/epipolar.py:251-255)
+//   pruning               active &= |r_m| <= th     (ref/epipolar.py:280-288)
+//   epipolar_loss("l1")   sum |r_m|                 (ref/epipolar.py:156-160)
+//   precompute_weights    W_n = sum w_m t_m t_m^T   (ref/epipolar.py:46-59)
+// with t_m = flatten(x2 x1^T) never materialised.  W_n has Kronecker structure
+// (t = x2 (x) x1), so it is carried as 36 fourth-order moments
+//   mom[sym(p,q)][sym(r,s)] = sum w x2_p x2_q x1_r x1_s,
+// plus the linearisation terms of the shifted quadratic model
+//   vgrad = sum w r0 t  (= W ghat0),  s0 = sum w r0^2  (= ghat0^T W ghat0),
+// which keep the per-step loss/gradient accurate with fp32 moments even
+// though W is ill-conditioned ("shifted quadratic model").
+//
+// Execution (hot kernel, z == 1): one warp per work item (a <= chunk-slot
+// slice of one image pair; pairs start 4-aligned so each lane moves whole
+// 32-byte (x, y) groups with 128-bit non-allocating loads, software-pipelined
+// one iteration ahead).  Residual, prune decision, s0 and L1 are fp64; the 45
+// moment / gradient accumulators are fp32 and use Blackwell's packed FFMA2
+// (fma.rn.f32x2: two FMAs per issue slot).  Warp totals come from a
+// fixed-order transpose reduction -- no floating-point atomics, so results are
+// bitwise reproducible run to run.
+#include "fm_common.cuh"
+
+namespace fm {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kNumRed = 46;  // 36 moments + 9 vgrad + post-prune count
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float2 f2(float s) { return make_float2(s, s); }
+
+// Fixed-order warp transpose reduction of 48 floats.  Levels 16/8/4/2 halve
+// the per-lane set (24 + 12 + 6 + 3 shuffles), the last level is a butterfly
+// on the remaining 3 values.  Afterwards lane l holds the warp totals of
+// values [base, base+3), base = 24*b4 + 12*b3 + 6*b2 + 3*b1 (b_k = bit k of l);
+// lanes l and l^1 hold the same totals.
+__device__ __forceinline__ void warp_transpose_reduce48(float (&v)[48], int lane) {
+#pragma unroll
+  for (int level = 0; level < 4; ++level) {
+    const int off = 16 >> level;
+    const int half = 24 >> level;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = upper ? v[i] : v[i + half];
+      const float keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 1);
+}
+
+__device__ __forceinline__ int red_base48(int lane) {
+  return 24 * ((lane >> 4) & 1) + 12 * ((lane >> 3) & 1) + 6 * ((lane >> 2) & 1) + 3 * ((lane >> 1) & 1);
+}
+
+// 64-value variant for the generic kernel: lane l ends with values 2l, 2l+1.
+template <typename T>
+__device__ __forceinline__ void warp_transpose_reduce64(T (&v)[64], int lane) {
+#pragma unroll
+  for (int level = 0; level < 5; ++level) {
+    const int off = 16 >> level;
+    const int half = 32 >> level;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const T send = upper ? v[i] : v[i + half];
+      const T keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+struct PartialBufs {
+  void* red;   // [kNumRed][n_items] of the accumulator type
+  double* s0;  // [n_items]
+  double* l1;  // [n_items]
+};
+
+// Hot-kernel accumulator order.  x2 products (rows) and x1 products (cols)
+// are both kept in the order {00, 01, 02, 12, 11, 22} so that pairs
+// (x^2, xy) = x*(x, y), (x, y) and (y^2, 1) are natural float2 registers.
+__device__ __forceinline__ int hot_perm(int k) { return k == 3 ? 4 : (k == 4 ? 3 : k); }
+
+// Canonical output index of hot accumulator slot v (0..45), or -1.
+// 0..35 moments (row-major 6x6 in hot order), 36..44 vgrad pairs, 45 count.
+__device__ __forceinline__ int hot_out_index(int v) {
+  if (v < 36) return hot_perm(v / 6) * 6 + hot_perm(v % 6);
+  switch (v) {  // V0=(v00,v01) V1=(v10,v11) V2=(v20,v21) V3=(v02,v12) v22
+    case 36: return 36 + 0;
+    case 37: return 36 + 1;
+    case 38: return 36 + 3;
+    case 39: return 36 + 4;
+    case 40: return 36 + 6;
+    case 41: return 36 + 7;
+    case 42: return 36 + 2;
+    case 43: return 36 + 5;
+    case 44: return 36 + 8;
+    case 45: return 45;
+    default: return -1;
+  }
+}
+
+__device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialBufs& part, bool single,
+                                          int64_t P, int64_t NI, int n, int64_t item, int k, float val,
+                                          bool lin) {
+  if (!single) {
+    static_cast<float*>(part.red)[k * NI + item] = val;
+    return;
+  }
+  if (k < 36) {
+    out.mom32[k * P + n] = val;
+  } else if (k < 45) {
+    if (lin) out.vgrad[(k - 36) * P + n] = val;
+  } else if (out.n_active) {
+    out.n_active[n] = (int32_t)val;
+  }
+}
+
+// ------------------------------------------------------------------ hot kernel
+// z == 1, fp32 moments.  MODE is a combination of PRUNE / L1 / MOMENTS|IRLS /
+// SKIP_DROPPED.
+template <unsigned MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
+point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
+               const int32_t* __restrict__ prev_active, const fm_pass_out out,
+               const PartialBufs part) {
+  constexpr bool kPrune = MODE & FM_PASS_PRUNE;
+  constexpr bool kL1 = MODE & FM_PASS_L1;
+  constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
+  constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
+
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (item >= s.n_items) return;
+  const int n = s.item_pair[item];
+  const int first = s.pair_item_off[n];
+  const bool single = (s.pair_item_off[n + 1] - first) == 1;
+  const int64_t P = s.n_pairs;
+
+  float2 M2[18];  // moments, row p (x2 product) x column pair q (x1 products)
+  float2 V0, V1, V2, V3;
+  float v22 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 18; ++k) M2[k] = f2(0.f);
+  V0 = V1 = V2 = V3 = f2(0.f);
+  double s0 = 0.0, l1 = 0.0;
+  int cnt = 0;
+
+  const bool skip = kSkip && prev_active[n] == 0;
+  if (!skip) {
+    double G[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) G[k] = ghat[k * P + n];
+    const int64_t base = s.pair_off[n];
+    const int64_t end = base + s.pair_len[n];
+    const int64_t lo = base + (int64_t)(item - first) * s.chunk;
+    const int64_t hi = end < lo + s.chunk ? end : lo + s.chunk;
+
+    int64_t b = lo + 4 * lane;
+    float4 P1a, P1b, P2a, P2b;  // x1 (slots b, b+1), (b+2, b+3); x2 likewise
+    bool have = b < hi;
+    if (have) {
+      P1a = ld_stream4(s.x1 + 2 * b);
+      P1b = ld_stream4(s.x1 + 2 * b + 4);
+      P2a = ld_stream4(s.x2 + 2 * b);
+      P2b = ld_stream4(s.x2 + 2 * b + 4);
+    }
+    while (have) {
+      const float4 c1a = P1a, c1b = P1b, c2a = P2a, c2b = P2b;
+      const int64_t cb = b;
+      b += 128;
+      have = b < hi;
+      if (have) {  // prefetch the next 4 slots while this group computes
+        P1a = ld_stream4(s.x1 + 2 * b);
+        P1b = ld_stream4(s.x1 + 2 * b + 4);
+        P2a = ld_stream4(s.x2 + 2 * b);
+        P2b = ld_stream4(s.x2 + 2 * b + 4);
+      }
+      const int shift = (int)(cb & 31);
+      const unsigned bits = (s.active[cb >> 5] >> shift) & 0xFu;
+      unsigned keep_bits = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4& q1 = k < 2 ? c1a : c1b;
+        const float4& q2 = k < 2 ? c2a : c2b;
+        const float2 X1 = (k & 1) ? make_float2(q1.z, q1.w) : make_float2(q1.x, q1.y);
+        const float2 X2 = (k & 1) ? make_float2(q2.z, q2.w) : make_float2(q2.x, q2.y);
+        const bool act = (cb + k < hi) && ((bits >> k) & 1u);
+        // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
+        const double a = X1.x, bb = X1.y, c = X2.x, d = X2.y;
+        const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
+        const double y1 = fma(G[3], a, fma(G[4], bb, G[5]));
+        const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
+        const double r = fma(c, y0, fma(d, y1, y2));
+        const double ar = fabs(r);
+        const bool keep = kPrune ? (act && ar <= thr) : act;
+        keep_bits |= (unsigned)keep << k;
+        cnt += keep;
+        if (kL1) l1 += act ? ar : 0.0;
+        if (kMom) {
+          // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58)
+          const float w = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
+          const bool big = ar >= 1e-6;
+          // w r0 and w r0^2 without a division: sign(r), |r| unless clamped
+          const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
+          s0 += keep ? (big ? ar : r * r * 1e6) : 0.0;
+          const float2 wX2 = __fmul2_rn(f2(w), X2);  // (w c, w d)
+          const float B[6] = {wX2.x * X2.x, wX2.x * X2.y, wX2.x, wX2.y * X2.y, wX2.y, w};
+          const float2 A0 = __fmul2_rn(f2(X1.x), X1);         // (a^2, a b)
+          const float2 A2 = make_float2(X1.y * X1.y, 1.f);    // (b^2, 1)
+          // hot order rows/cols: {aa|cc, ab|cd, a|c, b|d, bb|dd, 1}
+          const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
+#pragma unroll
+          for (int p = 0; p < 6; ++p) {
+            M2[p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[p * 3 + 0]);
+            M2[p * 3 + 1] = __ffma2_rn(f2(Brow[p]), X1, M2[p * 3 + 1]);
+            M2[p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[p * 3 + 2]);
+          }
+          const float2 wrX2 = __fmul2_rn(f2(wr), X2);  // (wr c, wr d)
+          V0 = __ffma2_rn(f2(wrX2.x), X1, V0);
+          V1 = __ffma2_rn(f2(wrX2.y), X1, V1);
+          V2 = __ffma2_rn(f2(wr), X1, V2);
+          V3 = __fadd2_rn(wrX2, V3);
+          v22 += wr;
+        }
+      }
+      if (kPrune) {
+        const unsigned cleared = bits & ~keep_bits & 0xFu;
+        if (cleared) atomicAnd(&s.active[cb >> 5], ~(cleared << shift));
+      }
+    }
+  }
+
+  // -------------------------------------------------------------- reduce
+  if (kMom) {
+    float v[48];
+#pragma unroll
+    for (int k = 0; k < 18; ++k) {
+      v[2 * k] = M2[k].x;
+      v[2 * k + 1] = M2[k].y;
+    }
+    v[36] = V0.x; v[37] = V0.y; v[38] = V1.x; v[39] = V1.y;
+    v[40] = V2.x; v[41] = V2.y; v[42] = V3.x; v[43] = V3.y;
+    v[44] = v22;
+    v[45] = (float)cnt;
+    v[46] = 0.f;
+    v[47] = 0.f;
+    warp_transpose_reduce48(v, lane);
+    if ((lane & 1) == 0) {
+      const int rb = red_base48(lane);
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        const int k = hot_out_index(rb + h);
+        if (k >= 0) store_red(out, part, single, P, s.n_items, n, item, k, v[h], true);
+      }
+    }
+  } else {
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) store_red(out, part, single, P, s.n_items, n, item, 45, (float)cnt, false);
+  }
+  if (kMom) {
+    s0 = warp_sum(s0);
+    if (lane == 0) {
+      if (single) out.s0[n] = s0;
+      else part.s0[item] = s0;
+    }
+  }
+  if (kL1) {
+    l1 = warp_sum(l1);
+    if (lane == 0) {
+      if (single) {
+        if (out.l1) out.l1[n] = l1;
+      } else {
+        part.l1[item] = l1;
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------------- generic kernel
+// API modes: optional z columns, fp64 moments, caller-given residual weights,
+// residual output, mask-free sweeps.  Plain scalar code; not on the hot loop.
+template <bool HOMOG, bool F64, unsigned MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+point_pass_generic(const fm_point_store s, const double* __restrict__ ghat,
+                   const double* __restrict__ res_in, const double thr,
+                   const int32_t* __restrict__ prev_active, const fm_pass_out out,
+                   const PartialBufs part) {
+  using Acc = typename std::conditional<F64, double, float>::type;
+  constexpr bool kPrune = MODE & FM_PASS_PRUNE;
+  constexpr bool kL1 = MODE & FM_PASS_L1;
+  constexpr bool kMom = MODE & FM_PASS_MOMENTS;
+  constexpr bool kIrls = MODE & FM_PASS_IRLS;
+  constexpr bool kAll = MODE & FM_PASS_ALL_POINTS;
+  constexpr bool kResOut = MODE & FM_PASS_RES_OUT;
+  constexpr bool kResIn = MODE & FM_PASS_RES_IN;
+  constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
+  constexpr bool kNeedR = kPrune || kL1 || kIrls || kResOut;
+  constexpr bool kLin = kMom && kIrls;
+
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (item >= s.n_items) return;
+  const int n = s.item_pair[item];
+  const int first = s.pair_item_off[n];
+  const bool single = (s.pair_item_off[n + 1] - first) == 1;
+  const int64_t P = s.n_pairs;
+
+  Acc mom[36], vg[9];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) mom[k] = Acc(0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) vg[k] = Acc(0);
+  double s0 = 0.0, l1 = 0.0;
+  int cnt = 0;
+
+  if (!(kSkip && prev_active[n] == 0)) {
+    double G[9];
+    if (kNeedR) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = ghat[k * P + n];
+    }
+    const int64_t base = s.pair_off[n];
+    const int64_t end = base + s.pair_len[n];
+    const int64_t lo = base + (int64_t)(item - first) * s.chunk;
+    const int64_t hi = end < lo + s.chunk ? end : lo + s.chunk;
+    for (int64_t cb = lo + 4 * lane; cb < hi; cb += 128) {
+      const int shift = (int)(cb & 31);
+      const unsigned bits = kAll ? 0xFu : ((s.active[cb >> 5] >> shift) & 0xFu);
+      unsigned keep_bits = 0;
+      for (int k = 0; k < 4; ++k) {
+        const int64_t sl = cb + k;
+        const bool valid = sl < hi;
+        const bool act = valid && ((bits >> k) & 1u);
+        if (!valid) continue;
+        const double a = s.x1[2 * sl], bb = s.x1[2 * sl + 1];
+        const double c = s.x2[2 * sl], d = s.x2[2 * sl + 1];
+        const double e = HOMOG ? (double)s.x1z[sl] : 1.0;
+        const double f = HOMOG ? (double)s.x2z[sl] : 1.0;
+        double r = 0.0;
+        if (kNeedR) {
+          const double y0 = fma(G[0], a, fma(G[1], bb, G[2] * e));
+          const double y1 = fma(G[3], a, fma(G[4], bb, G[5] * e));
+          const double y2 = fma(G[6], a, fma(G[7], bb, G[8] * e));
+          r = fma(c, y0, fma(d, y1, f * y2));
+        }
+        const double ar = fabs(r);
+        if (kResOut) out.residual[sl] = ar;
+        const bool keep = kPrune ? (act && ar <= thr) : act;
+        keep_bits |= (unsigned)keep << k;
+        cnt += keep;
+        if (kL1) l1 += act ? ar : 0.0;
+        if (kMom && keep) {
+          double w = 1.0;
+          if (kIrls) w = 1.0 / fmax(ar, 1e-6);
+          else if (kResIn) w = 1.0 / fmax(fabs(res_in[sl]), 1e-6);
+          const double A6[6] = {a * a, a * bb, a * e, bb * bb, bb * e, e * e};
+          const double wc = w * c, wd = w * d, wf = w * f;
+          const double B6[6] = {wc * c, wc * d, wc * f, wd * d, wd * f, wf * f};
+#pragma unroll
+          for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = 0; j < 6; ++j) mom[i * 6 + j] += Acc(B6[i] * A6[j]);
+          if (kLin) {
+            const double wr = w * r;
+            s0 += wr * r;
+            const double x2v[3] = {wr * c, wr * d, wr * f};
+            const double x1v[3] = {a, bb, e};
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+#pragma unroll
+              for (int q = 0; q < 3; ++q) vg[p * 3 + q] += Acc(x2v[p] * x1v[q]);
+          }
+        }
+      }
+      if (kPrune) {
+        const unsigned cleared = bits & ~keep_bits & 0xFu;
+        if (cleared) atomicAnd(&s.active[cb >> 5], ~(cleared << shift));
+      }
+    }
+  }
+
+  if (kMom) {
+    Acc v[64];
+#pragma unroll
+    for (int k = 0; k < 36; ++k) v[k] = mom[k];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[36 + k] = vg[k];
+    v[45] = Acc(cnt);
+#pragma unroll
+    for (int k = 46; k < 64; ++k) v[k] = Acc(0);
+    warp_transpose_reduce64(v, lane);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * lane + h;
+      if (k >= kNumRed) continue;
+      if (!single) {
+        static_cast<Acc*>(part.red)[k * s.n_items + item] = v[h];
+      } else if (k < 36) {
+        if (F64) out.mom64[k * P + n] = (double)v[h];
+        else out.mom32[k * P + n] = (float)v[h];
+      } else if (k < 45) {
+        if (kLin && out.vgrad) out.vgrad[(k - 36) * P + n] = (float)v[h];
+      } else if (out.n_active) {
+        out.n_active[n] = (int32_t)v[h];
+      }
+    }
+  } else {
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) {
+      if (!single) static_cast<Acc*>(part.red)[45 * s.n_items + item] = Acc(cnt);
+      else if (out.n_active) out.n_active[n] = cnt;
+    }
+  }
+  if (kLin) {
+    s0 = warp_sum(s0);
+    if (lane == 0) {
+      if (single) { if (out.s0) out.s0[n] = s0; }
+      else part.s0[item] = s0;
+    }
+  }
+  if (kL1) {
+    l1 = warp_sum(l1);
+    if (lane == 0) {
+      if (single) { if (out.l1) out.l1[n] = l1; }
+      else part.l1[item] = l1;
+    }
+  }
+}
+
+// Sum the partials of pairs split over several work items, in item order.
+template <bool F64, unsigned MODE>
+__global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
+                               const PartialBufs part) {
+  using Acc = typename std::conditional<F64, double, float>::type;
+  constexpr bool kL1 = MODE & FM_PASS_L1;
+  constexpr bool kMom = MODE & FM_PASS_MOMENTS;
+  constexpr bool kLin = kMom && (MODE & FM_PASS_IRLS);
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= s.n_pairs) return;
+  const int i0 = s.pair_item_off[n], i1 = s.pair_item_off[n + 1];
+  if (i1 - i0 <= 1) return;
+  const int64_t P = s.n_pairs, NI = s.n_items;
+  const Acc* red = static_cast<const Acc*>(part.red);
+  for (int k = kMom ? 0 : 45; k < kNumRed; ++k) {
+    Acc acc = 0;
+    for (int i = i0; i < i1; ++i) acc += red[k * NI + i];
+    if (k < 36) {
+      if (F64) out.mom64[k * P + n] = (double)acc;
+      else out.mom32[k * P + n] = (float)acc;
+    } else if (k < 45) {
+      if (kLin && out.vgrad) out.vgrad[(k - 36) * P + n] = (float)acc;
+    } else if (out.n_active) {
+      out.n_active[n] = (int32_t)acc;
+    }
+  }
+  if (kLin && out.s0) {
+    double acc = 0;
+    for (int i = i0; i < i1; ++i) acc += part.s0[i];
+    out.s0[n] = acc;
+  }
+  if (kL1 && out.l1) {
+    double acc = 0;
+    for (int i = i0; i < i1; ++i) acc += part.l1[i];
+    out.l1[n] = acc;
+  }
+}
+
+template <unsigned MODE>
+int launch_hot(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
+               const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
+  const int64_t blocks = ceil_div(s.n_items, kWarpsPerBlock);
+  point_pass_hot<MODE><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, stream>>>(s, ghat, thr, prev_active,
+                                                                            out, part);
+  FM_LAUNCHED(point_pass_hot);
+  if (s.n_items > s.n_pairs) {
+    combine_kernel<false, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part);
+    FM_LAUNCHED(combine_kernel);
+  }
+  return FM_OK;
+}
+
+template <bool HOMOG, bool F64, unsigned MODE>
+int launch_generic(const fm_point_store& s, double thr, const double* ghat, const double* res_in,
+                   const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
+                   cudaStream_t stream) {
+  const int64_t blocks = ceil_div(s.n_items, kWarpsPerBlock);
+  point_pass_generic<HOMOG, F64, MODE><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, stream>>>(
+      s, ghat, res_in, thr, prev_active, out, part);
+  FM_LAUNCHED(point_pass_generic);
+  if (s.n_items > s.n_pairs) {
+    combine_kernel<F64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part);
+    FM_LAUNCHED(combine_kernel);
+  }
+  return FM_OK;
+}
+
+constexpr unsigned kSkipD = FM_PASS_SKIP_DROPPED;
+constexpr unsigned kIrlsM = FM_PASS_MOMENTS | FM_PASS_IRLS;
+
+// Hot combinations (z == 1, fp32 moments): the passes of irls_refine.
+#define FM_HOT_MODES(X)                                  \
+  X(FM_PASS_PRUNE | kIrlsM)                              \
+  X(FM_PASS_PRUNE | kIrlsM | kSkipD)                     \
+  X(FM_PASS_L1 | FM_PASS_PRUNE | kIrlsM)                 \
+  X(FM_PASS_L1 | FM_PASS_PRUNE | kIrlsM | kSkipD)        \
+  X(kIrlsM)                                              \
+  X(kIrlsM | kSkipD)                                     \
+  X(FM_PASS_L1)                                          \
+  X(FM_PASS_L1 | kSkipD)                                 \
+  X(FM_PASS_PRUNE)                                       \
+  X(FM_PASS_PRUNE | kSkipD)
+
+// Generic combinations (API functions, any z, fp32 or fp64 accumulation).
+#define FM_GENERIC_MODES(X)                                          \
+  FM_HOT_MODES(X)                                                    \
+  X(FM_PASS_ALL_POINTS | FM_PASS_RES_OUT)                            \
+  X(FM_PASS_MOMENTS)                                                 \
+  X(FM_PASS_MOMENTS | FM_PASS_ALL_POINTS)                            \
+  X(FM_PASS_MOMENTS | FM_PASS_ALL_POINTS | FM_PASS_RES_IN)           \
+  X(FM_PASS_MOMENTS | FM_PASS_RES_IN)                                \
+  X(FM_PASS_MOMENTS | FM_PASS_L1)
+
+template <bool HOMOG, bool F64>
+int dispatch_generic(unsigned mode, const fm_point_store& s, double thr, const double* ghat,
+                     const double* res_in, const int32_t* prev_active, const fm_pass_out& out,
+                     const PartialBufs& part, cudaStream_t stream) {
+#define FM_CASE(M) \
+  if (mode == (M)) return launch_generic<HOMOG, F64, (M)>(s, thr, ghat, res_in, prev_active, out, part, stream);
+  FM_GENERIC_MODES(FM_CASE)
+#undef FM_CASE
+  return set_error(FM_ERR_INVALID, "unsupported point-pass mode 0x%x", mode);
+}
+
+int dispatch_hot(unsigned mode, const fm_point_store& s, double thr, const double* ghat,
+                 const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
+                 cudaStream_t stream, bool* handled) {
+  *handled = true;
+#define FM_CASE(M) \
+  if (mode == (M)) return launch_hot<(M)>(s, thr, ghat, prev_active, out, part, stream);
+  FM_HOT_MODES(FM_CASE)
+#undef FM_CASE
+  *handled = false;
+  return FM_OK;
+}
+
+}  // namespace
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+size_t fm_point_pass_scratch_bytes(const fm_point_store* store) {
+  if (!store) return 0;
+  const size_t ni = (size_t)store->n_items;
+  return scratch_round(ni * kNumRed * sizeof(double)) + 2 * scratch_round(ni * sizeof(double)) + 256;
+}
+
+int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, const double* ghat,
+                  const double* res_in, const int32_t* prev_active, const fm_pass_out* out,
+                  void* scratch, size_t scratch_bytes, void* stream) {
+  FM_REQUIRE(store && out, "null store/out");
+  const fm_point_store& s = *store;
+  FM_REQUIRE(s.n_pairs >= 0 && s.n_items >= s.n_pairs && s.chunk > 0 && s.chunk % 128 == 0,
+             "bad store geometry (pairs=%lld items=%lld chunk=%lld)", (long long)s.n_pairs,
+             (long long)s.n_items, (long long)s.chunk);
+  FM_REQUIRE(s.n_slots % 128 == 0, "n_slots must be a multiple of 128");
+  if (s.n_pairs == 0) return FM_OK;
+  FM_REQUIRE(s.x1 && s.x2 && s.active && s.pair_off && s.pair_len && s.pair_item_off && s.item_pair,
+             "incomplete point store");
+  FM_REQUIRE(((uintptr_t)s.x1 % 16) == 0 && ((uintptr_t)s.x2 % 16) == 0,
+             "coordinate columns must be 16-byte aligned");
+  const bool homog = s.x1z != nullptr;
+  FM_REQUIRE(homog == (s.x2z != nullptr), "x1z and x2z must both be set or both NULL");
+  const bool f64 = (mode & FM_PASS_F64) != 0;
+  const unsigned m = mode & ~FM_PASS_F64;
+  const bool need_r = m & (FM_PASS_PRUNE | FM_PASS_L1 | FM_PASS_IRLS | FM_PASS_RES_OUT);
+  FM_REQUIRE(!need_r || ghat, "mode 0x%x needs ghat", mode);
+  FM_REQUIRE(!(m & FM_PASS_RES_IN) || res_in, "FM_PASS_RES_IN needs res_in");
+  FM_REQUIRE(!(m & FM_PASS_RES_OUT) || out->residual, "FM_PASS_RES_OUT needs out->residual");
+  FM_REQUIRE(!(m & FM_PASS_SKIP_DROPPED) || prev_active, "SKIP_DROPPED needs prev_active");
+  if (m & FM_PASS_MOMENTS) {
+    FM_REQUIRE(f64 ? out->mom64 != nullptr : out->mom32 != nullptr, "moment output missing");
+    if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
+  }
+  PartialBufs part{nullptr, nullptr, nullptr};
+  if (s.n_items > s.n_pairs) {
+    Scratch sc(scratch, scratch_bytes);
+    part.red = sc.take<double>((size_t)s.n_items * kNumRed);
+    part.s0 = sc.take<double>((size_t)s.n_items);
+    part.l1 = sc.take<double>((size_t)s.n_items);
+    FM_REQUIRE(scratch && sc.ok(), "point-pass scratch too small (%zu < %zu)", scratch_bytes, sc.used);
+  }
+  cudaStream_t st = as_stream(stream);
+  if (!homog && !f64) {
+    bool handled = false;
+    const int rc = dispatch_hot(m, s, threshold, ghat, prev_active, *out, part, st, &handled);
+    if (handled) return rc;
+  }
+  if (homog) {
+    return f64 ? dispatch_generic<true, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
+               : dispatch_generic<true, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+  }
+  return f64 ? dispatch_generic<false, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
+             : dispatch_generic<false, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+"""Device-resident data layouts of the hot path and their (bit-exact) builders.
+
+* :class:`PointPairStore` -- the per-point data of a list of ``EpipolarPair``
+  (ref/epipolar.py:19-36) re-laid out as a structure of arrays in HBM: fp32
+  ``(x, y)`` columns for each image side, a 1-bit active mask, image pairs
+  sorted by ``(i, j)`` (stable, so duplicates keep caller order), each pair
+  starting on a 4-slot boundary.  ``terms`` (72 B/point in the reference) is
+  never stored: the kernels rebuild ``flatten(x2 x1^T)`` in registers.
+* :class:`PairGraph` -- image-pair -> dense-image / camera indices plus the
+  incidence lists that make per-image and per-camera gradient sums
+  deterministic gathers (ref/epipolar.py:163-169 remap, :219-224 scatter).
+* :class:`DirGraphDevice` -- ``DirectionGraph`` (ref/translation.py:104-109)
+  plus its node incidence list.
+
+All index bookkeeping is integer numpy (exact); the float payload is uploaded
+once and stays on the device.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+CHUNK = 8192          # slots per work item (multiple of 128)
+CAM_CHUNK = 4096      # incidences per camera-reduction chunk
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _dev(a, device):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device, non_blocking=False)
+
+
+def pair_order(i, j):
+    """Stable (i, j) order of image pairs (ref/tracks.py:104 sorts this way)."""
+    i = np.asarray(i, dtype=np.int64)
+    j = np.asarray(j, dtype=np.int64)
+    return np.lexsort((j, i)).astype(np.int64)
+
+
+def slot_layout(lengths, chunk=CHUNK):
+    """4-aligned slot offsets and work items for per-pair point counts.
+
+    Returns (pair_off [P+1] int64, n_slots, pair_item_off [P+1] int32,
+    item_pair [n_items] int32).
+    """
+    lengths = np.asarray(lengths, dtype=np.int64)
+    P = len(lengths)
+    padded = (lengths + 3) // 4 * 4
+    pair_off = np.zeros(P + 1, dtype=np.int64)
+    np.cumsum(padded, out=pair_off[1:])
+    n_slots = int((pair_off[-1] + 127) // 128 * 128)
+    n_slots = max(n_slots, 128)
+    items = np.maximum(1, (lengths + chunk - 1) // chunk)
+    pair_item_off = np.zeros(P + 1, dtype=np.int64)
+    np.cumsum(items, out=pair_item_off[1:])
+    item_pair = np.repeat(np.arange(P, dtype=np.int64), items)
+    if pair_item_off[-1] >= 2**31:
+        raise ValueError("too many work items")
+    return pair_off, n_slots, _i32(pair_item_off), _i32(item_pair)
+
+
+class PointPairStore:
+    """SoA point-pair store on one device.
+
+    ``order[k]`` is the caller index of the k-th stored pair; ``rank`` is its
+    inverse.  ``point_slot`` maps every caller point (pairs in caller order,
+    points in pair order) to its slot.
+    """
+
+    def __init__(self, x1, x2, lengths, pair_i, pair_j, active=None, device=None,
+                 chunk=CHUNK, order=None):
+        """x1, x2: (Z, 2) or (Z, 3) float arrays of all points, pairs in caller
+        order; lengths: points per pair (caller order)."""
+        device = device or N.require_cuda()
+        lengths = np.asarray(lengths, dtype=np.int64)
+        P = len(lengths)
+        self.device = device
+        self.n_pairs = P
+        self.chunk = chunk
+        if order is None:
+            order = pair_order(pair_i, pair_j)
+        self.order = np.asarray(order, dtype=np.int64)
+        self.rank = np.empty(P, dtype=np.int64)
+        self.rank[self.order] = np.arange(P)
+        self.len_caller = lengths
+        s_len = lengths[self.order]
+        pair_off, n_slots, pair_item_off, item_pair = slot_layout(s_len, chunk)
+        self.pair_off = pair_off
+        self.n_slots = n_slots
+        self.n_items = len(item_pair)
+        self.n_points = int(lengths.sum())
+        # slot of every caller point
+        caller_start = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(lengths, out=caller_start[1:])
+        rank_of_point = np.repeat(self.rank, lengths)
+        within = np.arange(self.n_points, dtype=np.int64) - np.repeat(caller_start[:-1], lengths)
+        self.point_slot = pair_off[:-1][rank_of_point] + within
+        self.caller_start = caller_start
+
+        x1 = np.asarray(x1)
+        x2 = np.asarray(x2)
+        homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
+        self.homogeneous = bool(homog)
+        c1 = np.zeros((n_slots, 2), dtype=np.float32)
+        c2 = np.zeros((n_slots, 2), dtype=np.float32)
+        c1[self.point_slot] = x1[:, :2]
+        c2[self.point_slot] = x2[:, :2]
+        self.x1 = _dev(c1, device)
+        self.x2 = _dev(c2, device)
+        if homog:
+            z1 = np.zeros(n_slots, dtype=np.float32)
+            z2 = np.zeros(n_slots, dtype=np.float32)
+            z1[self.point_slot] = x1[:, 2]
+            z2[self.point_slot] = x2[:, 2]
+            self.x1z = _dev(z1, device)
+            self.x2z = _dev(z2, device)
+        else:
+            self.x1z = self.x2z = None
+        bits = np.zeros(n_slots, dtype=bool)
+        bits[self.point_slot] = True if active is None else np.asarray(active, dtype=bool)
+        self.active = _dev(np.packbits(bits, bitorder="little").view(np.int32), device)
+        self.pair_off_d = _dev(pair_off, device)
+        self.pair_len_d = _dev(_i32(s_len), device)
+        self.pair_item_off_d = _dev(pair_item_off, device)
+        self.item_pair_d = _dev(item_pair, device)
+        self._struct = None
+
+    # ---------------------------------------------------------------- ctypes
+    def struct(self):
+        if self._struct is None:
+            self._struct = N.PointStore(
+                n_pairs=self.n_pairs, n_slots=self.n_slots, n_items=self.n_items,
+                chunk=self.chunk,
+                pair_off=self.pair_off_d.data_ptr(), pair_len=self.pair_len_d.data_ptr(),
+                pair_item_off=self.pair_item_off_d.data_ptr(),
+                item_pair=self.item_pair_d.data_ptr(),
+                x1=self.x1.data_ptr(), x2=self.x2.data_ptr(),
+                x1z=self.x1z.data_ptr() if self.x1z is not None else None,
+                x2z=self.x2z.data_ptr() if self.x2z is not None else None,
+                active=self.active.data_ptr())
+        return self._struct
+
+    def scratch(self):
+        nbytes = N.lib().fm_point_pass_scratch_bytes(ctypes.byref(self.struct()))
+        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+
+    # ------------------------------------------------------------- masks
+    def active_bits(self):
+        """Active flag of every slot (device bool tensor)."""
+        words = self.active.view(torch.int32)
+        shifts = torch.arange(32, device=self.device, dtype=torch.int32)
+        return ((words.unsqueeze(1) >> shifts) & 1).reshape(-1).bool()
+
+    def caller_masks(self):
+        """Active mask of every caller point, host bool array (caller order)."""
+        bits = self.active_bits()
+        slot = torch.from_numpy(self.point_slot).to(self.device)
+        return bits[slot].cpu().numpy()
+
+    def write_back(self, pairs):
+        """In-place update of each pair's ``active`` array (ref/epipolar.py:283)."""
+        masks = self.caller_masks()
+        for k, p in enumerate(pairs):
+            seg = masks[self.caller_start[k]:self.caller_start[k + 1]]
+            if isinstance(p.active, np.ndarray) and p.active.dtype == bool and p.active.shape == seg.shape:
+                p.active[...] = seg
+            else:
+                p.active = seg.copy()
+
+    def to_stored(self, per_pair_caller):
+        return np.asarray(per_pair_caller)[self.order]
+
+    @classmethod
+    def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False):
+        """Build from EpipolarPair-like objects (reference or ours)."""
+        lengths = np.array([len(p.x1) for p in pairs], dtype=np.int64)
+        if len(pairs):
+            x1 = np.concatenate([np.asarray(p.x1, dtype=np.float64).reshape(-1, 3) for p in pairs])
+            x2 = np.concatenate([np.asarray(p.x2, dtype=np.float64).reshape(-1, 3) for p in pairs])
+            act = None if all_active else np.concatenate(
+                [np.asarray(p.active, dtype=bool).reshape(-1) for p in pairs])
+        else:
+            x1 = np.zeros((0, 3))
+            x2 = np.zeros((0, 3))
+            act = None
+        i = np.array([p.i for p in pairs], dtype=np.int64)
+        j = np.array([p.j for p in pairs], dtype=np.int64)
+        return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk)
+
+
+def csr(keys, n_keys, payload):
+    """Stable CSR of payload grouped by key (keys in [0, n_keys))."""
+    keys = np.asarray(keys, dtype=np.int64)
+    order = np.lexsort((np.asarray(payload, dtype=np.int64), keys))
+    off = np.zeros(n_keys + 1, dtype=np.int64)
+    np.cumsum(np.bincount(keys, minlength=n_keys), out=off[1:])
+    return _i32(off), _i32(np.asarray(payload, dtype=np.int64)[order])
+
+
+class PairGraph:
+    """Image-pair graph of the adjustment on one device (pairs in store order)."""
+
+    def __init__(self, idx_i, idx_j, cam_i, cam_j, n_images, n_cameras, refine_focal,
+                 device=None):
+        device = device or N.require_cuda()
+        self.device = device
+        idx_i = np.asarray(idx_i, dtype=np.int64)
+        idx_j = np.asarray(idx_j, dtype=np.int64)
+        cam_i = np.asarray(cam_i, dtype=np.int64)
+        cam_j = np.asarray(cam_j, dtype=np.int64)
+        P = len(idx_i)
+        self.n_pairs = P
+        self.n_images = int(n_images)
+        self.n_cameras = int(n_cameras)
+        self.refine_focal = bool(refine_focal)
+        if self.refine_focal and P and (min(cam_i.min(), cam_j.min()) < 0 or
+                                        max(cam_i.max(), cam_j.max()) >= n_cameras):
+            raise IndexError("camera id out of range of log_focal")
+        inc = np.concatenate([np.arange(P) * 2, np.arange(P) * 2 + 1])
+        self.img_off, self.img_inc = csr(np.concatenate([idx_i, idx_j]), self.n_images, inc)
+        if self.refine_focal:
+            self.cam_off, self.cam_inc = csr(np.concatenate([cam_i, cam_j]), self.n_cameras, inc)
+            lo, cam, coff = [], [], [0]
+            for c in range(self.n_cameras):
+                a, b = int(self.cam_off[c]), int(self.cam_off[c + 1])
+                for s in range(a, b, CAM_CHUNK):
+                    lo.append(s)
+                    cam.append(c)
+                coff.append(len(lo))
+            lo.append(int(self.cam_off[-1]))
+            self.cam_chunk_lo = _i32(lo)
+            self.cam_chunk_cam = _i32(cam if cam else [0])
+            self.cam_chunk_off = _i32(coff)
+        else:
+            self.cam_off = _i32(np.zeros(max(self.n_cameras, 0) + 1))
+            self.cam_inc = _i32([0])
+            self.cam_chunk_lo = _i32([0])
+            self.cam_chunk_cam = _i32([0])
+            self.cam_chunk_off = _i32(np.zeros(max(self.n_cameras, 0) + 1))
+        self.n_cam_chunks = len(self.cam_chunk_lo) - 1
+        host = {"pair_i": _i32(idx_i), "pair_j": _i32(idx_j), "pair_ci": _i32(cam_i),
+                "pair_cj": _i32(cam_j), "img_off": self.img_off, "img_inc": self.img_inc,
+                "cam_off": self.cam_off, "cam_inc": self.cam_inc,
+                "cam_chunk_lo": self.cam_chunk_lo, "cam_chunk_cam": self.cam_chunk_cam,
+                "cam_chunk_off": self.cam_chunk_off}
+        self.t = {k: _dev(v if len(v) else _i32([0]), device) for k, v in host.items()}
+        self._struct = None
+        self.n_params = 9 * self.n_images + (self.n_cameras if self.refine_focal else 0)
+
+    def struct(self):
+        if self._struct is None:
+            t = self.t
+            self._struct = N.PairGraph(
+                n_images=self.n_images, n_cameras=self.n_cameras,
+                refine_focal=int(self.refine_focal), n_cam_chunks=self.n_cam_chunks,
+                n_pairs=self.n_pairs,
+                **{k: t[k].data_ptr() for k in ("pair_i", "pair_j", "pair_ci", "pair_cj",
+                                                 "img_off", "img_inc", "cam_off", "cam_inc",
+                                                 "cam_chunk_lo", "cam_chunk_cam",
+                                                 "cam_chunk_off")})
+        return self._struct
+
+    def scratch(self):
+        nbytes = N.lib().fm_epi_scratch_bytes(ctypes.byref(self.struct()))
+        return torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+
+
+class DirGraphDevice:
+    """DirectionGraph on one device with its node incidence list."""
+
+    def __init__(self, graph, device=None):
+        device = device or N.require_cuda()
+        self.device = device
+        ei = np.asarray(graph.edges_i, dtype=np.int64)
+        ej = np.asarray(graph.edges_j, dtype=np.int64)
+        m = len(ei)
+        self.n = int(graph.n)
+        self.m = m
+        if m and (min(ei.min(), ej.min()) < 0 or max(ei.max(), ej.max()) >= self.n):
+            raise IndexError("edge endpoint out of range")
+        inc = np.concatenate([np.arange(m) * 2, np.arange(m) * 2 + 1])
+        self.node_off, self.node_inc = csr(np.concatenate([ei, ej]), self.n, inc)
+        self.ei = _dev(_i32(ei), device)
+        self.ej = _dev(_i32(ej), device)
+        self.dirs = _dev(np.asarray(graph.directions, dtype=np.float64).reshape(m, 3), device)
+        self.off_d = _dev(self.node_off, device)
+        self.inc_d = _dev(self.node_inc, device)
+        self._struct = N.DirGraph(n_nodes=self.n, n_edges=m, edge_i=self.ei.data_ptr(),
+                                  edge_j=self.ej.data_ptr(), dirs=self.dirs.data_ptr(),
+                                  node_off=self.off_d.data_ptr(), node_inc=self.inc_d.data_ptr())
+
+    def struct(self):
+        return self._struct
+
+    def scratch(self, runs):
+        nbytes = N.lib().fm_tr_scratch_bytes(self.n, self.m, runs)
+        return torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)

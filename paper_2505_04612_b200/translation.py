@@ -1,0 +1,171 @@
+"""Drop-in for the global-alignment half of ``fastmap.translation``
+(ref/translation.py:98-186) on the B200.
+
+``translation_loss_and_grad`` -> ``fm_tr_loss_grad`` (behind the
+``TranslationL1Loss`` autograd function); ``align_centers`` ->
+``fm_tr_align`` (fused loss + gradient + Adam per step, CUDA-graph replay);
+``multi_init_align`` runs all ``translation_inits`` random starts in
+lock-step as one batched descent (one read of every edge serves all runs),
+merges them on the device (``fm_tr_merge``) and finishes with the final
+descent.  The random starts are drawn with the reference's own seeded numpy
+generator, so run k starts from bit-identical centres.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .store import DirGraphDevice
+
+_NORM_EPS = 1e-8
+
+
+def world_direction(t_ij, R_j):
+    """Unit vector from camera center i to j in world coordinates
+    (ref/translation.py:98-101; input construction helper)."""
+    d = -np.asarray(R_j).T @ np.asarray(t_ij)
+    return d / np.linalg.norm(d)
+
+
+@dataclass
+class DirectionGraph:
+    n: int  # number of registered nodes (dense indices)
+    edges_i: np.ndarray  # (m,)
+    edges_j: np.ndarray  # (m,)
+    directions: np.ndarray  # (m, 3) unit o^{i->j}
+
+
+_GRAPH_CACHE = {}
+
+
+def device_graph(graph):
+    """Upload (and memoise per graph object) the direction graph."""
+    key = id(graph)
+    hit = _GRAPH_CACHE.get(key)
+    if hit is not None and hit[0] is graph:
+        return hit[1]
+    dg = DirGraphDevice(graph)
+    if len(_GRAPH_CACHE) > 8:
+        _GRAPH_CACHE.clear()
+    _GRAPH_CACHE[key] = (graph, dg)
+    return dg
+
+
+class TranslationL1Loss(torch.autograd.Function):
+    """Mean per-edge L1 direction loss of B runs; forward and backward from
+    one fm_tr_loss_grad call.  centers: (n, B, 3) fp64 device tensor."""
+
+    @staticmethod
+    def forward(ctx, centers, dg):
+        B = centers.shape[1]
+        loss = torch.empty(B, dtype=torch.float64, device=centers.device)
+        grad = torch.empty_like(centers)
+        scratch = dg.scratch(B)
+        N.check(N.lib().fm_tr_loss_grad(ctypes.byref(dg.struct()), N.ptr(centers.detach()), B,
+                                        N.ptr(loss), N.ptr(grad), N.ptr(scratch), scratch.numel(),
+                                        N.stream_handle()))
+        ctx.save_for_backward(grad)
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (grad,) = ctx.saved_tensors
+        return grad * grad_out.view(1, -1, 1), None
+
+
+def translation_loss_and_grad(centers, graph):
+    """Mean per-edge L1 direction loss and its gradient w.r.t. centers
+    (ref/translation.py:112-125)."""
+    dg = device_graph(graph)
+    c = np.asarray(centers, dtype=np.float64)
+    t = torch.as_tensor(np.ascontiguousarray(c.reshape(graph.n, 1, 3)), device=dg.device)
+    t.requires_grad_(True)
+    loss = TranslationL1Loss.apply(t, dg)
+    loss.sum().backward()
+    return float(loss[0].item()), t.grad.reshape(c.shape).cpu().numpy()
+
+
+def canonicalize(centers):
+    """Centroid to the origin, unit mean norm (ref/translation.py:128-134)."""
+    device = N.require_cuda()
+    c = np.asarray(centers, dtype=np.float64)
+    t = torch.as_tensor(np.ascontiguousarray(c.reshape(-1, 1, 3)).copy(), device=device)
+    N.check(N.lib().fm_tr_canonicalize(N.ptr(t), t.shape[0], 1, None, 0, N.stream_handle()))
+    return t.reshape(c.shape).cpu().numpy()
+
+
+def _align(dg, init, cfg, steps):
+    """Batched descent of B runs from init (n, B, 3); returns (centers, loss[B])."""
+    B = init.shape[1]
+    if isinstance(init, torch.Tensor):
+        c = init.to(dg.device, torch.float64).contiguous().clone()
+    else:
+        c = torch.as_tensor(np.ascontiguousarray(init, dtype=np.float64), device=dg.device).clone()
+    if steps == 0:
+        return c, np.full(B, np.inf)
+    loss = torch.empty(B, dtype=torch.float64, device=dg.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=dg.device)
+    scratch = dg.scratch(B)
+    N.check(N.lib().fm_tr_align(ctypes.byref(dg.struct()), N.ptr(c), B, int(steps),
+                                cfg.translation_lr, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
+                                N.ptr(loss), N.ptr(flag), N.ptr(scratch), scratch.numel(),
+                                N.stream_handle()))
+    N.raise_flag(flag.item(), "translation")
+    return c, loss.cpu().numpy()
+
+
+def align_centers(graph, cfg, seed=0, init=None, steps=None):
+    """Adam descent of the L1 direction loss from a random (or given)
+    initialization (ref/translation.py:137-152).  Returns (centers, loss)."""
+    rng = np.random.default_rng(seed)
+    if init is None:
+        init = rng.standard_normal((graph.n, 3))
+    dg = device_graph(graph)
+    n_steps = steps if steps is not None else cfg.translation_steps
+    c, loss = _align(dg, np.asarray(init, dtype=np.float64).reshape(graph.n, 1, 3), cfg, n_steps)
+    return c.reshape(graph.n, 3).cpu().numpy(), float(loss[0])
+
+
+def per_node_residuals(centers, graph):
+    """Mean incident-edge L1 residual per node (ref/translation.py:155-166)."""
+    dg = device_graph(graph)
+    c = torch.as_tensor(np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(graph.n, 1, 3)),
+                        device=dg.device)
+    out = torch.empty(graph.n, dtype=torch.float64, device=dg.device)
+    N.check(N.lib().fm_tr_node_residuals(ctypes.byref(dg.struct()), N.ptr(c), 1, N.ptr(out),
+                                         N.stream_handle()))
+    return out.cpu().numpy()
+
+
+def multi_init_inits(n, inits, seed):
+    """The reference's random starts of runs seed..seed+inits-1, node-major
+    (n, inits, 3) (ref/translation.py:140-142, :179-180)."""
+    return np.stack([np.random.default_rng(seed + k).standard_normal((n, 3))
+                     for k in range(inits)], axis=1)
+
+
+def multi_init_align(graph, cfg, seed=0, return_choice=False):
+    """Independent random-seed runs merged per image, then a final descent
+    (ref/translation.py:169-186).  All runs execute as one batched descent."""
+    if cfg.translation_inits == 1:
+        return align_centers(graph, cfg, seed=seed)
+    dg = device_graph(graph)
+    B = cfg.translation_inits
+    runs, _ = _align(dg, multi_init_inits(graph.n, B, seed), cfg, cfg.translation_steps)
+    merged = torch.empty((graph.n, 1, 3), dtype=torch.float64, device=dg.device)
+    choice = torch.empty(graph.n, dtype=torch.int32, device=dg.device)
+    scratch = dg.scratch(B)
+    N.check(N.lib().fm_tr_merge(ctypes.byref(dg.struct()), N.ptr(runs), B, N.ptr(merged),
+                                N.ptr(choice), N.ptr(scratch), scratch.numel(), N.stream_handle()))
+    c, loss = _align(dg, merged, cfg, cfg.translation_steps)
+    out = (c.reshape(graph.n, 3).cpu().numpy(), float(loss[0]))
+    if return_choice:
+        return out + (choice.cpu().numpy(),)
+    return out
+
+
+__all__ = ["world_direction", "DirectionGraph", "translation_loss_and_grad", "canonicalize",
+           "align_centers", "per_node_residuals", "multi_init_align", "TranslationL1Loss"]
