@@ -1,0 +1,434 @@
+"""Benchmark of the FastMap B200 hot path (BASELINE.json metric).
+
+A step = one fused point-pair pass (residual + prune + L1 + IRLS-weighted W
+moments + linearisation gradient terms: the heaviest pass of irls_refine,
+ref/epipolar.py:280-310) over the whole synthetic workload, plus the scalar
+all-reduce (Z, L1) that irls_refine needs per pass when N > 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c5]
+  python bench.py --impl reference ...     # CPU oracle port on the host cores
+
+Workload at N=1: BASELINE configs[1] (C2: 500 images, 25,000 image pairs,
+10,000,000 point pairs), generated on the device.  N>1 (torchrun, one rank
+per GPU, NCCL): every rank holds its own C2-sized shard (weak scaling); the
+value is all ranks' point pairs / max-over-ranks device time.
+
+The L2 (126 MB) is flushed between timed steps (256 MB write, outside the
+events); inputs (161 MB) are larger than L2 anyway.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "point-pair residual+grad evals/sec (fraction of HBM roofline); SfM optimize time s"
+UNIT = "point pairs/s"
+BYTES_PER_POINT = 16.0 + 1.0 / 8.0      # fp32 (x1, y1, x2, y2) + 1 mask bit (read)
+BYTES_PER_PAIR = 72.0 + 36 * 8 + 8 + 4 + 8 + 4 + 4 + 4 + 4  # ghat in, fp64 W moments/L1/count out, indices
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return world, rank, local
+
+
+# ------------------------------------------------------------ reference arm
+def _ref_worker(args):
+    x1, x2, lengths, ghat, th = args
+    from oracle import fastmap_oracle as O
+    flat = O.FlatPairs(np.column_stack([x1, np.ones(len(x1))]),
+                       np.column_stack([x2, np.ones(len(x2))]), lengths)
+    out = O.point_pass(flat, ghat, threshold=th)
+    return float(out["l1"].sum())
+
+
+def cpu_sample(spec, n_pairs_sample):
+    """A bounded prefix of the workload on the host (fp32 coordinates)."""
+    import torch
+    from paper_2505_04612_b200 import scenes
+    device = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    sc = scenes.generate(spec, device, pair_slice=slice(0, n_pairs_sample))
+    ids = np.arange(spec.n_images)
+    params = scenes.initial_params(sc, ids, refine_focal=True)
+    from oracle import fastmap_oracle as O
+    ij = sc["ij"]
+    gh = O.pair_forward(params, spec.n_images, ij[:, 0], ij[:, 1], np.zeros(len(ij), int),
+                        np.zeros(len(ij), int), True)["ghat"]
+    return (sc["x1"].cpu().numpy().astype(np.float64), sc["x2"].cpu().numpy().astype(np.float64),
+            sc["lengths"], gh)
+
+
+def time_cpu_pass(spec, n_pairs_sample, procs, repeats=1):
+    """Oracle port of the fused pass on a sample, sharded over `procs`
+    processes; returns (point pairs/s, seconds, points)."""
+    import multiprocessing as mp
+    x1, x2, lengths, gh = cpu_sample(spec, n_pairs_sample)
+    P = len(lengths)
+    bounds = np.linspace(0, P, procs + 1).astype(int)
+    start = np.concatenate([[0], np.cumsum(lengths)])
+    jobs = [(x1[start[a]:start[b]], x2[start[a]:start[b]], lengths[a:b], gh[a:b], 0.01)
+            for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    ctx = mp.get_context("fork")
+    best = None
+    with ctx.Pool(len(jobs)) as pool:
+        pool.map(_ref_worker, jobs[:1])  # warm the workers
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, jobs)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+    Z = int(lengths.sum())
+    return Z / best, best, Z
+
+
+def run_reference(args, spec, world, rank):
+    if rank != 0:
+        return
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    procs = len(os.sched_getaffinity(0))
+    n_pairs_sample = min(spec.n_pairs, max(procs * 10, int(1.5e6 // spec.points_per_pair)))
+    vals = []
+    import multiprocessing as mp
+    x1, x2, lengths, gh = cpu_sample(spec, n_pairs_sample)
+    P = len(lengths)
+    bounds = np.linspace(0, P, procs + 1).astype(int)
+    start = np.concatenate([[0], np.cumsum(lengths)])
+    jobs = [(x1[start[a]:start[b]], x2[start[a]:start[b]], lengths[a:b], gh[a:b], 0.01)
+            for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    Z = int(lengths.sum())
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, jobs)
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                vals.append(dt)
+    t = float(np.mean(vals))
+    v = Z / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config.upper()} prefix sample", "pass": "L1+prune+IRLS W"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": f"{Z} point pairs ({P} image pairs) of {args.config.upper()} "
+                                       f"per step, numpy oracle (oracle/fastmap_oracle.py) "
+                                       f"point_pass sharded over {procs} processes"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args, spec, world, rank, local):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_04612_b200 import _native as N
+    from paper_2505_04612_b200 import epipolar as E
+    from paper_2505_04612_b200 import scenes
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    spec_r = scenes.SceneSpec(**{**spec.__dict__, "seed": spec.seed + rank})
+    scene = scenes.generate(spec_r, device)
+    store = scenes.device_store(scene, device)
+    graph, ids = scenes.device_graph(scene, device)
+    params = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
+    stream = torch.cuda.Stream(device)
+    Z = store.n_points
+    P = store.n_pairs
+    lib = N.lib()
+    with torch.cuda.stream(stream):
+        eng = E.IrlsEngine(store, graph, params, args.cfg)
+        eng._ghat()
+    mode = N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    scal = torch.zeros(2, dtype=torch.float64, device=device)
+    sync_bytes = 0
+
+    def one_pass():
+        eng.point_pass(mode, 0.01, 0, 0)
+
+    def reduce_scalars():
+        scal[0] = eng.buf.l1[:P].sum()
+        scal[1] = eng.buf.n_active[0][:P].sum().double()
+        if world > 1:
+            dist.all_reduce(scal)
+
+    # first pass sets the counts used by SKIP_DROPPED and the steady-state mask
+    with torch.cuda.stream(stream):
+        eng.buf.n_active[0].fill_(1)
+        one_pass()
+    torch.cuda.synchronize()
+
+    def timed(k_steps, with_flush=True):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
+        with torch.cuda.stream(stream):
+            for k in range(k_steps):
+                if with_flush:
+                    flush.fill_(k & 0xFF)
+                starts[k].record(stream)
+                one_pass()
+                ends[k].record(stream)
+                reduce_scalars()
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+    timed(args.warmup)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = timed(args.steps)
+    ms_step = float(np.mean(ms))
+    t_max = torch.tensor([ms_step], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_step = float(t_max.item())
+    value = world * Z / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (the pass) from the same events
+    bytes_launch = BYTES_PER_POINT * Z + BYTES_PER_PAIR * P
+    hbm, hbm_kind = peaks()
+    achieved = bytes_launch / (ms_step * 1e-3) / 1e9
+
+    # --------------------------------------------------------------- e2e
+    # through the C ABI with HOST buffers: pinned host store columns -> H2D,
+    # pass, per-pair results -> D2H, every step.
+    h_x1 = store.x1.cpu().pin_memory()
+    h_x2 = store.x2.cpu().pin_memory()
+    h_act = store.active.cpu().pin_memory()
+    outs = eng.buf.outputs()
+    h_outs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    h2d = sum(t.numel() * t.element_size() for t in (h_x1, h_x2, h_act))
+    d2h = sum(t.numel() * t.element_size() for t in h_outs)
+
+    def e2e_steps(k_steps):
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            s0.record(stream)
+            for _ in range(k_steps):
+                store.x1.copy_(h_x1, non_blocking=True)
+                store.x2.copy_(h_x2, non_blocking=True)
+                store.active.copy_(h_act, non_blocking=True)
+                one_pass()
+                for h, o in zip(h_outs, outs):
+                    h.copy_(o, non_blocking=True)
+            s1.record(stream)
+        torch.cuda.synchronize()
+        return s0.elapsed_time(s1) / k_steps
+
+    e2e_steps(2)
+    e2e_ms = e2e_steps(max(3, min(args.steps, 10)))
+    t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t_e2e.item())
+
+    # ------------------------------------------- SfM optimize time (rank 0)
+    extra = {}
+    if rank == 0 and not args.skip_optimize:
+        params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
+        store.reset_active()
+        with torch.cuda.stream(stream):
+            eng2 = E.IrlsEngine(store, graph, params0, args.cfg)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            l1h = eng2.run()
+            torch.cuda.synchronize()
+            t_irls = time.perf_counter() - t0
+        extra["sfm_optimize"] = {"irls_refine_s": t_irls, "l1_history": l1h,
+                                 "dropped_pairs": eng2.dropped, "active_pairs": eng2.kept,
+                                 "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"}
+        extra["sfm_optimize"].update(translation_bench(device, stream))
+
+    # ---------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        procs = 1
+        try:
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(1)
+        except Exception:
+            pass
+        n_s = max(64, int(1.0e6 // spec.points_per_pair))
+        v_cpu, t_cpu, z_cpu = time_cpu_pass(spec, n_s, procs)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": procs, "kind": "port",
+               "sample": f"{z_cpu} point pairs ({n_s} image pairs) prefix of {args.config.upper()}, "
+                         f"oracle/fastmap_oracle.py point_pass, single process, {t_cpu:.2f} s"}
+
+    launches = args.steps * (1 + (1 if store.n_items > store.n_pairs else 0))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 coords+moments / f64 residual",
+            "data": "synthetic (device-generated ring scene, random-perturbed poses)",
+            "config": {"workload": f"{args.config.upper()}: {spec.n_images} images, {P} image pairs, "
+                                   f"{Z} point pairs per GPU (band {spec.band}, {spec.points_per_pair}"
+                                   f" pts/pair)",
+                       "pass": "fused L1 + prune + IRLS W moments + linearisation gradient",
+                       "l2": "flushed between steps (256 MB write) and inputs > L2",
+                       "parallelism": f"dp{world} (point pairs sharded by image pair)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "peak_kind": hbm_kind,
+                         "algorithmic_bytes_per_launch": bytes_launch},
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * Z / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            **extra,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def translation_bench(device, stream):
+    """BASELINE configs[2]: 16 batched inits, 2k nodes / 200k edges, 6000
+    steps each + merge + final 6000-step run (ref/translation.py:169-186)."""
+    import torch
+    from paper_2505_04612_b200 import translation as T
+    rng = np.random.default_rng(0)
+    n, m = 2000, 200_000
+    c = rng.normal(size=(n, 3))
+    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], axis=1)
+    extra = set()
+    while len(extra) < m - n:
+        a = rng.integers(0, n, size=(m, 2))
+        for i, j in a:
+            if i != j:
+                extra.add((min(i, j), max(i, j)))
+            if len(extra) >= m - n:
+                break
+    e = np.concatenate([np.sort(ring, axis=1), np.array(sorted(extra))])
+    d = c[e[:, 1]] - c[e[:, 0]]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d += rng.normal(scale=np.radians(1.0), size=d.shape)
+    bad = rng.random(m) < 0.05
+    d[bad] = rng.normal(size=(bad.sum(), 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    g = T.DirectionGraph(n=n, edges_i=e[:, 0], edges_j=e[:, 1], directions=d)
+
+    class C:
+        translation_lr, translation_steps, translation_inits = 1e-3, 6000, 16
+        adam_beta1, adam_beta2, adam_eps = 0.9, 0.999, 1e-8
+    with torch.cuda.stream(stream):
+        T.align_centers(g, C, seed=0, steps=200)  # warm-up (graph upload, capture)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        centers, loss = T.multi_init_align(g, C, seed=0)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    evals = (16 + 1) * 6000 * m
+    return {"multi_init_align_s": dt, "translation_loss": loss,
+            "translation_config": "C3: 2000 nodes, 200000 edges, 16 inits x 6000 steps + final",
+            "translation_edge_evals_per_s": evals / dt}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-optimize", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    from paper_2505_04612_b200 import scenes
+    from paper_2505_04612_b200.config import HotPathConfig
+    args.cfg = HotPathConfig()
+    spec = scenes.CONFIGS[args.config]
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, spec, world, rank)
+    else:
+        run_ours(args, spec, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

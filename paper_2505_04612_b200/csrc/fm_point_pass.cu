@@ -52,7 +52,8 @@ __device__ __forceinline__ float2 f2(float s) { return make_float2(s, s); }
 // on the remaining 3 values.  Afterwards lane l holds the warp totals of
 // values [base, base+3), base = 24*b4 + 12*b3 + 6*b2 + 3*b1 (b_k = bit k of l);
 // lanes l and l^1 hold the same totals.
-__device__ __forceinline__ void warp_transpose_reduce48(float (&v)[48], int lane) {
+template <typename T>
+__device__ __forceinline__ void warp_transpose_reduce48(T (&v)[48], int lane) {
 #pragma unroll
   for (int level = 0; level < 4; ++level) {
     const int off = 16 >> level;
@@ -60,8 +61,8 @@ __device__ __forceinline__ void warp_transpose_reduce48(float (&v)[48], int lane
     const bool upper = (lane & off) != 0;
 #pragma unroll
     for (int i = 0; i < half; ++i) {
-      const float send = upper ? v[i] : v[i + half];
-      const float keep = upper ? v[i + half] : v[i];
+      const T send = upper ? v[i] : v[i + half];
+      const T keep = upper ? v[i + half] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
@@ -144,111 +145,235 @@ __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialB
 }
 
 // ------------------------------------------------------------------ hot kernel
-// z == 1, fp32 moments.  MODE is a combination of PRUNE / L1 / MOMENTS|IRLS /
-// SKIP_DROPPED.
-template <unsigned MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
+// z == 1.  Persistent warps walk their work items (static round robin) while
+// lane 0 streams the items' coordinates into a per-warp ring of kStages
+// shared-memory stages with 1-D bulk async copies (cp.async.bulk -> UBLKCP,
+// completion on an mbarrier): kStages x 2 KB in flight per warp without
+// holding registers, and the next item's data arrives while the current
+// item's warp reduction runs.
+//
+// MOM64 = true (default, exact): the 36 Kronecker moments accumulate in fp64,
+// so W matches the reference's fp64 W to rounding -- the IRLS quadratic form
+// is ill-conditioned and fp32 moments visibly move the optimum.
+// MOM64 = false (opt-in fast mode): fp32 moments with packed FFMA2 plus the
+// shifted-model linearisation terms vgrad / s0.
+constexpr int kStages = 4;
+constexpr int kStageSlots = 128;
+constexpr int kHotWarps = 4;
+
+struct HotWarpSmem {
+  float2 x1[kStages][kStageSlots];
+  float2 x2[kStages][kStageSlots];
+  unsigned long long bar[kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+
+struct ItemDesc {
+  int64_t lo;  // first slot
+  int len;     // points in the item
+  int n;       // image pair
+  int nst;     // stages (0 if the pair is skipped)
+};
+
+template <bool kSkip>
+__device__ __forceinline__ ItemDesc load_item(const fm_point_store& s, int64_t k,
+                                              const int32_t* __restrict__ prev_active) {
+  ItemDesc d;
+  d.n = s.item_pair[k];
+  const int c = (int)(k - s.pair_item_off[d.n]);
+  d.lo = s.pair_off[d.n] + (int64_t)c * s.chunk;
+  const int64_t rem = (int64_t)s.pair_len[d.n] - (int64_t)c * s.chunk;
+  d.len = (int)(rem < s.chunk ? rem : s.chunk);
+  d.nst = (d.len + kStageSlots - 1) / kStageSlots;
+  if (kSkip && prev_active[d.n] == 0) d.nst = 0;
+  return d;
+}
+
+template <unsigned MODE, bool MOM64>
+__global__ void __launch_bounds__(kHotWarps * 32)
 point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                const int32_t* __restrict__ prev_active, const fm_pass_out out,
                const PartialBufs part) {
   constexpr bool kPrune = MODE & FM_PASS_PRUNE;
   constexpr bool kL1 = MODE & FM_PASS_L1;
   constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
+  constexpr bool kLin = kMom && !MOM64;
   constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
 
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (item >= s.n_items) return;
-  const int n = s.item_pair[item];
-  const int first = s.pair_item_off[n];
-  const bool single = (s.pair_item_off[n + 1] - first) == 1;
+  const int wib = threadIdx.x >> 5;
+  HotWarpSmem& sm = reinterpret_cast<HotWarpSmem*>(smem_raw)[wib];
+  const int64_t W = (int64_t)gridDim.x * kHotWarps;
+  const int64_t w0 = (int64_t)blockIdx.x * kHotWarps + wib;
   const int64_t P = s.n_pairs;
+  const int64_t NI = s.n_items;
 
-  float2 M2[18];  // moments, row p (x2 product) x column pair q (x1 products)
-  float2 V0, V1, V2, V3;
-  float v22 = 0.f;
+  if (lane == 0) {
 #pragma unroll
-  for (int k = 0; k < 18; ++k) M2[k] = f2(0.f);
-  V0 = V1 = V2 = V3 = f2(0.f);
-  double s0 = 0.0, l1 = 0.0;
-  int cnt = 0;
+    for (int k = 0; k < kStages; ++k) mbar_init(&sm.bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
 
-  const bool skip = kSkip && prev_active[n] == 0;
-  if (!skip) {
+  // ---------------------------------------------------------- producer
+  int64_t p_item = w0;
+  ItemDesc pd;
+  if (p_item < NI) pd = load_item<kSkip>(s, p_item, prev_active);
+  int p_st = 0;
+  uint32_t issued = 0;
+  auto produce = [&]() {
+    while (p_item < NI && p_st >= pd.nst) {
+      p_item += W;
+      if (p_item < NI) pd = load_item<kSkip>(s, p_item, prev_active);
+      p_st = 0;
+    }
+    if (p_item >= NI) return;
+    const int64_t b = pd.lo + (int64_t)p_st * kStageSlots;
+    const int rem = pd.len - p_st * kStageSlots;
+    const int nsl = rem < kStageSlots ? ((rem + 3) & ~3) : kStageSlots;
+    const uint32_t bytes = (uint32_t)nsl * 8u;
+    const int st = issued % kStages;
+    if (lane == 0) {
+      mbar_expect_tx(&sm.bar[st], 2u * bytes);
+      bulk_g2s(&sm.x1[st][0], s.x1 + 2 * b, bytes, &sm.bar[st]);
+      bulk_g2s(&sm.x2[st][0], s.x2 + 2 * b, bytes, &sm.bar[st]);
+    }
+    ++issued;
+    ++p_st;
+  };
+#pragma unroll 1
+  for (int k = 0; k < kStages; ++k) produce();
+
+  // ---------------------------------------------------------- consumer
+  uint32_t consumed = 0;
+#pragma unroll 1
+  for (int64_t item = w0; item < NI; item += W) {
+    const ItemDesc d = load_item<kSkip>(s, item, prev_active);
+    const bool single = (s.pair_item_off[d.n + 1] - s.pair_item_off[d.n]) == 1;
     double G[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) G[k] = ghat[k * P + n];
-    const int64_t base = s.pair_off[n];
-    const int64_t end = base + s.pair_len[n];
-    const int64_t lo = base + (int64_t)(item - first) * s.chunk;
-    const int64_t hi = end < lo + s.chunk ? end : lo + s.chunk;
+    for (int k = 0; k < 9; ++k) G[k] = d.nst ? ghat[k * P + d.n] : 0.0;
 
-    int64_t b = lo + 4 * lane;
-    float4 P1a, P1b, P2a, P2b;  // x1 (slots b, b+1), (b+2, b+3); x2 likewise
-    bool have = b < hi;
-    if (have) {
-      P1a = ld_stream4(s.x1 + 2 * b);
-      P1b = ld_stream4(s.x1 + 2 * b + 4);
-      P2a = ld_stream4(s.x2 + 2 * b);
-      P2b = ld_stream4(s.x2 + 2 * b + 4);
+    double M64[MOM64 ? 36 : 1];
+    float2 M2[MOM64 ? 1 : 18];
+    float2 V0, V1, V2, V3;
+    float v22 = 0.f, s0f = 0.f;
+    if (MOM64) {
+#pragma unroll
+      for (int k = 0; k < (MOM64 ? 36 : 1); ++k) M64[k] = 0.0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < (MOM64 ? 1 : 18); ++k) M2[k] = f2(0.f);
     }
-    while (have) {
-      const float4 c1a = P1a, c1b = P1b, c2a = P2a, c2b = P2b;
-      const int64_t cb = b;
-      b += 128;
-      have = b < hi;
-      if (have) {  // prefetch the next 4 slots while this group computes
-        P1a = ld_stream4(s.x1 + 2 * b);
-        P1b = ld_stream4(s.x1 + 2 * b + 4);
-        P2a = ld_stream4(s.x2 + 2 * b);
-        P2b = ld_stream4(s.x2 + 2 * b + 4);
-      }
+    V0 = V1 = V2 = V3 = f2(0.f);
+    double l1 = 0.0;
+    int cnt = 0;
+    const int64_t hi = d.lo + d.len;
+
+#pragma unroll 1
+    for (int st_i = 0; st_i < d.nst; ++st_i) {
+      const int st = consumed % kStages;
+      const uint32_t phase = (consumed / kStages) & 1u;
+      const int64_t cb = d.lo + (int64_t)st_i * kStageSlots + 4 * lane;
       const int shift = (int)(cb & 31);
-      const unsigned bits = (s.active[cb >> 5] >> shift) & 0xFu;
+      const unsigned bits = cb < hi ? ((s.active[cb >> 5] >> shift) & 0xFu) : 0u;
+      mbar_wait(&sm.bar[st], phase);
+      const float4 q1a = *reinterpret_cast<const float4*>(&sm.x1[st][4 * lane]);
+      const float4 q1b = *reinterpret_cast<const float4*>(&sm.x1[st][4 * lane + 2]);
+      const float4 q2a = *reinterpret_cast<const float4*>(&sm.x2[st][4 * lane]);
+      const float4 q2b = *reinterpret_cast<const float4*>(&sm.x2[st][4 * lane + 2]);
+      __syncwarp();
+      ++consumed;
+      produce();  // refill the stage just drained
+
       unsigned keep_bits = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float4& q1 = k < 2 ? c1a : c1b;
-        const float4& q2 = k < 2 ? c2a : c2b;
+        const float4& q1 = k < 2 ? q1a : q1b;
+        const float4& q2 = k < 2 ? q2a : q2b;
         const float2 X1 = (k & 1) ? make_float2(q1.z, q1.w) : make_float2(q1.x, q1.y);
         const float2 X2 = (k & 1) ? make_float2(q2.z, q2.w) : make_float2(q2.x, q2.y);
         const bool act = (cb + k < hi) && ((bits >> k) & 1u);
         // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
-        const double a = X1.x, bb = X1.y, c = X2.x, d = X2.y;
+        const double a = X1.x, bb = X1.y, c = X2.x, dd = X2.y;
         const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
         const double y1 = fma(G[3], a, fma(G[4], bb, G[5]));
         const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
-        const double r = fma(c, y0, fma(d, y1, y2));
+        const double r = fma(c, y0, fma(dd, y1, y2));
         const double ar = fabs(r);
         const bool keep = kPrune ? (act && ar <= thr) : act;
         keep_bits |= (unsigned)keep << k;
         cnt += keep;
         if (kL1) l1 += act ? ar : 0.0;
         if (kMom) {
-          // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58)
-          const float w = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
-          const bool big = ar >= 1e-6;
-          // w r0 and w r0^2 without a division: sign(r), |r| unless clamped
-          const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
-          s0 += keep ? (big ? ar : r * r * 1e6) : 0.0;
-          const float2 wX2 = __fmul2_rn(f2(w), X2);  // (w c, w d)
-          const float B[6] = {wX2.x * X2.x, wX2.x * X2.y, wX2.x, wX2.y * X2.y, wX2.y, w};
-          const float2 A0 = __fmul2_rn(f2(X1.x), X1);         // (a^2, a b)
-          const float2 A2 = make_float2(X1.y * X1.y, 1.f);    // (b^2, 1)
-          // hot order rows/cols: {aa|cc, ab|cd, a|c, b|d, bb|dd, 1}
-          const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
+          // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); a per-point
+          // relative error of the weight keeps each term rank-1 exact.
+          // Dropped / padding / stale-stage slots are zeroed by select (not by
+          // a zero weight: 0 * NaN would poison the sums).
+          const float wf = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
+          const float2 Y1 = keep ? X1 : f2(0.f);
+          const float2 Y2 = keep ? X2 : f2(0.f);
+          if (MOM64) {
+            const double w = wf;
+            const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
+            const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
+            const double wc = w * kc, wd = w * kd;
+            const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
+            // canonical sym order {00,01,02,11,12,22} for both factors
 #pragma unroll
-          for (int p = 0; p < 6; ++p) {
-            M2[p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[p * 3 + 0]);
-            M2[p * 3 + 1] = __ffma2_rn(f2(Brow[p]), X1, M2[p * 3 + 1]);
-            M2[p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[p * 3 + 2]);
+            for (int i = 0; i < 6; ++i)
+#pragma unroll
+              for (int j = 0; j < 6; ++j) M64[i * 6 + j] = fma(B[i], A[j], M64[i * 6 + j]);
+          } else {
+            const bool big = ar >= 1e-6;
+            const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
+            s0f += keep ? (big ? (float)ar : (float)(r * r * 1e6)) : 0.f;
+            const float2 wX2 = __fmul2_rn(f2(wf), Y2);
+            const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
+            const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
+            const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
+            const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
+#pragma unroll
+            for (int p = 0; p < 6; ++p) {
+              M2[p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[p * 3 + 0]);
+              M2[p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[p * 3 + 1]);
+              M2[p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[p * 3 + 2]);
+            }
+            const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
+            V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
+            V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
+            V2 = __ffma2_rn(f2(wr), Y1, V2);
+            V3 = __fadd2_rn(wrX2, V3);
+            v22 += wr;
           }
-          const float2 wrX2 = __fmul2_rn(f2(wr), X2);  // (wr c, wr d)
-          V0 = __ffma2_rn(f2(wrX2.x), X1, V0);
-          V1 = __ffma2_rn(f2(wrX2.y), X1, V1);
-          V2 = __ffma2_rn(f2(wr), X1, V2);
-          V3 = __fadd2_rn(wrX2, V3);
-          v22 += wr;
         }
       }
       if (kPrune) {
@@ -256,49 +381,84 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
         if (cleared) atomicAnd(&s.active[cb >> 5], ~(cleared << shift));
       }
     }
-  }
 
-  // -------------------------------------------------------------- reduce
-  if (kMom) {
-    float v[48];
+    // ------------------------------------------------------------ reduce
+    if (kMom && MOM64) {
+      double v[48];
 #pragma unroll
-    for (int k = 0; k < 18; ++k) {
-      v[2 * k] = M2[k].x;
-      v[2 * k + 1] = M2[k].y;
-    }
-    v[36] = V0.x; v[37] = V0.y; v[38] = V1.x; v[39] = V1.y;
-    v[40] = V2.x; v[41] = V2.y; v[42] = V3.x; v[43] = V3.y;
-    v[44] = v22;
-    v[45] = (float)cnt;
-    v[46] = 0.f;
-    v[47] = 0.f;
-    warp_transpose_reduce48(v, lane);
-    if ((lane & 1) == 0) {
-      const int rb = red_base48(lane);
+      for (int k = 0; k < 36; ++k) v[k] = M64[k];
+      v[36] = (double)cnt;
+      v[37] = l1;
 #pragma unroll
-      for (int h = 0; h < 3; ++h) {
-        const int k = hot_out_index(rb + h);
-        if (k >= 0) store_red(out, part, single, P, s.n_items, n, item, k, v[h], true);
+      for (int k = 38; k < 48; ++k) v[k] = 0.0;
+      warp_transpose_reduce48(v, lane);
+      if ((lane & 1) == 0) {
+        const int rb = red_base48(lane);
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const int k = rb + h;
+          if (k >= 38) continue;
+          if (!single) {
+            if (k < 36) static_cast<double*>(part.red)[k * NI + item] = v[h];
+            else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = v[h];
+            else part.l1[item] = v[h];
+          } else if (k < 36) {
+            out.mom64[k * P + d.n] = v[h];
+          } else if (k == 36) {
+            if (out.n_active) out.n_active[d.n] = (int32_t)v[h];
+          } else if (kL1 && out.l1) {
+            out.l1[d.n] = v[h];
+          }
+        }
       }
-    }
-  } else {
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) store_red(out, part, single, P, s.n_items, n, item, 45, (float)cnt, false);
-  }
-  if (kMom) {
-    s0 = warp_sum(s0);
-    if (lane == 0) {
-      if (single) out.s0[n] = s0;
-      else part.s0[item] = s0;
-    }
-  }
-  if (kL1) {
-    l1 = warp_sum(l1);
-    if (lane == 0) {
-      if (single) {
-        if (out.l1) out.l1[n] = l1;
+    } else {
+      if (kMom) {
+        float v[48];
+#pragma unroll
+        for (int k = 0; k < 18; ++k) {
+          v[2 * k] = M2[MOM64 ? 0 : k].x;
+          v[2 * k + 1] = M2[MOM64 ? 0 : k].y;
+        }
+        v[36] = V0.x; v[37] = V0.y; v[38] = V1.x; v[39] = V1.y;
+        v[40] = V2.x; v[41] = V2.y; v[42] = V3.x; v[43] = V3.y;
+        v[44] = v22;
+        v[45] = (float)cnt;
+        v[46] = s0f;
+        v[47] = 0.f;
+        warp_transpose_reduce48(v, lane);
+        if ((lane & 1) == 0) {
+          const int rb = red_base48(lane);
+#pragma unroll
+          for (int h = 0; h < 3; ++h) {
+            const int vi = rb + h;
+            if (vi == 46) {
+              if (single) out.s0[d.n] = (double)v[h];
+              else part.s0[item] = (double)v[h];
+              continue;
+            }
+            const int k = hot_out_index(vi);
+            if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, v[h], kLin);
+          }
+        }
       } else {
-        part.l1[item] = l1;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+          if (single) {
+            if (out.n_active) out.n_active[d.n] = cnt;
+          } else {
+            static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
+          }
+        }
+      }
+      if (kL1) {
+        l1 = warp_sum(l1);
+        if (lane == 0) {
+          if (single) {
+            if (out.l1) out.l1[d.n] = l1;
+          } else {
+            part.l1[item] = l1;
+          }
+        }
       }
     }
   }
@@ -458,11 +618,11 @@ point_pass_generic(const fm_point_store s, const double* __restrict__ ghat,
 // Sum the partials of pairs split over several work items, in item order.
 template <bool F64, unsigned MODE>
 __global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
-                               const PartialBufs part) {
+                               const PartialBufs part, const bool has_lin) {
   using Acc = typename std::conditional<F64, double, float>::type;
   constexpr bool kL1 = MODE & FM_PASS_L1;
   constexpr bool kMom = MODE & FM_PASS_MOMENTS;
-  constexpr bool kLin = kMom && (MODE & FM_PASS_IRLS);
+  const bool kLin = kMom && (MODE & FM_PASS_IRLS) && has_lin;
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= s.n_pairs) return;
   const int i0 = s.pair_item_off[n], i1 = s.pair_item_off[n + 1];
@@ -471,6 +631,7 @@ __global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
   const Acc* red = static_cast<const Acc*>(part.red);
   for (int k = kMom ? 0 : 45; k < kNumRed; ++k) {
     Acc acc = 0;
+    if (k >= 36 && k < 45 && !kLin) continue;
     for (int i = i0; i < i1; ++i) acc += red[k * NI + i];
     if (k < 36) {
       if (F64) out.mom64[k * P + n] = (double)acc;
@@ -493,15 +654,26 @@ __global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
   }
 }
 
-template <unsigned MODE>
+template <unsigned MODE, bool MOM64>
 int launch_hot(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
                const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
-  const int64_t blocks = ceil_div(s.n_items, kWarpsPerBlock);
-  point_pass_hot<MODE><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, stream>>>(s, ghat, thr, prev_active,
-                                                                            out, part);
+  static int blocks_per_sm = 0;
+  const size_t smem = kHotWarps * sizeof(HotWarpSmem);
+  if (!blocks_per_sm) {
+    FM_CUDA(cudaFuncSetAttribute(point_pass_hot<MODE, MOM64>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, point_pass_hot<MODE, MOM64>,
+                                                          kHotWarps * 32, smem));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t want = ceil_div(s.n_items, kHotWarps);
+  const int64_t grid = std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count());
+  point_pass_hot<MODE, MOM64><<<(unsigned)grid, kHotWarps * 32, smem, stream>>>(s, ghat, thr, prev_active,
+                                                                               out, part);
   FM_LAUNCHED(point_pass_hot);
   if (s.n_items > s.n_pairs) {
-    combine_kernel<false, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part);
+    combine_kernel<MOM64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
+                                                                                        !MOM64);
     FM_LAUNCHED(combine_kernel);
   }
   return FM_OK;
@@ -516,7 +688,8 @@ int launch_generic(const fm_point_store& s, double thr, const double* ghat, cons
       s, ghat, res_in, thr, prev_active, out, part);
   FM_LAUNCHED(point_pass_generic);
   if (s.n_items > s.n_pairs) {
-    combine_kernel<F64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part);
+    combine_kernel<F64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
+                                                                                      true);
     FM_LAUNCHED(combine_kernel);
   }
   return FM_OK;
@@ -559,14 +732,21 @@ int dispatch_generic(unsigned mode, const fm_point_store& s, double thr, const d
   return set_error(FM_ERR_INVALID, "unsupported point-pass mode 0x%x", mode);
 }
 
-int dispatch_hot(unsigned mode, const fm_point_store& s, double thr, const double* ghat,
+int dispatch_hot(unsigned mode, bool f64, const fm_point_store& s, double thr, const double* ghat,
                  const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
                  cudaStream_t stream, bool* handled) {
   *handled = true;
+  if (f64) {
 #define FM_CASE(M) \
-  if (mode == (M)) return launch_hot<(M)>(s, thr, ghat, prev_active, out, part, stream);
-  FM_HOT_MODES(FM_CASE)
+  if (mode == (M)) return launch_hot<(M), true>(s, thr, ghat, prev_active, out, part, stream);
+    FM_HOT_MODES(FM_CASE)
 #undef FM_CASE
+  } else {
+#define FM_CASE(M) \
+  if (mode == (M)) return launch_hot<(M), false>(s, thr, ghat, prev_active, out, part, stream);
+    FM_HOT_MODES(FM_CASE)
+#undef FM_CASE
+  }
   *handled = false;
   return FM_OK;
 }
@@ -621,10 +801,14 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE(scratch && sc.ok(), "point-pass scratch too small (%zu < %zu)", scratch_bytes, sc.used);
   }
   cudaStream_t st = as_stream(stream);
-  if (!homog && !f64) {
+  if (!homog) {
+    // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
+    const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
     bool handled = false;
-    const int rc = dispatch_hot(m, s, threshold, ghat, prev_active, *out, part, st, &handled);
-    if (handled) return rc;
+    if (hot_f64 || (m & FM_PASS_IRLS)) {
+      const int rc = dispatch_hot(m, hot_f64, s, threshold, ghat, prev_active, *out, part, st, &handled);
+      if (handled) return rc;
+    }
   }
   if (homog) {
     return f64 ? dispatch_generic<true, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)

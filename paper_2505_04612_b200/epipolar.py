@@ -307,23 +307,43 @@ def prune_thresholds(cfg):
 
 
 class IrlsBuffers:
-    """Device buffers of one irls_refine run (per image pair, store order)."""
+    """Device buffers of one irls_refine run (per image pair, store order).
 
-    def __init__(self, P, device):
+    precision "fp64" (default): exact fp64 W moments, unshifted model.
+    precision "fp32": fp32 moments + shifted-model terms (fast mode)."""
+
+    def __init__(self, P, device, precision="fp64"):
         Pm = max(P, 1)
+        self.precision = precision
         self.ghat0 = torch.zeros((9, Pm), dtype=torch.float64, device=device)
-        self.mom32 = torch.zeros((36, Pm), dtype=torch.float32, device=device)
-        self.vgrad = torch.zeros((9, Pm), dtype=torch.float32, device=device)
-        self.s0 = torch.zeros(Pm, dtype=torch.float64, device=device)
         self.l1 = torch.zeros(Pm, dtype=torch.float64, device=device)
         self.n_active = [torch.zeros(Pm, dtype=torch.int32, device=device) for _ in range(2)]
-        self.quad = N.QuadModel(kind=N.FM_QUAD_SHIFTED32, mom32=self.mom32.data_ptr(),
-                                vgrad=self.vgrad.data_ptr(), s0=self.s0.data_ptr(),
-                                ghat0=self.ghat0.data_ptr())
+        if precision == "fp64":
+            self.mom64 = torch.zeros((36, Pm), dtype=torch.float64, device=device)
+            self.quad = N.QuadModel(kind=N.FM_QUAD_MOM64, mom64=self.mom64.data_ptr())
+            self.flags = N.FM_PASS_F64
+        elif precision == "fp32":
+            self.mom32 = torch.zeros((36, Pm), dtype=torch.float32, device=device)
+            self.vgrad = torch.zeros((9, Pm), dtype=torch.float32, device=device)
+            self.s0 = torch.zeros(Pm, dtype=torch.float64, device=device)
+            self.quad = N.QuadModel(kind=N.FM_QUAD_SHIFTED32, mom32=self.mom32.data_ptr(),
+                                    vgrad=self.vgrad.data_ptr(), s0=self.s0.data_ptr(),
+                                    ghat0=self.ghat0.data_ptr())
+            self.flags = 0
+        else:
+            raise ValueError(f"unknown precision {precision!r}")
 
     def out(self, k):
-        return {"mom32": self.mom32, "vgrad": self.vgrad, "s0": self.s0, "l1": self.l1,
-                "n_active": self.n_active[k]}
+        o = {"l1": self.l1, "n_active": self.n_active[k]}
+        if self.precision == "fp64":
+            o["mom64"] = self.mom64
+        else:
+            o.update(mom32=self.mom32, vgrad=self.vgrad, s0=self.s0)
+        return o
+
+    def outputs(self):
+        """Per-pair result tensors of a pass (for the e2e benchmark)."""
+        return [t for t in self.out(0).values()]
 
 
 class IrlsEngine:
@@ -331,7 +351,7 @@ class IrlsEngine:
     over an already-built store and pair graph.  Used by ``irls_refine`` and
     directly by the benchmark (store built on the device)."""
 
-    def __init__(self, store, graph, params, cfg, use_graph=True):
+    def __init__(self, store, graph, params, cfg, use_graph=True, precision="fp64"):
         self.store = store
         self.graph = graph
         self.device = store.device
@@ -339,7 +359,7 @@ class IrlsEngine:
         self.params = params
         self.use_graph = use_graph
         P = graph.n_pairs
-        self.buf = IrlsBuffers(P, self.device)
+        self.buf = IrlsBuffers(P, self.device, precision)
         self.pscratch = store.scratch()
         self.gscratch = graph.scratch()
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -354,6 +374,8 @@ class IrlsEngine:
                                      self.gscratch.numel(), N.stream_handle()))
 
     def point_pass(self, mode, threshold, cur, prev):
+        if mode & N.FM_PASS_MOMENTS:
+            mode |= self.buf.flags
         _pass(self.store, mode, threshold, ghat=self.buf.ghat0,
               prev_active=self.buf.n_active[prev] if (mode & N.FM_PASS_SKIP_DROPPED) else None,
               out=self.buf.out(cur), scratch=self.pscratch)
@@ -417,7 +439,7 @@ class IrlsEngine:
         return l1_history
 
 
-def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True):
+def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True, precision="fp64"):
     """Scheduled IRLS refinement of global poses (and optionally focals)
     (ref/epipolar.py:265-319).  Mutates pair ``active`` masks during pruning.
     Returns (poses, focal_scale per camera, report dict)."""
@@ -430,7 +452,7 @@ def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True):
     graph = PairGraph(idx_i[o], idx_j[o], cam_i[o], cam_j[o], len(image_ids), n_cameras,
                       cfg.refine_focal, device=device)
     params = torch.as_tensor(state.pack(), device=device)
-    engine = IrlsEngine(store, graph, params, cfg, use_graph=use_graph)
+    engine = IrlsEngine(store, graph, params, cfg, use_graph=use_graph, precision=precision)
     try:
         l1_history = engine.run()
     finally:

@@ -1,0 +1,215 @@
+"""Data-parallel epipolar adjustment: point pairs sharded by contiguous
+image-pair ranges across GPUs (one process per GPU, NCCL over NVLink).
+
+Every shard owns whole image pairs, so the fused point pass, the W moments,
+the prune masks and the per-pair partials stay local.  The exchanges are
+(ref/epipolar.py:279-312 schedule):
+
+* after each prune pass: one all-reduce of {Z, kept pairs, L1 sum} (3 doubles);
+* per Adam step: one all-reduce of the packed per-image gradient
+  (9N + C doubles) and the loss; Adam then runs replicated on every rank
+  (identical inputs -> identical parameters, no broadcast).
+
+``ShardedIrlsEngine`` holds one or more local shards; with one shard per
+process and a ``torch.distributed`` communicator it is the multi-GPU engine,
+with several shards in one process it is the same algebra on one GPU (used to
+test the sharded schedule against the single-store engine).
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .epipolar import IrlsBuffers, prune_thresholds
+
+
+def partition_pairs(lengths, world):
+    """Contiguous image-pair ranges [b_k, b_{k+1}) balanced by point count.
+
+    b_k is the first pair whose preceding points reach k/world of the total,
+    so shard point counts differ by at most one pair's points."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    P = len(lengths)
+    before = np.concatenate([[0], np.cumsum(lengths)])[:-1] if P else np.zeros(0, np.int64)
+    total = int(lengths.sum())
+    bounds = [0]
+    for k in range(1, world):
+        b = int(np.searchsorted(before, total * k / world, side="left")) if P else 0
+        bounds.append(max(b, bounds[-1]))
+    bounds.append(P)
+    return np.array(bounds, dtype=np.int64)
+
+
+class TorchComm:
+    """Sum all-reduce over a torch.distributed process group (NCCL/gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def allreduce_(self, t):
+        if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+class NoComm:
+    def allreduce_(self, t):
+        return t
+
+
+class Shard:
+    """One store + pair graph (global image / camera indexing)."""
+
+    def __init__(self, store, graph, precision="fp64"):
+        self.store = store
+        self.graph = graph
+        self.device = store.device
+        self.buf = IrlsBuffers(graph.n_pairs, self.device, precision)
+        self.pscratch = store.scratch()
+        self.gscratch = graph.scratch()
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.grad = torch.zeros(graph.n_params, dtype=torch.float64, device=self.device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+
+class ShardedIrlsEngine:
+    """irls_refine schedule over sharded point pairs (see module docstring)."""
+
+    def __init__(self, shards, params, cfg, comm=None):
+        self.shards = shards
+        self.params = params
+        self.cfg = cfg
+        self.comm = comm or NoComm()
+        self.device = params.device
+        self.m = torch.zeros_like(params)
+        self.v = torch.zeros_like(params)
+        self.aflag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.lib = N.lib()
+
+    def _ghat(self, sh):
+        N.check(self.lib.fm_epi_pair_ghat(ctypes.byref(sh.graph.struct()), N.ptr(self.params),
+                                          N.ptr(sh.buf.ghat0), N.ptr(sh.flag), N.ptr(sh.gscratch),
+                                          sh.gscratch.numel(), N.stream_handle()))
+
+    def _pass(self, sh, mode, th, cur, prev):
+        from .epipolar import _pass
+        if mode & N.FM_PASS_MOMENTS:
+            mode |= sh.buf.flags
+        _pass(sh.store, mode, th, ghat=sh.buf.ghat0,
+              prev_active=sh.buf.n_active[prev] if (mode & N.FM_PASS_SKIP_DROPPED) else None,
+              out=sh.buf.out(cur), scratch=sh.pscratch)
+
+    def _scalars(self, cur, with_l1):
+        s = torch.zeros(4, dtype=torch.float64, device=self.device)
+        for sh in self.shards:
+            P = sh.graph.n_pairs
+            cnt = sh.buf.n_active[cur][:P]
+            s[0] += cnt.sum().double()
+            s[1] += (cnt > 0).sum().double()
+            if with_l1:
+                s[2] += sh.buf.l1[:P].sum()
+            s[3] += P
+        self.comm.allreduce_(s)
+        return s.cpu().numpy()
+
+    def _check_flags(self):
+        for sh in self.shards:
+            N.raise_flag(sh.flag.item())
+        N.raise_flag(self.aflag.item())
+
+    def _step(self, t, lr, scale):
+        cfg = self.cfg
+        total = None
+        for sh in self.shards:
+            N.check(self.lib.fm_epi_loss_grad(
+                ctypes.byref(sh.graph.struct()), ctypes.byref(sh.buf.quad), N.ptr(self.params),
+                scale, N.ptr(sh.loss), N.ptr(sh.grad), N.ptr(sh.flag), N.ptr(sh.gscratch),
+                sh.gscratch.numel(), N.stream_handle()))
+            if total is None:
+                total = torch.cat([sh.grad, sh.loss])
+            else:
+                total += torch.cat([sh.grad, sh.loss])
+        self.comm.allreduce_(total)
+        if not torch.isfinite(total[-1]):
+            self.aflag.fill_(N.FM_ERR_NONFINITE_LOSS)
+            return
+        g = total[:-1].contiguous()
+        N.check(self.lib.fm_adam_step(N.ptr(self.params), N.ptr(self.m), N.ptr(self.v), N.ptr(g),
+                                      self.params.numel(), t, lr, cfg.adam_beta1, cfg.adam_beta2,
+                                      cfg.adam_eps, N.ptr(self.aflag), N.stream_handle()))
+
+    def run(self):
+        cfg = self.cfg
+        l1_history = []
+        lr = cfg.epipolar_lr
+        cur = 0
+        Z = None
+        for rnd, th in enumerate(prune_thresholds(cfg)):
+            mode = N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS
+            if rnd > 0:
+                mode |= N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED
+            prev, cur = cur, 1 - cur
+            for sh in self.shards:
+                self._ghat(sh)
+                self._pass(sh, mode, th, cur, prev)
+            z, kept, l1, p_total = self._scalars(cur, rnd > 0)
+            if rnd > 0:
+                l1_history.append(float(l1) / Z)
+            self._check_flags()
+            Z = int(z)
+            self.kept = int(kept)
+            self.dropped = int(p_total) - self.kept
+            if self.kept == 0:
+                raise ValueError("all pairs pruned away")
+            self.m.zero_()
+            self.v.zero_()
+            steps = cfg.epipolar_epoch_steps
+            for it in range(cfg.irls_iters_between_prunes):
+                if it > 0:
+                    for sh in self.shards:
+                        self._ghat(sh)
+                        self._pass(sh, N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED,
+                                   0.0, 1 - cur, cur)
+                        sh.buf.n_active[cur], sh.buf.n_active[1 - cur] = \
+                            sh.buf.n_active[1 - cur], sh.buf.n_active[cur]
+                for k in range(steps):
+                    self._step(it * steps + k + 1, lr, 2.0 / Z)
+                self._check_flags()
+            lr /= cfg.lr_decay
+        for sh in self.shards:
+            self._ghat(sh)
+            self._pass(sh, N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED, 0.0, 1 - cur, cur)
+            sh.buf.n_active[cur], sh.buf.n_active[1 - cur] = \
+                sh.buf.n_active[1 - cur], sh.buf.n_active[cur]
+        _, kept, l1, _ = self._scalars(cur, True)
+        self._check_flags()
+        l1_history.append(float(l1) / Z)
+        return l1_history
+
+
+def make_shards(x1, x2, lengths, ij, cams, n_images, n_cameras, refine_focal, bounds, device,
+                precision="fp64", ranks=None):
+    """Build the shards [bounds[k], bounds[k+1]) of a (sorted) pair list.
+
+    x1, x2: host arrays (Z, 2|3); lengths, ij (P, 2) dense image indices,
+    cams (P, 2).  ranks selects which shards to build (default: all)."""
+    from .store import PairGraph, PointPairStore
+    lengths = np.asarray(lengths, dtype=np.int64)
+    start = np.concatenate([[0], np.cumsum(lengths)])
+    out = []
+    for k in (range(len(bounds) - 1) if ranks is None else ranks):
+        a, b = int(bounds[k]), int(bounds[k + 1])
+        sl = slice(start[a], start[b])
+        store = PointPairStore(x1[sl], x2[sl], lengths[a:b], ij[a:b, 0], ij[a:b, 1],
+                               device=device, order=np.arange(b - a))
+        graph = PairGraph(ij[a:b, 0], ij[a:b, 1], cams[a:b, 0], cams[a:b, 1], n_images, n_cameras,
+                          refine_focal, device=device)
+        out.append(Shard(store, graph, precision))
+    return out
+
+
+__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NoComm", "make_shards"]

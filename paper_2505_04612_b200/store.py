@@ -158,9 +158,7 @@ class PointPairStore:
 
     def caller_masks(self):
         """Active mask of every caller point, host bool array (caller order)."""
-        bits = self.active_bits()
-        slot = torch.from_numpy(self.point_slot).to(self.device)
-        return bits[slot].cpu().numpy()
+        return self.active_bits()[self.slots_device].cpu().numpy()
 
     def write_back(self, pairs):
         """In-place update of each pair's ``active`` array (ref/epipolar.py:283)."""
@@ -174,6 +172,67 @@ class PointPairStore:
 
     def to_stored(self, per_pair_caller):
         return np.asarray(per_pair_caller)[self.order]
+
+    @classmethod
+    def from_device(cls, x1, x2, lengths, device, chunk=CHUNK):
+        """Build from device tensors x1, x2 (Z, 2) float32 whose pairs are
+        already in (i, j) order with ``lengths`` points each (all active)."""
+        self = cls.__new__(cls)
+        lengths = np.asarray(lengths, dtype=np.int64)
+        P = len(lengths)
+        self.device = device
+        self.n_pairs = P
+        self.chunk = chunk
+        self.order = np.arange(P, dtype=np.int64)
+        self.rank = self.order.copy()
+        self.len_caller = lengths
+        pair_off, n_slots, pair_item_off, item_pair = slot_layout(lengths, chunk)
+        self.pair_off = pair_off
+        self.n_slots = n_slots
+        self.n_items = len(item_pair)
+        self.n_points = int(lengths.sum())
+        self.caller_start = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(lengths, out=self.caller_start[1:])
+        lens_d = torch.as_tensor(lengths, device=device)
+        seg = torch.repeat_interleave(torch.arange(P, device=device), lens_d)
+        start_d = torch.as_tensor(self.caller_start[:-1], device=device)
+        off_d = torch.as_tensor(pair_off[:-1], device=device)
+        slot = off_d[seg] + (torch.arange(self.n_points, device=device) - start_d[seg])
+        del seg
+        self.point_slot_d = slot
+        self.point_slot = None
+        self.x1 = torch.zeros((n_slots, 2), dtype=torch.float32, device=device)
+        self.x2 = torch.zeros((n_slots, 2), dtype=torch.float32, device=device)
+        self.x1[slot] = x1.to(torch.float32)
+        self.x2[slot] = x2.to(torch.float32)
+        self.x1z = self.x2z = None
+        self.homogeneous = False
+        bits = torch.zeros(n_slots, dtype=torch.int64, device=device)
+        bits[slot] = 1
+        w = (bits.view(-1, 32) << torch.arange(32, device=device, dtype=torch.int64)).sum(1)
+        self.active = torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
+        del bits, w
+        self.pair_off_d = _dev(pair_off, device)
+        self.pair_len_d = _dev(_i32(lengths), device)
+        self.pair_item_off_d = _dev(pair_item_off, device)
+        self.item_pair_d = _dev(item_pair, device)
+        self._struct = None
+        return self
+
+    def reset_active(self):
+        """Mark every real point active again (benchmark repetitions)."""
+        slot = self.point_slot_d if self.point_slot is None else \
+            torch.from_numpy(self.point_slot).to(self.device)
+        bits = torch.zeros(self.n_slots, dtype=torch.int64, device=self.device)
+        bits[slot] = 1
+        w = (bits.view(-1, 32) << torch.arange(32, device=self.device, dtype=torch.int64)).sum(1)
+        self.active.copy_(torch.where(w >= 2**31, w - 2**32, w).to(torch.int32))
+
+    @property
+    def slots_device(self):
+        if self.point_slot is None:
+            return self.point_slot_d
+        return torch.from_numpy(self.point_slot).to(self.device)
 
     @classmethod
     def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False):

@@ -66,7 +66,9 @@ class SimplePair:
 
 
 class Poses:
-    def __init__(self, rotations, centers):
+    """PoseState stand-in (same constructor keywords as ref/model.py:129-135)."""
+
+    def __init__(self, rotations, centers, registered=None):
         self.rotations = rotations
         self.centers = centers
-        self.registered = np.ones(len(rotations), dtype=bool)
+        self.registered = np.ones(len(rotations), dtype=bool) if registered is None else registered
