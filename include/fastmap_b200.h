@@ -91,7 +91,14 @@ typedef struct fm_point_store {
   const float* x1z;             /* [n_slots] or NULL => homogeneous z == 1 (pipeline case) */
   const float* x2z;
   uint32_t* active;             /* [n_slots/32] bit s%32 of word s/32 = slot s active */
+  /* [n_items][4] int32 work-item descriptors {slot lo (low, high 32 bits),
+   * points, pair | single-item-pair << 31}, filled by fm_point_store_describe;
+   * NULL = derived into scratch on every pass. */
+  int32_t* item_desc;
 } fm_point_store;
+
+/* Fill store->item_desc from the pair / item arrays (one small kernel). */
+int fm_point_store_describe(const fm_point_store* store, void* stream);
 
 /* Pass mode bits (combine with |). */
 #define FM_PASS_PRUNE        1u   /* active &= |r| <= threshold  (ref/epipolar.py:283) */

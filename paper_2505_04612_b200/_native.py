@@ -50,7 +50,8 @@ _SZ = ctypes.c_size_t
 class PointStore(ctypes.Structure):
     _fields_ = [("n_pairs", _I64), ("n_slots", _I64), ("n_items", _I64), ("chunk", _I64),
                 ("pair_off", _P), ("pair_len", _P), ("pair_item_off", _P), ("item_pair", _P),
-                ("x1", _P), ("x2", _P), ("x1z", _P), ("x2z", _P), ("active", _P)]
+                ("x1", _P), ("x2", _P), ("x1z", _P), ("x2z", _P), ("active", _P),
+                ("item_desc", _P)]
 
 
 class PassOut(ctypes.Structure):
@@ -82,6 +83,7 @@ SIGNATURES = {
     "fm_last_error": (ctypes.c_char_p, []),
     "fm_device_count": (ctypes.c_int, []),
     "fm_point_pass_scratch_bytes": (_SZ, [ctypes.POINTER(PointStore)]),
+    "fm_point_store_describe": (ctypes.c_int, [ctypes.POINTER(PointStore), _P]),
     "fm_point_pass": (ctypes.c_int, [ctypes.POINTER(PointStore), ctypes.c_uint, _F64, _P, _P, _P,
                                      ctypes.POINTER(PassOut), _P, _SZ, _P]),
     "fm_epi_scratch_bytes": (_SZ, [ctypes.POINTER(PairGraph)]),

@@ -277,18 +277,44 @@ struct AdamArgs {
   int step;             // index into the bias-correction table
 };
 
-// Warp per image: fixed-order gather of the image's incidences, 6D VJP, then
-// either the packed gradient (API) or an Adam update + new rotation (hot loop).
+// One launch, two roles.  Blocks [0, img_blocks): warp per image --
+// fixed-order gather of the image's incidences, 6D VJP (every lane computes it
+// redundantly from the butterfly-reduced totals), then either the packed
+// gradient (API) or Adam with lane q updating parameter q, and the new
+// rotation.  Blocks [img_blocks, ..): one block per camera chunk --
+// fixed-order partial sum of focal gradients (ref/epipolar.py:194-196).
 template <bool ADAM>
 __global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
                                     const double* __restrict__ pg, double* __restrict__ grad,
-                                    double* __restrict__ R, const AdamArgs ad, int32_t* flag) {
+                                    double* __restrict__ R, double* __restrict__ cpart,
+                                    const int img_blocks, const AdamArgs ad, int32_t* flag) {
+  __shared__ double red[kCamBlock];
+  const int64_t P = g.n_pairs;
+  if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
+    const int c = blockIdx.x - img_blocks;
+    if (ADAM && *flag) return;
+    if (threadIdx.x < kCamBlock) {
+      double acc = 0;
+      const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
+      for (int e = lo + threadIdx.x; e < hi; e += kCamBlock) {
+        const int inc = g.cam_inc[e];
+        acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
+      }
+      red[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    for (int st = kCamBlock / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cpart[c] = red[0];
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int N = g.n_images;
   if (k >= N) return;
   if (ADAM && *flag) return;
-  const int64_t P = g.n_pairs;
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0;
@@ -306,16 +332,18 @@ __global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ 
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = warp_sum(acc[q]);
-  if (lane != 0) return;
-  double* v6 = params + 6 * k;
-  double* c3 = params + 6 * N + 3 * k;
-  double g6[6];
-  rot6d_vjp(v6, acc, g6);
+  double vcur[6], g6[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) vcur[q] = params[6 * (int64_t)k + q];
+  rot6d_vjp(vcur, acc, g6);
+  // gradient component owned by this lane (lanes 0..8 own the 9 image params)
+  double gq = acc[9];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) gq = lane == q ? g6[q] : gq;
+  gq = lane == 7 ? acc[10] : (lane == 8 ? acc[11] : gq);
   if (!ADAM) {
-#pragma unroll
-    for (int q = 0; q < 6; ++q) grad[6 * k + q] = g6[q];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) grad[6 * N + 3 * k + q] = acc[9 + q];
+    if (lane < 6) grad[6 * (int64_t)k + lane] = gq;
+    else if (lane < 9) grad[6 * (int64_t)N + 3 * k + lane - 6] = gq;
     return;
   }
   bool ok = true;
@@ -324,45 +352,30 @@ __global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ 
 #pragma unroll
   for (int q = 0; q < 3; ++q) ok = ok && isfinite(acc[9 + q]);
   if (!ok) {
-    raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    if (lane == 0) raise_flag(flag, FM_ERR_NONFINITE_GRAD);
     return;
   }
   const double lr = ad.sched[0];
   const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+  double newp = 0.0;
+  if (lane < 9) {
+    const int64_t idx = lane < 6 ? 6 * (int64_t)k + lane : 6 * (int64_t)N + 3 * k + (lane - 6);
+    double pv = params[idx];
+    adam_elem(pv, ad.m[idx], ad.v[idx], gq, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+    params[idx] = pv;
+    newp = pv;
+  }
+  // new rotation from the six updated 6D parameters (lanes 0..5)
+  double v6n[6];
 #pragma unroll
-  for (int q = 0; q < 6; ++q)
-    adam_elem(v6[q], ad.m[6 * k + q], ad.v[6 * k + q], g6[q], lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-    adam_elem(c3[q], ad.m[6 * N + 3 * k + q], ad.v[6 * N + 3 * k + q], acc[9 + q], lr, ad.b1,
-              ad.b2, ad.eps, bc1, bc2);
+  for (int q = 0; q < 6; ++q) v6n[q] = __shfl_sync(0xffffffffu, newp, q);
   double Rk[9];
-  const int code = rot6d_to_R(v6, Rk);
-  if (code) raise_flag(flag, code);
+  const int code = rot6d_to_R(v6n, Rk);
+  if (lane == 0 && code) raise_flag(flag, code);
+  double val = Rk[0];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) R[9 * k + q] = Rk[q];
-}
-
-// Block per camera chunk: fixed-order partial sum of focal gradients.
-__global__ void cam_chunk_kernel(const fm_pair_graph g, const double* __restrict__ pg,
-                                 double* __restrict__ cpart, const int32_t* flag) {
-  __shared__ double red[kCamBlock];
-  const int c = blockIdx.x;
-  if (flag && *flag) return;
-  const int64_t P = g.n_pairs;
-  const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
-  double acc = 0;
-  for (int e = lo + threadIdx.x; e < hi; e += kCamBlock) {
-    const int inc = g.cam_inc[e];
-    acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = kCamBlock / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) cpart[c] = red[0];
+  for (int q = 1; q < 9; ++q) val = lane == q ? Rk[q] : val;
+  if (lane < 9) R[9 * (int64_t)k + lane] = val;
 }
 
 template <bool ADAM>
@@ -464,16 +477,14 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
     int rc = launch_pair_grad(g, q, params, s, flag, st);
     if (rc) return rc;
     AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
-    if (N > 0) {
-      image_reduce_kernel<true><<<(unsigned)ceil_div((int64_t)N * 32, 256), 256, 0, st>>>(
-          g, params, s.pg, nullptr, s.R, ad, flag);
+    const int img_blocks = (int)ceil_div((int64_t)N * 32, 256);
+    const int cam_blocks = (g.refine_focal && g.n_cameras > 0) ? g.n_cam_chunks : 0;
+    if (img_blocks + cam_blocks > 0) {
+      image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), 256, 0, st>>>(
+          g, params, s.pg, nullptr, s.R, s.cpart, img_blocks, ad, flag);
       FM_LAUNCHED(image_reduce_kernel);
     }
     if (g.refine_focal && g.n_cameras > 0) {
-      if (g.n_cam_chunks > 0) {
-        cam_chunk_kernel<<<(unsigned)g.n_cam_chunks, kCamBlock, 0, st>>>(g, s.pg, s.cpart, flag);
-        FM_LAUNCHED(cam_chunk_kernel);
-      }
       cam_final_kernel<true><<<(unsigned)ceil_div(g.n_cameras, 128), 128, 0, st>>>(
           g, params, s.cpart, nullptr, ad, flag);
       FM_LAUNCHED(cam_final_kernel);
@@ -579,16 +590,16 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   // API semantics: evaluate even if `flag` is already set by the caller
   if (int rc = launch_pair_grad(*g, *q, params, s, nullptr, st)) return rc;
   AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, 0};
-  if (N > 0) {
-    image_reduce_kernel<false><<<(unsigned)ceil_div((int64_t)N * 32, 256), 256, 0, st>>>(
-        *g, const_cast<double*>(params), s.pg, grad_out, s.R, none, flag);
-    FM_LAUNCHED(image_reduce_kernel);
+  {
+    const int img_blocks = (int)ceil_div((int64_t)N * 32, 256);
+    const int cam_blocks = (g->refine_focal && g->n_cameras > 0) ? g->n_cam_chunks : 0;
+    if (img_blocks + cam_blocks > 0) {
+      image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), 256, 0, st>>>(
+          *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, img_blocks, none, flag);
+      FM_LAUNCHED(image_reduce_kernel);
+    }
   }
   if (g->refine_focal && g->n_cameras > 0) {
-    if (g->n_cam_chunks > 0) {
-      cam_chunk_kernel<<<(unsigned)g->n_cam_chunks, kCamBlock, 0, st>>>(*g, s.pg, s.cpart, nullptr);
-      FM_LAUNCHED(cam_chunk_kernel);
-    }
     cam_final_kernel<false><<<(unsigned)ceil_div(g->n_cameras, 128), 128, 0, st>>>(
         *g, const_cast<double*>(params), s.cpart, grad_out, none, flag);
     FM_LAUNCHED(cam_final_kernel);

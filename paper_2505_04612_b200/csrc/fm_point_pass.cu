@@ -146,25 +146,36 @@ __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialB
 
 // ------------------------------------------------------------------ hot kernel
 // z == 1.  Persistent warps walk their work items (static round robin) while
-// lane 0 streams the items' coordinates into a per-warp ring of kStages
-// shared-memory stages with 1-D bulk async copies (cp.async.bulk -> UBLKCP,
-// completion on an mbarrier): kStages x 2 KB in flight per warp without
-// holding registers, and the next item's data arrives while the current
-// item's warp reduction runs.
+// lane 0 streams the items' coordinates and mask words into a per-warp ring
+// of kStages shared-memory stages with 1-D bulk async copies (cp.async.bulk ->
+// UBLKCP, completion on an mbarrier with expect_tx): 2 KB per stage, 8 KB per
+// warp in flight without holding registers; the next item streams in while
+// the current item's reduction runs.  A stage is consumed with 4, 2 or 1
+// points per lane (the item tail of C2's 400-point pairs uses a narrow
+// iteration instead of a 128-slot one).  Per-lane partials are reduced
+// through shared memory in a fixed order (lane-major rows summed
+// sequentially), so results are bitwise reproducible.
 //
 // MOM64 = true (default, exact): the 36 Kronecker moments accumulate in fp64,
 // so W matches the reference's fp64 W to rounding -- the IRLS quadratic form
 // is ill-conditioned and fp32 moments visibly move the optimum.
 // MOM64 = false (opt-in fast mode): fp32 moments with packed FFMA2 plus the
 // shifted-model linearisation terms vgrad / s0.
-constexpr int kStages = 4;
-constexpr int kStageSlots = 128;
+constexpr int kStages = 3;
+constexpr int kStageSlots = 256;
+constexpr int kSubSlots = 128;  // slots per 4-points-per-lane sub-iteration
+constexpr int kMaskWords = 12;
 constexpr int kHotWarps = 4;
+constexpr int kRedRow = 33;   // padded row of the smem reduction (bank spread)
+constexpr int kRed64 = 38;    // 36 moments + count + L1
+constexpr int kRed32 = 47;    // 36 moments + 9 vgrad + count + s0
 
 struct HotWarpSmem {
   float2 x1[kStages][kStageSlots];
   float2 x2[kStages][kStageSlots];
+  uint32_t mask[kStages][kMaskWords];
   unsigned long long bar[kStages];
+  double red[((kRed64 + 1) / 2) * kRedRow];  // half the rows per phase (floats: 24 rows)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -194,30 +205,178 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase)
       "r"(phase)
       : "memory");
 }
+// x if keep else +0.0, as an integer AND so the compiler cannot hoist the
+// fp64 conversion above it (non-finite data on dropped points stays out).
+__device__ __forceinline__ float keep_or_zero(float x, unsigned keep_mask) {
+  return __uint_as_float(__float_as_uint(x) & keep_mask);
+}
 
 struct ItemDesc {
-  int64_t lo;  // first slot
-  int len;     // points in the item
-  int n;       // image pair
-  int nst;     // stages (0 if the pair is skipped)
+  int64_t lo;   // first slot
+  int len;      // points in the item
+  int n;        // image pair
+  int nst;      // stages (0 if the pair is skipped)
+  bool single;  // the pair is one work item
 };
 
-template <bool kSkip>
-__device__ __forceinline__ ItemDesc load_item(const fm_point_store& s, int64_t k,
-                                              const int32_t* __restrict__ prev_active) {
+// Descriptor {lo (2 x int32), len, n | single << 31} -> ItemDesc (no stage count yet).
+__device__ __forceinline__ ItemDesc decode_item(int4 q) {
   ItemDesc d;
-  d.n = s.item_pair[k];
-  const int c = (int)(k - s.pair_item_off[d.n]);
-  d.lo = s.pair_off[d.n] + (int64_t)c * s.chunk;
-  const int64_t rem = (int64_t)s.pair_len[d.n] - (int64_t)c * s.chunk;
-  d.len = (int)(rem < s.chunk ? rem : s.chunk);
+  d.lo = (int64_t)(uint32_t)q.x | ((int64_t)q.y << 32);
+  d.len = q.z;
+  d.n = q.w & 0x7fffffff;
+  d.single = (q.w >> 31) & 1;
   d.nst = (d.len + kStageSlots - 1) / kStageSlots;
-  if (kSkip && prev_active[d.n] == 0) d.nst = 0;
   return d;
 }
 
+__device__ __forceinline__ int4 ld_desc(const int32_t* desc, int64_t k) {
+  return __ldg(reinterpret_cast<const int4*>(desc) + k);
+}
+
+__global__ void describe_items_kernel(const fm_point_store s, int32_t* __restrict__ desc) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= s.n_items) return;
+  const int n = s.item_pair[k];
+  const int first = s.pair_item_off[n];
+  const int c = (int)(k - first);
+  const int64_t lo = s.pair_off[n] + (int64_t)c * s.chunk;
+  const int64_t rem = (int64_t)s.pair_len[n] - (int64_t)c * s.chunk;
+  const int len = (int)(rem < s.chunk ? rem : s.chunk);
+  const bool single = (s.pair_item_off[n + 1] - first) == 1;
+  int4 q;
+  q.x = (int)(uint32_t)(lo & 0xffffffffll);
+  q.y = (int)(lo >> 32);
+  q.z = len;
+  q.w = n | (single ? (int)0x80000000 : 0);
+  reinterpret_cast<int4*>(desc)[k] = q;
+}
+
+template <bool kPrune, bool kL1, bool kMom, bool MOM64>
+struct HotAcc {
+  double M64[MOM64 ? 36 : 1];
+  float2 M2[MOM64 ? 1 : 18];
+  float2 V0, V1, V2, V3;
+  float v22, s0f;
+  double l1;
+  int cnt;
+
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < (MOM64 ? 36 : 1); ++k) M64[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < (MOM64 ? 1 : 18); ++k) M2[k] = f2(0.f);
+    V0 = V1 = V2 = V3 = f2(0.f);
+    v22 = s0f = 0.f;
+    l1 = 0.0;
+    cnt = 0;
+  }
+
+  // one point pair; returns the post-prune keep flag
+  __device__ __forceinline__ bool point(const double (&G)[9], float2 X1, float2 X2, bool act,
+                                        double thr) {
+    // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
+    const double a = X1.x, bb = X1.y, c = X2.x, dd = X2.y;
+    const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
+    const double y1 = fma(G[3], a, fma(G[4], bb, G[5]));
+    const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
+    const double r = fma(c, y0, fma(dd, y1, y2));
+    const double ar = fabs(r);
+    const bool keep = kPrune ? (act && ar <= thr) : act;
+    cnt += keep;
+    if (kL1) l1 += act ? ar : 0.0;
+    if (kMom) {
+      // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); a per-point relative
+      // error of the weight keeps every term rank-1 exact.
+      const unsigned km = keep ? 0xffffffffu : 0u;
+      const float wf = keep_or_zero(rcp_approx(fmaxf((float)ar, 1e-6f)), km);
+      const float2 Y1 = make_float2(keep_or_zero(X1.x, km), keep_or_zero(X1.y, km));
+      const float2 Y2 = make_float2(keep_or_zero(X2.x, km), keep_or_zero(X2.y, km));
+      if (MOM64) {
+        const double w = wf;
+        const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
+        const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
+        const double wc = w * kc, wd = w * kd;
+        const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int j = 0; j < 6; ++j) M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
+      } else {
+        const bool big = ar >= 1e-6;
+        const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
+        s0f += keep ? (big ? (float)ar : (float)(r * r * 1e6)) : 0.f;
+        const float2 wX2 = __fmul2_rn(f2(wf), Y2);
+        const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
+        const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
+        const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
+        const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+          M2[MOM64 ? 0 : p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[MOM64 ? 0 : p * 3 + 0]);
+          M2[MOM64 ? 0 : p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[MOM64 ? 0 : p * 3 + 1]);
+          M2[MOM64 ? 0 : p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[MOM64 ? 0 : p * 3 + 2]);
+        }
+        const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
+        V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
+        V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
+        V2 = __ffma2_rn(f2(wr), Y1, V2);
+        V3 = __fadd2_rn(wrX2, V3);
+        v22 += wr;
+      }
+    }
+    return keep;
+  }
+};
+
+// Consume the sub-block [sb, sb + 32*NPT) of stage st (slot offset so within
+// the stage) with NPT points per lane.
+template <int NPT, bool kPrune, bool kL1, bool kMom, bool MOM64>
+__device__ __forceinline__ void consume_sub(HotAcc<kPrune, kL1, kMom, MOM64>& acc,
+                                            const HotWarpSmem& sm, int st, int so, int64_t stage_b,
+                                            int64_t hi, const double (&G)[9], double thr, int lane,
+                                            uint32_t* __restrict__ active) {
+  const int64_t cb = stage_b + so + (int64_t)NPT * lane;
+  const int64_t left = hi - cb;
+  const int nvalid = left <= 0 ? 0 : (left >= NPT ? NPT : (int)left);
+  // mask words of the stage were copied from word (stage_b >> 5) & ~3 on
+  const unsigned word = sm.mask[st][(int)((cb >> 5) - ((stage_b >> 5) & ~int64_t(3)))];
+  const int shift = (int)(cb & 31);
+  const unsigned valid_bits = (1u << nvalid) - 1u;
+  const unsigned bits = (word >> shift) & valid_bits;
+  const float2* x1 = &sm.x1[st][so];
+  const float2* x2 = &sm.x2[st][so];
+  float2 X1[NPT], X2[NPT];
+  if (NPT == 4) {
+    const float4 a0 = *reinterpret_cast<const float4*>(&x1[4 * lane]);
+    const float4 a1 = *reinterpret_cast<const float4*>(&x1[4 * lane + 2]);
+    const float4 b0 = *reinterpret_cast<const float4*>(&x2[4 * lane]);
+    const float4 b1 = *reinterpret_cast<const float4*>(&x2[4 * lane + 2]);
+    X1[0] = make_float2(a0.x, a0.y); X1[NPT > 1 ? 1 : 0] = make_float2(a0.z, a0.w);
+    X1[NPT > 2 ? 2 : 0] = make_float2(a1.x, a1.y); X1[NPT > 3 ? 3 : 0] = make_float2(a1.z, a1.w);
+    X2[0] = make_float2(b0.x, b0.y); X2[NPT > 1 ? 1 : 0] = make_float2(b0.z, b0.w);
+    X2[NPT > 2 ? 2 : 0] = make_float2(b1.x, b1.y); X2[NPT > 3 ? 3 : 0] = make_float2(b1.z, b1.w);
+  } else if (NPT == 2) {
+    const float4 a0 = *reinterpret_cast<const float4*>(&x1[2 * lane]);
+    const float4 b0 = *reinterpret_cast<const float4*>(&x2[2 * lane]);
+    X1[0] = make_float2(a0.x, a0.y); X1[NPT > 1 ? 1 : 0] = make_float2(a0.z, a0.w);
+    X2[0] = make_float2(b0.x, b0.y); X2[NPT > 1 ? 1 : 0] = make_float2(b0.z, b0.w);
+  } else {
+    X1[0] = x1[lane];
+    X2[0] = x2[lane];
+  }
+  unsigned keep_bits = 0;
+#pragma unroll
+  for (int k = 0; k < NPT; ++k)
+    keep_bits |= (unsigned)acc.point(G, X1[k], X2[k], (bits >> k) & 1u, thr) << k;
+  if (kPrune) {
+    const unsigned cleared = bits & ~keep_bits;
+    if (cleared) atomicAnd(&active[cb >> 5], ~(cleared << shift));
+  }
+}
+
 template <unsigned MODE, bool MOM64>
-__global__ void __launch_bounds__(kHotWarps * 32)
+__global__ void __launch_bounds__(kHotWarps * 32, 3)
 point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                const int32_t* __restrict__ prev_active, const fm_pass_out out,
                const PartialBufs part) {
@@ -235,24 +394,56 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   const int64_t w0 = (int64_t)blockIdx.x * kHotWarps + wib;
   const int64_t P = s.n_pairs;
   const int64_t NI = s.n_items;
+  const int64_t n_words = s.n_slots >> 5;
 
+  {  // stale stage bytes must be finite: zero the ring once
+    float4* z = reinterpret_cast<float4*>(&sm.x1[0][0]);
+    constexpr int n4 = (int)(2 * sizeof(float2) * kStages * kStageSlots / sizeof(float4));
+#pragma unroll
+    for (int k = lane; k < n4; k += 32) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < kStages; ++k) mbar_init(&sm.bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncwarp();
 
   // ---------------------------------------------------------- producer
+  // Streams stages of items w0, w0+W, ...; the descriptor of the item after
+  // the current one is already in flight (registers), so item switches do
+  // not expose a dependent global-load chain.
+  const int32_t* desc = s.item_desc;
   int64_t p_item = w0;
   ItemDesc pd;
-  if (p_item < NI) pd = load_item<kSkip>(s, p_item, prev_active);
+  int4 p_next_q = make_int4(0, 0, 0, 0);
+  // skip flag of the next item: loaded one produce() call after its
+  // descriptor, long before the producer switches to that item
+  int p_next_skip = 0;
+  bool p_next_skip_ready = false;
+  if (p_item < NI) {
+    pd = decode_item(ld_desc(desc, p_item));
+    if (kSkip && prev_active[pd.n] == 0) pd.nst = 0;
+    if (p_item + W < NI) p_next_q = ld_desc(desc, p_item + W);
+  }
   int p_st = 0;
   uint32_t issued = 0;
   auto produce = [&]() {
+    if (kSkip && !p_next_skip_ready && p_item + W < NI) {
+      p_next_skip = prev_active[decode_item(p_next_q).n] == 0;
+      p_next_skip_ready = true;
+    }
     while (p_item < NI && p_st >= pd.nst) {
       p_item += W;
-      if (p_item < NI) pd = load_item<kSkip>(s, p_item, prev_active);
+      if (p_item >= NI) break;
+      pd = decode_item(p_next_q);
+      if (kSkip) {
+        if (!p_next_skip_ready) p_next_skip = prev_active[pd.n] == 0;
+        if (p_next_skip) pd.nst = 0;
+        p_next_skip_ready = false;
+      }
+      if (p_item + W < NI) p_next_q = ld_desc(desc, p_item + W);
       p_st = 0;
     }
     if (p_item >= NI) return;
@@ -260,11 +451,15 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
     const int rem = pd.len - p_st * kStageSlots;
     const int nsl = rem < kStageSlots ? ((rem + 3) & ~3) : kStageSlots;
     const uint32_t bytes = (uint32_t)nsl * 8u;
+    const int64_t mw = (b >> 5) & ~int64_t(3);
+    const int64_t mwords = n_words - mw < kMaskWords ? n_words - mw : kMaskWords;
+    const uint32_t mbytes = (uint32_t)mwords * 4u;
     const int st = issued % kStages;
     if (lane == 0) {
-      mbar_expect_tx(&sm.bar[st], 2u * bytes);
+      mbar_expect_tx(&sm.bar[st], 2u * bytes + mbytes);
       bulk_g2s(&sm.x1[st][0], s.x1 + 2 * b, bytes, &sm.bar[st]);
       bulk_g2s(&sm.x2[st][0], s.x2 + 2 * b, bytes, &sm.bar[st]);
+      bulk_g2s(&sm.mask[st][0], s.active + mw, mbytes, &sm.bar[st]);
     }
     ++issued;
     ++p_st;
@@ -273,191 +468,169 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   for (int k = 0; k < kStages; ++k) produce();
 
   // ---------------------------------------------------------- consumer
+  // Also one item ahead: the next descriptor, its skip flag and its ghat
+  // (lanes 0..8 hold one component each) are loaded while this item runs.
   uint32_t consumed = 0;
+  HotAcc<kPrune, kL1, kMom, MOM64> acc;
+  int4 c_q = w0 < NI ? ld_desc(desc, w0) : make_int4(0, 0, 0, 0);
+  double g_mine = 0.0;  // lane k < 9: component k of the current item's ghat
+  int c_skip = 0;
+  if (w0 < NI) {
+    const ItemDesc d0 = decode_item(c_q);
+    if (lane < 9) g_mine = ghat[lane * P + d0.n];
+    if (kSkip) c_skip = prev_active[d0.n] == 0;
+  }
 #pragma unroll 1
   for (int64_t item = w0; item < NI; item += W) {
-    const ItemDesc d = load_item<kSkip>(s, item, prev_active);
-    const bool single = (s.pair_item_off[d.n + 1] - s.pair_item_off[d.n]) == 1;
+    ItemDesc d = decode_item(c_q);
+    if (kSkip && c_skip) d.nst = 0;
+    const bool single = d.single;
     double G[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) G[k] = d.nst ? ghat[k * P + d.n] : 0.0;
-
-    double M64[MOM64 ? 36 : 1];
-    float2 M2[MOM64 ? 1 : 18];
-    float2 V0, V1, V2, V3;
-    float v22 = 0.f, s0f = 0.f;
-    if (MOM64) {
-#pragma unroll
-      for (int k = 0; k < (MOM64 ? 36 : 1); ++k) M64[k] = 0.0;
-    } else {
-#pragma unroll
-      for (int k = 0; k < (MOM64 ? 1 : 18); ++k) M2[k] = f2(0.f);
-    }
-    V0 = V1 = V2 = V3 = f2(0.f);
-    double l1 = 0.0;
-    int cnt = 0;
+    for (int k = 0; k < 9; ++k) G[k] = __shfl_sync(0xffffffffu, g_mine, k);
+    // prefetch the next item (descriptor, then its ghat / skip flag)
+    int4 n_q = make_int4(0, 0, 0, 0);
+    if (item + W < NI) n_q = ld_desc(desc, item + W);
+    acc.zero();
     const int64_t hi = d.lo + d.len;
-
+    bool next_loaded = false;
+    double g_next = 0.0;
+    int skip_next = 0;
 #pragma unroll 1
     for (int st_i = 0; st_i < d.nst; ++st_i) {
       const int st = consumed % kStages;
       const uint32_t phase = (consumed / kStages) & 1u;
-      const int64_t cb = d.lo + (int64_t)st_i * kStageSlots + 4 * lane;
-      const int shift = (int)(cb & 31);
-      const unsigned bits = cb < hi ? ((s.active[cb >> 5] >> shift) & 0xFu) : 0u;
+      const int64_t sb = d.lo + (int64_t)st_i * kStageSlots;
+      const int64_t rem = hi - sb;
       mbar_wait(&sm.bar[st], phase);
-      const float4 q1a = *reinterpret_cast<const float4*>(&sm.x1[st][4 * lane]);
-      const float4 q1b = *reinterpret_cast<const float4*>(&sm.x1[st][4 * lane + 2]);
-      const float4 q2a = *reinterpret_cast<const float4*>(&sm.x2[st][4 * lane]);
-      const float4 q2b = *reinterpret_cast<const float4*>(&sm.x2[st][4 * lane + 2]);
+      if (!next_loaded && item + W < NI) {  // the descriptor has arrived by now
+        const ItemDesc dn = decode_item(n_q);
+        if (lane < 9) g_next = ghat[lane * P + dn.n];
+        if (kSkip) skip_next = prev_active[dn.n] == 0;
+        next_loaded = true;
+      }
+#pragma unroll 1
+      for (int so = 0; so < kStageSlots && rem > so; so += kSubSlots) {
+        const int64_t r = rem - so;
+        if (r > 64) {
+          consume_sub<4>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
+        } else if (r > 32) {
+          consume_sub<2>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
+        } else {
+          consume_sub<1>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
+        }
+      }
       __syncwarp();
       ++consumed;
       produce();  // refill the stage just drained
-
-      unsigned keep_bits = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float4& q1 = k < 2 ? q1a : q1b;
-        const float4& q2 = k < 2 ? q2a : q2b;
-        const float2 X1 = (k & 1) ? make_float2(q1.z, q1.w) : make_float2(q1.x, q1.y);
-        const float2 X2 = (k & 1) ? make_float2(q2.z, q2.w) : make_float2(q2.x, q2.y);
-        const bool act = (cb + k < hi) && ((bits >> k) & 1u);
-        // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
-        const double a = X1.x, bb = X1.y, c = X2.x, dd = X2.y;
-        const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
-        const double y1 = fma(G[3], a, fma(G[4], bb, G[5]));
-        const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
-        const double r = fma(c, y0, fma(dd, y1, y2));
-        const double ar = fabs(r);
-        const bool keep = kPrune ? (act && ar <= thr) : act;
-        keep_bits |= (unsigned)keep << k;
-        cnt += keep;
-        if (kL1) l1 += act ? ar : 0.0;
-        if (kMom) {
-          // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); a per-point
-          // relative error of the weight keeps each term rank-1 exact.
-          // Dropped / padding / stale-stage slots are zeroed by select (not by
-          // a zero weight: 0 * NaN would poison the sums).
-          const float wf = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
-          const float2 Y1 = keep ? X1 : f2(0.f);
-          const float2 Y2 = keep ? X2 : f2(0.f);
-          if (MOM64) {
-            const double w = wf;
-            const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
-            const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
-            const double wc = w * kc, wd = w * kd;
-            const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
-            // canonical sym order {00,01,02,11,12,22} for both factors
-#pragma unroll
-            for (int i = 0; i < 6; ++i)
-#pragma unroll
-              for (int j = 0; j < 6; ++j) M64[i * 6 + j] = fma(B[i], A[j], M64[i * 6 + j]);
-          } else {
-            const bool big = ar >= 1e-6;
-            const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
-            s0f += keep ? (big ? (float)ar : (float)(r * r * 1e6)) : 0.f;
-            const float2 wX2 = __fmul2_rn(f2(wf), Y2);
-            const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
-            const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
-            const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
-            const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
-#pragma unroll
-            for (int p = 0; p < 6; ++p) {
-              M2[p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[p * 3 + 0]);
-              M2[p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[p * 3 + 1]);
-              M2[p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[p * 3 + 2]);
-            }
-            const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
-            V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
-            V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
-            V2 = __ffma2_rn(f2(wr), Y1, V2);
-            V3 = __fadd2_rn(wrX2, V3);
-            v22 += wr;
-          }
-        }
-      }
-      if (kPrune) {
-        const unsigned cleared = bits & ~keep_bits & 0xFu;
-        if (cleared) atomicAnd(&s.active[cb >> 5], ~(cleared << shift));
-      }
     }
+    if (!next_loaded && item + W < NI) {
+      const ItemDesc dn = decode_item(n_q);
+      if (lane < 9) g_next = ghat[lane * P + dn.n];
+      if (kSkip) skip_next = prev_active[dn.n] == 0;
+    }
+    c_q = n_q;
+    g_mine = g_next;
+    c_skip = skip_next;
 
     // ------------------------------------------------------------ reduce
+    // lane-major rows in smem, each lane sums rows in a fixed order
     if (kMom && MOM64) {
-      double v[48];
+      double* red = sm.red;
+      constexpr int kHalf = (kRed64 + 1) / 2;  // 19 rows per phase
 #pragma unroll
-      for (int k = 0; k < 36; ++k) v[k] = M64[k];
-      v[36] = (double)cnt;
-      v[37] = l1;
+      for (int ph = 0; ph < 2; ++ph) {
 #pragma unroll
-      for (int k = 38; k < 48; ++k) v[k] = 0.0;
-      warp_transpose_reduce48(v, lane);
-      if ((lane & 1) == 0) {
-        const int rb = red_base48(lane);
+        for (int k = 0; k < kHalf; ++k) {
+          const int row = ph * kHalf + k;
+          const double val = row < 36 ? acc.M64[MOM64 ? (row < 36 ? row : 0) : 0]
+                                      : (row == 36 ? (double)acc.cnt : acc.l1);
+          red[k * kRedRow + lane] = val;
+        }
+        __syncwarp();
+        if (lane < kHalf) {
+          const int k = ph * kHalf + lane;
+          double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
 #pragma unroll
-        for (int h = 0; h < 3; ++h) {
-          const int k = rb + h;
-          if (k >= 38) continue;
+          for (int j = 0; j < 32; j += 4) {
+            t0 += red[lane * kRedRow + j];
+            t1 += red[lane * kRedRow + j + 1];
+            t2 += red[lane * kRedRow + j + 2];
+            t3 += red[lane * kRedRow + j + 3];
+          }
+          const double t = (t0 + t1) + (t2 + t3);
           if (!single) {
-            if (k < 36) static_cast<double*>(part.red)[k * NI + item] = v[h];
-            else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = v[h];
-            else part.l1[item] = v[h];
+            if (k < 36) static_cast<double*>(part.red)[k * NI + item] = t;
+            else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = t;
+            else part.l1[item] = t;
           } else if (k < 36) {
-            out.mom64[k * P + d.n] = v[h];
+            out.mom64[k * P + d.n] = t;
           } else if (k == 36) {
-            if (out.n_active) out.n_active[d.n] = (int32_t)v[h];
+            if (out.n_active) out.n_active[d.n] = (int32_t)t;
           } else if (kL1 && out.l1) {
-            out.l1[d.n] = v[h];
+            out.l1[d.n] = t;
           }
         }
+        __syncwarp();
       }
-    } else {
-      if (kMom) {
-        float v[48];
+    } else if (kMom) {
+      float* red = reinterpret_cast<float*>(sm.red);
+      constexpr int kHalf = (kRed32 + 1) / 2;  // 24 rows per phase
+      const float vv[11] = {acc.V0.x, acc.V0.y, acc.V1.x, acc.V1.y, acc.V2.x, acc.V2.y,
+                            acc.V3.x, acc.V3.y, acc.v22, (float)acc.cnt, acc.s0f};
 #pragma unroll
-        for (int k = 0; k < 18; ++k) {
-          v[2 * k] = M2[MOM64 ? 0 : k].x;
-          v[2 * k + 1] = M2[MOM64 ? 0 : k].y;
+      for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll
+        for (int k = 0; k < kHalf; ++k) {
+          const int row = ph * kHalf + k;
+          if (row >= kRed32) break;
+          const float val = row < 36 ? ((row & 1) ? acc.M2[MOM64 ? 0 : (row < 36 ? row / 2 : 0)].y
+                                                  : acc.M2[MOM64 ? 0 : (row < 36 ? row / 2 : 0)].x)
+                                     : vv[row - 36 < 11 ? row - 36 : 0];
+          red[k * kRedRow + lane] = val;
         }
-        v[36] = V0.x; v[37] = V0.y; v[38] = V1.x; v[39] = V1.y;
-        v[40] = V2.x; v[41] = V2.y; v[42] = V3.x; v[43] = V3.y;
-        v[44] = v22;
-        v[45] = (float)cnt;
-        v[46] = s0f;
-        v[47] = 0.f;
-        warp_transpose_reduce48(v, lane);
-        if ((lane & 1) == 0) {
-          const int rb = red_base48(lane);
+        __syncwarp();
+        const int vi = ph * kHalf + lane;
+        if (lane < kHalf && vi < kRed32) {
+          float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
 #pragma unroll
-          for (int h = 0; h < 3; ++h) {
-            const int vi = rb + h;
-            if (vi == 46) {
-              if (single) out.s0[d.n] = (double)v[h];
-              else part.s0[item] = (double)v[h];
-              continue;
-            }
-            const int k = hot_out_index(vi);
-            if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, v[h], kLin);
+          for (int j = 0; j < 32; j += 4) {
+            t0 += red[lane * kRedRow + j];
+            t1 += red[lane * kRedRow + j + 1];
+            t2 += red[lane * kRedRow + j + 2];
+            t3 += red[lane * kRedRow + j + 3];
           }
-        }
-      } else {
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) {
-          if (single) {
-            if (out.n_active) out.n_active[d.n] = cnt;
+          const float t = (t0 + t1) + (t2 + t3);
+          if (vi == 46) {
+            if (single) out.s0[d.n] = (double)t;
+            else part.s0[item] = (double)t;
           } else {
-            static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
+            const int k = hot_out_index(vi);
+            if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, t, kLin);
           }
         }
+        __syncwarp();
       }
       if (kL1) {
-        l1 = warp_sum(l1);
+        const double l1 = warp_sum(acc.l1);
         if (lane == 0) {
           if (single) {
             if (out.l1) out.l1[d.n] = l1;
           } else {
             part.l1[item] = l1;
           }
+        }
+      }
+    } else {
+      const int cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
+      const double l1 = kL1 ? warp_sum(acc.l1) : 0.0;
+      if (lane == 0) {
+        if (single) {
+          if (out.n_active) out.n_active[d.n] = cnt;
+          if (kL1 && out.l1) out.l1[d.n] = l1;
+        } else {
+          static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
+          if (kL1) part.l1[item] = l1;
         }
       }
     }
@@ -659,6 +832,7 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
                const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
   static int blocks_per_sm = 0;
   const size_t smem = kHotWarps * sizeof(HotWarpSmem);
+  static_assert(sizeof(HotWarpSmem) % 128 == 0 || true, "");
   if (!blocks_per_sm) {
     FM_CUDA(cudaFuncSetAttribute(point_pass_hot<MODE, MOM64>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -762,7 +936,17 @@ extern "C" {
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store) {
   if (!store) return 0;
   const size_t ni = (size_t)store->n_items;
-  return scratch_round(ni * kNumRed * sizeof(double)) + 2 * scratch_round(ni * sizeof(double)) + 256;
+  return scratch_round(ni * kNumRed * sizeof(double)) + 2 * scratch_round(ni * sizeof(double)) +
+         scratch_round(ni * 4 * sizeof(int32_t)) + 256;
+}
+
+int fm_point_store_describe(const fm_point_store* store, void* stream) {
+  FM_REQUIRE(store && store->item_desc, "null store or item_desc");
+  if (store->n_items == 0) return FM_OK;
+  describe_items_kernel<<<(unsigned)ceil_div(store->n_items, 256), 256, 0, as_stream(stream)>>>(
+      *store, store->item_desc);
+  FM_LAUNCHED(describe_items_kernel);
+  return FM_OK;
 }
 
 int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, const double* ghat,
@@ -793,20 +977,28 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
   }
   PartialBufs part{nullptr, nullptr, nullptr};
-  if (s.n_items > s.n_pairs) {
-    Scratch sc(scratch, scratch_bytes);
-    part.red = sc.take<double>((size_t)s.n_items * kNumRed);
-    part.s0 = sc.take<double>((size_t)s.n_items);
-    part.l1 = sc.take<double>((size_t)s.n_items);
-    FM_REQUIRE(scratch && sc.ok(), "point-pass scratch too small (%zu < %zu)", scratch_bytes, sc.used);
-  }
   cudaStream_t st = as_stream(stream);
+  fm_point_store s2 = s;  // with item descriptors
+  {
+    Scratch sc(scratch, scratch_bytes);
+    if (s.n_items > s.n_pairs) {
+      part.red = sc.take<double>((size_t)s.n_items * kNumRed);
+      part.s0 = sc.take<double>((size_t)s.n_items);
+      part.l1 = sc.take<double>((size_t)s.n_items);
+    }
+    if (!s.item_desc) {
+      s2.item_desc = sc.take<int32_t>((size_t)s.n_items * 4);
+      if (int rc = fm_point_store_describe(&s2, stream)) return rc;
+    }
+    FM_REQUIRE((sc.used == 0 || scratch) && sc.ok(), "point-pass scratch too small (%zu < %zu)",
+               scratch_bytes, sc.used);
+  }
   if (!homog) {
     // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
     const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
     bool handled = false;
     if (hot_f64 || (m & FM_PASS_IRLS)) {
-      const int rc = dispatch_hot(m, hot_f64, s, threshold, ghat, prev_active, *out, part, st, &handled);
+      const int rc = dispatch_hot(m, hot_f64, s2, threshold, ghat, prev_active, *out, part, st, &handled);
       if (handled) return rc;
     }
   }

@@ -142,7 +142,11 @@ class PointPairStore:
                 x1=self.x1.data_ptr(), x2=self.x2.data_ptr(),
                 x1z=self.x1z.data_ptr() if self.x1z is not None else None,
                 x2z=self.x2z.data_ptr() if self.x2z is not None else None,
-                active=self.active.data_ptr())
+                active=self.active.data_ptr(), item_desc=None)
+            self.item_desc_d = torch.empty((max(self.n_items, 1), 4), dtype=torch.int32,
+                                           device=self.device)
+            self._struct.item_desc = self.item_desc_d.data_ptr()
+            N.check(N.lib().fm_point_store_describe(ctypes.byref(self._struct), N.stream_handle()))
         return self._struct
 
     def scratch(self):

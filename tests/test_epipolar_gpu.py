@@ -260,3 +260,41 @@ def test_nonfinite_pose_is_pruned_like_reference(golden_small):
     poses.centers[:] = np.nan
     with pytest.raises(ValueError, match="all pairs pruned away"):
         E.irls_refine(poses, pairs, Cfg(), n_cameras=1)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_nonfinite_inactive_points_do_not_poison_moments(precision):
+    """Inactive points may hold NaN/inf (the reference only reads active ones,
+    ref/epipolar.py:297-301); the fused pass must ignore them."""
+    poses, pairs = random_scene(n_images=5, n_points=300, seed=9)
+    rng = np.random.default_rng(4)
+    for p in pairs:
+        bad = rng.random(len(p.x1)) < 0.1
+        p.active &= ~bad
+        p.x1[bad, 0] = np.nan
+        p.x2[bad, 1] = np.inf
+    n = len(poses.rotations)
+    st = E.AdjustmentState.from_poses(poses, list(range(n)), 2, True)
+    dev = torch.device("cuda")
+    store = PointPairStore.from_pairs(pairs, device=dev)
+    o = store.order
+    ii, jj, ci, cj = E._pair_indices(st, pairs)
+    graph = PairGraph(ii[o], jj[o], ci[o], cj[o], n, 2, True, device=dev)
+    eng = E.IrlsEngine(store, graph, torch.as_tensor(st.pack(), device=dev), Cfg(),
+                       precision=precision)
+    eng._ghat()
+    eng.point_pass(N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS, 0.02, 1, 0)
+    P = len(pairs)
+    sp = [pairs[q] for q in o]
+    flat = O.FlatPairs.from_pairs(sp)
+    flat.x1 = np.nan_to_num(flat.x1, nan=0.0, posinf=0.0)
+    flat.x2 = np.nan_to_num(flat.x2, nan=0.0, posinf=0.0)
+    gh = O.pair_forward(st.pack(), n, ii[o], jj[o], ci[o], cj[o], True)["ghat"]
+    ref = O.point_pass(flat, gh, threshold=0.02)
+    mom = (eng.buf.mom64 if precision == "fp64" else eng.buf.mom32).cpu().numpy()[:, :P]
+    assert np.all(np.isfinite(mom))
+    W = E.moments_to_weights(mom)
+    scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
+    assert np.max(np.abs(W - ref["W"]) / scale) < (3e-7 if precision == "fp64" else 2e-5)
+    assert np.array_equal(eng.buf.n_active[1].cpu().numpy()[:P], ref["n_active"])
+    assert np.all(np.isfinite(eng.buf.l1.cpu().numpy()[:P]))
