@@ -22,6 +22,9 @@
 // (fma.rn.f32x2: two FMAs per issue slot).  Warp totals come from a
 // fixed-order transpose reduction -- no floating-point atomics, so results are
 // bitwise reproducible run to run.
+#include <cmath>
+#include <cstdlib>
+
 #include "fm_common.cuh"
 
 namespace fm {
@@ -145,93 +148,60 @@ __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialB
 }
 
 // ------------------------------------------------------------------ hot kernel
-// z == 1.  Persistent warps walk their work items (static round robin) while
-// lane 0 streams the items' coordinates and mask words into a per-warp ring
-// of kStages shared-memory stages with 1-D bulk async copies (cp.async.bulk ->
-// UBLKCP, completion on an mbarrier with expect_tx): 2 KB per stage, 8 KB per
-// warp in flight without holding registers; the next item streams in while
-// the current item's reduction runs.  A stage is consumed with 4, 2 or 1
-// points per lane (the item tail of C2's 400-point pairs uses a narrow
-// iteration instead of a 128-slot one).  Per-lane partials are reduced
-// through shared memory in a fixed order (lane-major rows summed
-// sequentially), so results are bitwise reproducible.
+// z == 1.  A warp works on 32/L consecutive work items at once: L lanes per
+// item (an item is a <= chunk-slot slice of one image pair).  Each lane owns
+// every L-th 4-slot group of its item and streams it through a private
+// per-lane ring of kRing shared-memory stages with cp.async (LDGSTS, 16-byte
+// L2-only copies, one commit group per iteration), so kRing x 64 B per lane
+// are in flight without holding registers.  Per-item totals need only
+// log2(L) butterfly levels across the item's lanes (fixed order -> bitwise
+// reproducible), instead of a 32-lane reduction per item.
 //
 // MOM64 = true (default, exact): the 36 Kronecker moments accumulate in fp64,
 // so W matches the reference's fp64 W to rounding -- the IRLS quadratic form
 // is ill-conditioned and fp32 moments visibly move the optimum.
 // MOM64 = false (opt-in fast mode): fp32 moments with packed FFMA2 plus the
 // shifted-model linearisation terms vgrad / s0.
-constexpr int kStages = 3;
-constexpr int kStageSlots = 256;
-constexpr int kSubSlots = 128;  // slots per 4-points-per-lane sub-iteration
-constexpr int kMaskWords = 12;
-constexpr int kHotWarps = 4;
-constexpr int kRedRow = 33;   // padded row of the smem reduction (bank spread)
-constexpr int kRed64 = 38;    // 36 moments + count + L1
-constexpr int kRed32 = 47;    // 36 moments + 9 vgrad + count + s0
+constexpr int kRing = 6;        // stages per lane
+constexpr int kGrpWarps = 4;    // warps per block
+constexpr int kStageSlots = 128;  // (descriptor decode only)
 
-struct HotWarpSmem {
-  float2 x1[kStages][kStageSlots];
-  float2 x2[kStages][kStageSlots];
-  uint32_t mask[kStages][kMaskWords];
-  unsigned long long bar[kStages];
-  double red[((kRed64 + 1) / 2) * kRedRow];  // half the rows per phase (floats: 24 rows)
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(phase)
-      : "memory");
-}
 // x if keep else +0.0, as an integer AND so the compiler cannot hoist the
 // fp64 conversion above it (non-finite data on dropped points stays out).
 __device__ __forceinline__ float keep_or_zero(float x, unsigned keep_mask) {
   return __uint_as_float(__float_as_uint(x) & keep_mask);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 struct ItemDesc {
   int64_t lo;   // first slot
   int len;      // points in the item
   int n;        // image pair
-  int nst;      // stages (0 if the pair is skipped)
   bool single;  // the pair is one work item
 };
 
-// Descriptor {lo (2 x int32), len, n | single << 31} -> ItemDesc (no stage count yet).
+// Descriptor {lo (2 x int32), len, n | single << 31} -> ItemDesc.
 __device__ __forceinline__ ItemDesc decode_item(int4 q) {
   ItemDesc d;
   d.lo = (int64_t)(uint32_t)q.x | ((int64_t)q.y << 32);
   d.len = q.z;
   d.n = q.w & 0x7fffffff;
   d.single = (q.w >> 31) & 1;
-  d.nst = (d.len + kStageSlots - 1) / kStageSlots;
   return d;
-}
-
-__device__ __forceinline__ int4 ld_desc(const int32_t* desc, int64_t k) {
-  return __ldg(reinterpret_cast<const int4*>(desc) + k);
 }
 
 __global__ void describe_items_kernel(const fm_point_store s, int32_t* __restrict__ desc) {
@@ -288,10 +258,12 @@ struct HotAcc {
     if (kMom) {
       // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); a per-point relative
       // error of the weight keeps every term rank-1 exact.
-      const unsigned km = keep ? 0xffffffffu : 0u;
-      const float wf = keep_or_zero(rcp_approx(fmaxf((float)ar, 1e-6f)), km);
-      const float2 Y1 = make_float2(keep_or_zero(X1.x, km), keep_or_zero(X1.y, km));
-      const float2 Y2 = make_float2(keep_or_zero(X2.x, km), keep_or_zero(X2.y, km));
+      // Coordinates of every slot are finite (the store builders zero and
+      // deactivate non-finite points), so a zero weight removes a dropped
+      // point exactly without selecting its coordinates.
+      const float wf = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
+      const float2 Y1 = X1;
+      const float2 Y2 = X2;
       if (MOM64) {
         const double w = wf;
         const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
@@ -301,7 +273,8 @@ struct HotAcc {
 #pragma unroll
         for (int i = 0; i < 6; ++i)
 #pragma unroll
-          for (int j = 0; j < 6; ++j) M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
+          for (int j = 0; j < 6; ++j)
+            M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
       } else {
         const bool big = ar >= 1e-6;
         const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
@@ -329,54 +302,30 @@ struct HotAcc {
   }
 };
 
-// Consume the sub-block [sb, sb + 32*NPT) of stage st (slot offset so within
-// the stage) with NPT points per lane.
-template <int NPT, bool kPrune, bool kL1, bool kMom, bool MOM64>
-__device__ __forceinline__ void consume_sub(HotAcc<kPrune, kL1, kMom, MOM64>& acc,
-                                            const HotWarpSmem& sm, int st, int so, int64_t stage_b,
-                                            int64_t hi, const double (&G)[9], double thr, int lane,
-                                            uint32_t* __restrict__ active) {
-  const int64_t cb = stage_b + so + (int64_t)NPT * lane;
-  const int64_t left = hi - cb;
-  const int nvalid = left <= 0 ? 0 : (left >= NPT ? NPT : (int)left);
-  // mask words of the stage were copied from word (stage_b >> 5) & ~3 on
-  const unsigned word = sm.mask[st][(int)((cb >> 5) - ((stage_b >> 5) & ~int64_t(3)))];
-  const int shift = (int)(cb & 31);
-  const unsigned valid_bits = (1u << nvalid) - 1u;
-  const unsigned bits = (word >> shift) & valid_bits;
-  const float2* x1 = &sm.x1[st][so];
-  const float2* x2 = &sm.x2[st][so];
-  float2 X1[NPT], X2[NPT];
-  if (NPT == 4) {
-    const float4 a0 = *reinterpret_cast<const float4*>(&x1[4 * lane]);
-    const float4 a1 = *reinterpret_cast<const float4*>(&x1[4 * lane + 2]);
-    const float4 b0 = *reinterpret_cast<const float4*>(&x2[4 * lane]);
-    const float4 b1 = *reinterpret_cast<const float4*>(&x2[4 * lane + 2]);
-    X1[0] = make_float2(a0.x, a0.y); X1[NPT > 1 ? 1 : 0] = make_float2(a0.z, a0.w);
-    X1[NPT > 2 ? 2 : 0] = make_float2(a1.x, a1.y); X1[NPT > 3 ? 3 : 0] = make_float2(a1.z, a1.w);
-    X2[0] = make_float2(b0.x, b0.y); X2[NPT > 1 ? 1 : 0] = make_float2(b0.z, b0.w);
-    X2[NPT > 2 ? 2 : 0] = make_float2(b1.x, b1.y); X2[NPT > 3 ? 3 : 0] = make_float2(b1.z, b1.w);
-  } else if (NPT == 2) {
-    const float4 a0 = *reinterpret_cast<const float4*>(&x1[2 * lane]);
-    const float4 b0 = *reinterpret_cast<const float4*>(&x2[2 * lane]);
-    X1[0] = make_float2(a0.x, a0.y); X1[NPT > 1 ? 1 : 0] = make_float2(a0.z, a0.w);
-    X2[0] = make_float2(b0.x, b0.y); X2[NPT > 1 ? 1 : 0] = make_float2(b0.z, b0.w);
-  } else {
-    X1[0] = x1[lane];
-    X2[0] = x2[lane];
-  }
-  unsigned keep_bits = 0;
+// Per-lane ring: stage d holds the lane's 4 slots of x1 (2 chunks of 16 B),
+// x2 (2 chunks) and the mask word, laid out chunk-major so that a warp's
+// LDS.128 of chunk k touches 32 consecutive 16-byte words (conflict free).
+struct LaneRing {
+  float4 c[kRing][4][32];   // [stage][chunk: x1 lo, x1 hi, x2 lo, x2 hi][lane]
+  uint32_t m[kRing][32];    // mask word of the lane's first slot pair
+  uint32_t m2[kRing][32];   // mask word of the lane's second slot pair
+};
+
+template <int L>
+__device__ __forceinline__ double group_sum(double x) {
 #pragma unroll
-  for (int k = 0; k < NPT; ++k)
-    keep_bits |= (unsigned)acc.point(G, X1[k], X2[k], (bits >> k) & 1u, thr) << k;
-  if (kPrune) {
-    const unsigned cleared = bits & ~keep_bits;
-    if (cleared) atomicAnd(&active[cb >> 5], ~(cleared << shift));
-  }
+  for (int off = 1; off < L; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+template <int L>
+__device__ __forceinline__ float group_sumf(float x) {
+#pragma unroll
+  for (int off = 1; off < L; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
 }
 
-template <unsigned MODE, bool MOM64>
-__global__ void __launch_bounds__(kHotWarps * 32, 3)
+template <unsigned MODE, bool MOM64, int L>
+__global__ void __launch_bounds__(kGrpWarps * 32, 3)
 point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                const int32_t* __restrict__ prev_active, const fm_pass_out out,
                const PartialBufs part) {
@@ -385,253 +334,170 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
   constexpr bool kLin = kMom && !MOM64;
   constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
+  constexpr int IPW = 32 / L;  // items per warp
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  HotWarpSmem& sm = reinterpret_cast<HotWarpSmem*>(smem_raw)[wib];
-  const int64_t W = (int64_t)gridDim.x * kHotWarps;
-  const int64_t w0 = (int64_t)blockIdx.x * kHotWarps + wib;
+  LaneRing& ring = reinterpret_cast<LaneRing*>(smem_raw)[wib];
   const int64_t P = s.n_pairs;
   const int64_t NI = s.n_items;
-  const int64_t n_words = s.n_slots >> 5;
+  const int g = lane % L;  // lane within the item group
+  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + lane / L;
+  const bool has_item = item < NI;
 
-  {  // stale stage bytes must be finite: zero the ring once
-    float4* z = reinterpret_cast<float4*>(&sm.x1[0][0]);
-    constexpr int n4 = (int)(2 * sizeof(float2) * kStages * kStageSlots / sizeof(float4));
+  ItemDesc d{0, 0, 0, true};
+  if (has_item) d = decode_item(__ldg(reinterpret_cast<const int4*>(s.item_desc) + item));
+  const bool skip = has_item && kSkip && prev_active[d.n] == 0;
+  double G[9];
 #pragma unroll
-    for (int k = lane; k < n4; k += 32) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < kStages; ++k) mbar_init(&sm.bar[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncwarp();
+  for (int k = 0; k < 9; ++k) G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+  // iterations of this group: 4L-slot blocks of the item (same for its lanes)
+  const int len = (has_item && !skip) ? d.len : 0;
+  const int nit = (len + 4 * L - 1) / (4 * L);
+  const int warp_it = __reduce_max_sync(0xffffffffu, nit);
+  const int64_t hi = d.lo + len;
 
-  // ---------------------------------------------------------- producer
-  // Streams stages of items w0, w0+W, ...; the descriptor of the item after
-  // the current one is already in flight (registers), so item switches do
-  // not expose a dependent global-load chain.
-  const int32_t* desc = s.item_desc;
-  int64_t p_item = w0;
-  ItemDesc pd;
-  int4 p_next_q = make_int4(0, 0, 0, 0);
-  // skip flag of the next item: loaded one produce() call after its
-  // descriptor, long before the producer switches to that item
-  int p_next_skip = 0;
-  bool p_next_skip_ready = false;
-  if (p_item < NI) {
-    pd = decode_item(ld_desc(desc, p_item));
-    if (kSkip && prev_active[pd.n] == 0) pd.nst = 0;
-    if (p_item + W < NI) p_next_q = ld_desc(desc, p_item + W);
-  }
-  int p_st = 0;
-  uint32_t issued = 0;
-  auto produce = [&]() {
-    if (kSkip && !p_next_skip_ready && p_item + W < NI) {
-      p_next_skip = prev_active[decode_item(p_next_q).n] == 0;
-      p_next_skip_ready = true;
-    }
-    while (p_item < NI && p_st >= pd.nst) {
-      p_item += W;
-      if (p_item >= NI) break;
-      pd = decode_item(p_next_q);
-      if (kSkip) {
-        if (!p_next_skip_ready) p_next_skip = prev_active[pd.n] == 0;
-        if (p_next_skip) pd.nst = 0;
-        p_next_skip_ready = false;
+  // Iteration `it` of a group covers the 4L-slot block at d.lo + 4L*it; lane g
+  // copies 16-byte chunks g and g + L of each column, so every copy
+  // instruction of the group reads whole 32-byte sectors, and owns slots
+  // {2g, 2g+1} and {2L+2g, 2L+2g+1} of the block.
+  auto issue = [&](int it) {
+    const int st = it % kRing;
+    if (it < nit) {
+      const int64_t blk = d.lo + (int64_t)4 * L * it;
+      const float4* x1 = reinterpret_cast<const float4*>(s.x1 + 2 * blk);
+      const float4* x2 = reinterpret_cast<const float4*>(s.x2 + 2 * blk);
+      // chunks starting at or past the item end are not fetched (they may lie
+      // past the allocation); their stale stage bytes are finite and masked
+      if (blk + 2 * g < hi) {
+        cp_async16(&ring.c[st][0][lane], x1 + g);
+        cp_async16(&ring.c[st][2][lane], x2 + g);
+        cp_async4(&ring.m[st][lane], s.active + ((blk + 2 * g) >> 5));
       }
-      if (p_item + W < NI) p_next_q = ld_desc(desc, p_item + W);
-      p_st = 0;
+      if (blk + 2 * L + 2 * g < hi) {
+        cp_async16(&ring.c[st][1][lane], x1 + g + L);
+        cp_async16(&ring.c[st][3][lane], x2 + g + L);
+        cp_async4(&ring.m2[st][lane], s.active + ((blk + 2 * L + 2 * g) >> 5));
+      }
     }
-    if (p_item >= NI) return;
-    const int64_t b = pd.lo + (int64_t)p_st * kStageSlots;
-    const int rem = pd.len - p_st * kStageSlots;
-    const int nsl = rem < kStageSlots ? ((rem + 3) & ~3) : kStageSlots;
-    const uint32_t bytes = (uint32_t)nsl * 8u;
-    const int64_t mw = (b >> 5) & ~int64_t(3);
-    const int64_t mwords = n_words - mw < kMaskWords ? n_words - mw : kMaskWords;
-    const uint32_t mbytes = (uint32_t)mwords * 4u;
-    const int st = issued % kStages;
-    if (lane == 0) {
-      mbar_expect_tx(&sm.bar[st], 2u * bytes + mbytes);
-      bulk_g2s(&sm.x1[st][0], s.x1 + 2 * b, bytes, &sm.bar[st]);
-      bulk_g2s(&sm.x2[st][0], s.x2 + 2 * b, bytes, &sm.bar[st]);
-      bulk_g2s(&sm.mask[st][0], s.active + mw, mbytes, &sm.bar[st]);
-    }
-    ++issued;
-    ++p_st;
+    cp_async_commit();
   };
-#pragma unroll 1
-  for (int k = 0; k < kStages; ++k) produce();
-
-  // ---------------------------------------------------------- consumer
-  // Also one item ahead: the next descriptor, its skip flag and its ghat
-  // (lanes 0..8 hold one component each) are loaded while this item runs.
-  uint32_t consumed = 0;
-  HotAcc<kPrune, kL1, kMom, MOM64> acc;
-  int4 c_q = w0 < NI ? ld_desc(desc, w0) : make_int4(0, 0, 0, 0);
-  double g_mine = 0.0;  // lane k < 9: component k of the current item's ghat
-  int c_skip = 0;
-  if (w0 < NI) {
-    const ItemDesc d0 = decode_item(c_q);
-    if (lane < 9) g_mine = ghat[lane * P + d0.n];
-    if (kSkip) c_skip = prev_active[d0.n] == 0;
+  {  // stale stage bytes must be finite: zero this lane's ring slots once
+#pragma unroll
+    for (int st = 0; st < kRing; ++st)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-#pragma unroll 1
-  for (int64_t item = w0; item < NI; item += W) {
-    ItemDesc d = decode_item(c_q);
-    if (kSkip && c_skip) d.nst = 0;
-    const bool single = d.single;
-    double G[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) G[k] = __shfl_sync(0xffffffffu, g_mine, k);
-    // prefetch the next item (descriptor, then its ghat / skip flag)
-    int4 n_q = make_int4(0, 0, 0, 0);
-    if (item + W < NI) n_q = ld_desc(desc, item + W);
-    acc.zero();
-    const int64_t hi = d.lo + d.len;
-    bool next_loaded = false;
-    double g_next = 0.0;
-    int skip_next = 0;
-#pragma unroll 1
-    for (int st_i = 0; st_i < d.nst; ++st_i) {
-      const int st = consumed % kStages;
-      const uint32_t phase = (consumed / kStages) & 1u;
-      const int64_t sb = d.lo + (int64_t)st_i * kStageSlots;
-      const int64_t rem = hi - sb;
-      mbar_wait(&sm.bar[st], phase);
-      if (!next_loaded && item + W < NI) {  // the descriptor has arrived by now
-        const ItemDesc dn = decode_item(n_q);
-        if (lane < 9) g_next = ghat[lane * P + dn.n];
-        if (kSkip) skip_next = prev_active[dn.n] == 0;
-        next_loaded = true;
-      }
-#pragma unroll 1
-      for (int so = 0; so < kStageSlots && rem > so; so += kSubSlots) {
-        const int64_t r = rem - so;
-        if (r > 64) {
-          consume_sub<4>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
-        } else if (r > 32) {
-          consume_sub<2>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
-        } else {
-          consume_sub<1>(acc, sm, st, so, sb, hi, G, thr, lane, s.active);
-        }
-      }
-      __syncwarp();
-      ++consumed;
-      produce();  // refill the stage just drained
-    }
-    if (!next_loaded && item + W < NI) {
-      const ItemDesc dn = decode_item(n_q);
-      if (lane < 9) g_next = ghat[lane * P + dn.n];
-      if (kSkip) skip_next = prev_active[dn.n] == 0;
-    }
-    c_q = n_q;
-    g_mine = g_next;
-    c_skip = skip_next;
+  for (int it = 0; it < kRing - 1; ++it) issue(it);
 
-    // ------------------------------------------------------------ reduce
-    // lane-major rows in smem, each lane sums rows in a fixed order
-    if (kMom && MOM64) {
-      double* red = sm.red;
-      constexpr int kHalf = (kRed64 + 1) / 2;  // 19 rows per phase
+  HotAcc<kPrune, kL1, kMom, MOM64> acc;
+  acc.zero();
+#pragma unroll 1
+  for (int it = 0; it < warp_it; ++it) {
+    issue(it + kRing - 1);
+    cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
+    const int st = it % kRing;
+    if (it < nit) {
+      const int64_t blk = d.lo + (int64_t)4 * L * it;
+      const int64_t sa = blk + 2 * g;          // first slot pair
+      const int64_t sb = blk + 2 * L + 2 * g;  // second slot pair
+      const int sha = (int)(sa & 31), shb = (int)(sb & 31);
+      const int64_t la = hi - sa, lb = hi - sb;
+      const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
+      const unsigned vb = lb >= 2 ? 3u : (lb > 0 ? 1u : 0u);
+      const unsigned bits = ((ring.m[st][lane] >> sha) & va) | (((ring.m2[st][lane] >> shb) & vb) << 2);
+      const float4 a0 = ring.c[st][0][lane];
+      const float4 a1 = ring.c[st][1][lane];
+      const float4 b0 = ring.c[st][2][lane];
+      const float4 b1 = ring.c[st][3][lane];
+      const float2 X1[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
+                            make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
+      const float2 X2[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                            make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
+      unsigned keep_bits = 0;
 #pragma unroll
-      for (int ph = 0; ph < 2; ++ph) {
-#pragma unroll
-        for (int k = 0; k < kHalf; ++k) {
-          const int row = ph * kHalf + k;
-          const double val = row < 36 ? acc.M64[MOM64 ? (row < 36 ? row : 0) : 0]
-                                      : (row == 36 ? (double)acc.cnt : acc.l1);
-          red[k * kRedRow + lane] = val;
-        }
-        __syncwarp();
-        if (lane < kHalf) {
-          const int k = ph * kHalf + lane;
-          double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            t0 += red[lane * kRedRow + j];
-            t1 += red[lane * kRedRow + j + 1];
-            t2 += red[lane * kRedRow + j + 2];
-            t3 += red[lane * kRedRow + j + 3];
-          }
-          const double t = (t0 + t1) + (t2 + t3);
-          if (!single) {
-            if (k < 36) static_cast<double*>(part.red)[k * NI + item] = t;
-            else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = t;
-            else part.l1[item] = t;
-          } else if (k < 36) {
-            out.mom64[k * P + d.n] = t;
-          } else if (k == 36) {
-            if (out.n_active) out.n_active[d.n] = (int32_t)t;
-          } else if (kL1 && out.l1) {
-            out.l1[d.n] = t;
-          }
-        }
-        __syncwarp();
+      for (int k = 0; k < 4; ++k)
+        keep_bits |= (unsigned)acc.point(G, X1[k], X2[k], (bits >> k) & 1u, thr) << k;
+      if (kPrune) {
+        const unsigned cleared = bits & ~keep_bits;
+        if (cleared & 3u) atomicAnd(&s.active[sa >> 5], ~((cleared & 3u) << sha));
+        if (cleared >> 2) atomicAnd(&s.active[sb >> 5], ~((cleared >> 2) << shb));
       }
-    } else if (kMom) {
-      float* red = reinterpret_cast<float*>(sm.red);
-      constexpr int kHalf = (kRed32 + 1) / 2;  // 24 rows per phase
-      const float vv[11] = {acc.V0.x, acc.V0.y, acc.V1.x, acc.V1.y, acc.V2.x, acc.V2.y,
-                            acc.V3.x, acc.V3.y, acc.v22, (float)acc.cnt, acc.s0f};
+    }
+  }
+  cp_async_wait<0>();
+
+  // ------------------------------------------------------------------ reduce
+  // log2(L) butterfly levels within the item's lanes; lane g then writes
+  // outputs k = g, g + L, ... (consecutive items -> coalesced SoA stores)
+  const bool single = d.single;
+  if (kMom && MOM64) {
+    double v[38];
 #pragma unroll
-      for (int ph = 0; ph < 2; ++ph) {
+    for (int k = 0; k < 36; ++k) v[k] = group_sum<L>(acc.M64[MOM64 ? k : 0]);
+    v[36] = group_sum<L>((double)acc.cnt);
+    v[37] = group_sum<L>(acc.l1);
+    if (has_item) {
 #pragma unroll
-        for (int k = 0; k < kHalf; ++k) {
-          const int row = ph * kHalf + k;
-          if (row >= kRed32) break;
-          const float val = row < 36 ? ((row & 1) ? acc.M2[MOM64 ? 0 : (row < 36 ? row / 2 : 0)].y
-                                                  : acc.M2[MOM64 ? 0 : (row < 36 ? row / 2 : 0)].x)
-                                     : vv[row - 36 < 11 ? row - 36 : 0];
-          red[k * kRedRow + lane] = val;
-        }
-        __syncwarp();
-        const int vi = ph * kHalf + lane;
-        if (lane < kHalf && vi < kRed32) {
-          float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            t0 += red[lane * kRedRow + j];
-            t1 += red[lane * kRedRow + j + 1];
-            t2 += red[lane * kRedRow + j + 2];
-            t3 += red[lane * kRedRow + j + 3];
-          }
-          const float t = (t0 + t1) + (t2 + t3);
-          if (vi == 46) {
-            if (single) out.s0[d.n] = (double)t;
-            else part.s0[item] = (double)t;
-          } else {
-            const int k = hot_out_index(vi);
-            if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, t, kLin);
-          }
-        }
-        __syncwarp();
-      }
-      if (kL1) {
-        const double l1 = warp_sum(acc.l1);
-        if (lane == 0) {
-          if (single) {
-            if (out.l1) out.l1[d.n] = l1;
-          } else {
-            part.l1[item] = l1;
-          }
+      for (int k = 0; k < 38; ++k) {
+        if (k % L != g) continue;
+        if (!single) {
+          if (k < 36) static_cast<double*>(part.red)[k * NI + item] = v[k];
+          else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = v[k];
+          else part.l1[item] = v[k];
+        } else if (k < 36) {
+          out.mom64[k * P + d.n] = v[k];
+        } else if (k == 36) {
+          if (out.n_active) out.n_active[d.n] = (int32_t)v[k];
+        } else if (kL1 && out.l1) {
+          out.l1[d.n] = v[k];
         }
       }
-    } else {
-      const int cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
-      const double l1 = kL1 ? warp_sum(acc.l1) : 0.0;
-      if (lane == 0) {
+    }
+  } else if (kMom) {
+    float v[47];
+#pragma unroll
+    for (int k = 0; k < 18; ++k) {
+      v[2 * k] = group_sumf<L>(acc.M2[MOM64 ? 0 : k].x);
+      v[2 * k + 1] = group_sumf<L>(acc.M2[MOM64 ? 0 : k].y);
+    }
+    const float vv[11] = {acc.V0.x, acc.V0.y, acc.V1.x, acc.V1.y, acc.V2.x, acc.V2.y,
+                          acc.V3.x, acc.V3.y, acc.v22, (float)acc.cnt, acc.s0f};
+#pragma unroll
+    for (int k = 0; k < 11; ++k) v[36 + k] = group_sumf<L>(vv[k]);
+    const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
+    if (has_item) {
+#pragma unroll
+      for (int vi = 0; vi < 47; ++vi) {
+        if (vi % L != g) continue;
+        if (vi == 46) {
+          if (single) out.s0[d.n] = (double)v[vi];
+          else part.s0[item] = (double)v[vi];
+          continue;
+        }
+        const int k = hot_out_index(vi);
+        if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, v[vi], kLin);
+      }
+      if (kL1 && g == 0) {
         if (single) {
-          if (out.n_active) out.n_active[d.n] = cnt;
-          if (kL1 && out.l1) out.l1[d.n] = l1;
+          if (out.l1) out.l1[d.n] = l1;
         } else {
-          static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
-          if (kL1) part.l1[item] = l1;
+          part.l1[item] = l1;
         }
+      }
+    }
+  } else {
+    const int cnt = (int)group_sum<L>((double)acc.cnt);
+    const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
+    if (has_item && g == 0) {
+      if (single) {
+        if (out.n_active) out.n_active[d.n] = cnt;
+        if (kL1 && out.l1) out.l1[d.n] = l1;
+      } else {
+        static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
+        if (kL1) part.l1[item] = l1;
       }
     }
   }
@@ -827,23 +693,30 @@ __global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
   }
 }
 
-template <unsigned MODE, bool MOM64>
-int launch_hot(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
-               const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
-  static int blocks_per_sm = 0;
-  const size_t smem = kHotWarps * sizeof(HotWarpSmem);
-  static_assert(sizeof(HotWarpSmem) % 128 == 0 || true, "");
-  if (!blocks_per_sm) {
-    FM_CUDA(cudaFuncSetAttribute(point_pass_hot<MODE, MOM64>,
+template <unsigned MODE, bool MOM64, int L>
+int hot_blocks_per_sm(int* out) {
+  static int cached = 0;
+  if (!cached) {
+    const size_t smem = kGrpWarps * sizeof(LaneRing);
+    FM_CUDA(cudaFuncSetAttribute(point_pass_hot<MODE, MOM64, L>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, point_pass_hot<MODE, MOM64>,
-                                                          kHotWarps * 32, smem));
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    int b = 0;
+    FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, point_pass_hot<MODE, MOM64, L>,
+                                                          kGrpWarps * 32, smem));
+    cached = b > 0 ? b : 1;
   }
-  const int64_t want = ceil_div(s.n_items, kHotWarps);
-  const int64_t grid = std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count());
-  point_pass_hot<MODE, MOM64><<<(unsigned)grid, kHotWarps * 32, smem, stream>>>(s, ghat, thr, prev_active,
-                                                                               out, part);
+  *out = cached;
+  return FM_OK;
+}
+
+template <unsigned MODE, bool MOM64, int L>
+int launch_hot_l(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
+                 const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
+  const size_t smem = kGrpWarps * sizeof(LaneRing);
+  const int64_t warps = ceil_div(s.n_items, 32 / L);
+  const int64_t grid = ceil_div(warps, kGrpWarps);
+  point_pass_hot<MODE, MOM64, L><<<(unsigned)grid, kGrpWarps * 32, smem, stream>>>(
+      s, ghat, thr, prev_active, out, part);
   FM_LAUNCHED(point_pass_hot);
   if (s.n_items > s.n_pairs) {
     combine_kernel<MOM64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
@@ -851,6 +724,42 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     FM_LAUNCHED(combine_kernel);
   }
   return FM_OK;
+}
+
+// Lanes per item L: blocks are one-shot, so the last wave of a launch is
+// partially filled.  Score each L by (work / slots-time) of its wave count
+// and a per-item reduction cost of log2(L) butterfly levels; short items
+// (< 4L slots per lane-iteration) also waste lanes.
+template <unsigned MODE, bool MOM64>
+int launch_hot(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
+               const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
+  int b4 = 1, b8 = 1, b16 = 1;
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 4>(&b4)) return rc;
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 8>(&b8)) return rc;
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 16>(&b16)) return rc;
+  const double mean_len = s.n_items ? (double)s.n_slots / (double)s.n_items : 0.0;
+  const int Ls[3] = {4, 8, 16};
+  const int bps[3] = {b4, b8, b16};
+  double best = -1.0;
+  int pick = 4;
+  for (int k = 0; k < 3; ++k) {
+    const int L = Ls[k];
+    const double blocks = std::ceil((double)s.n_items / (32.0 / L) / kGrpWarps);
+    const double resident = (double)bps[k] * sm_count();
+    const double waves = blocks / resident;
+    const double fill = waves / std::ceil(waves);
+    const double lane_use = std::min(1.0, mean_len / (4.0 * L)) ;
+    const double red = 1.0 / (1.0 + 0.02 * (k + 2) * 400.0 / std::max(mean_len, 1.0));
+    const double score = fill * lane_use * red;
+    if (score > best * 1.03) {
+      best = score;
+      pick = L;
+    }
+  }
+  if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
+  if (pick == 16) return launch_hot_l<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream);
+  if (pick == 8) return launch_hot_l<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream);
+  return launch_hot_l<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);
 }
 
 template <bool HOMOG, bool F64, unsigned MODE>

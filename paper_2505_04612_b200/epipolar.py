@@ -352,6 +352,9 @@ class IrlsEngine:
     directly by the benchmark (store built on the device)."""
 
     def __init__(self, store, graph, params, cfg, use_graph=True, precision="fp64"):
+        if not getattr(store, "sanitized", False):
+            raise ValueError("IrlsEngine needs a sanitized store (finite coordinates on every "
+                             "slot; build it with sanitize=True)")
         self.store = store
         self.graph = graph
         self.device = store.device
@@ -447,7 +450,7 @@ def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True, precision="fp64"
     state = AdjustmentState.from_poses(poses, image_ids, n_cameras, cfg.refine_focal)
     device = N.require_cuda()
     idx_i, idx_j, cam_i, cam_j = _pair_indices(state, pairs)
-    store = PointPairStore.from_pairs(pairs, device=device)
+    store = PointPairStore.from_pairs(pairs, device=device, sanitize=True)
     o = store.order
     graph = PairGraph(idx_i[o], idx_j[o], cam_i[o], cam_j[o], len(image_ids), n_cameras,
                       cfg.refine_focal, device=device)

@@ -205,7 +205,7 @@ def make_shards(x1, x2, lengths, ij, cams, n_images, n_cameras, refine_focal, bo
         a, b = int(bounds[k]), int(bounds[k + 1])
         sl = slice(start[a], start[b])
         store = PointPairStore(x1[sl], x2[sl], lengths[a:b], ij[a:b, 0], ij[a:b, 1],
-                               device=device, order=np.arange(b - a))
+                               device=device, order=np.arange(b - a), sanitize=True)
         graph = PairGraph(ij[a:b, 0], ij[a:b, 1], cams[a:b, 0], cams[a:b, 1], n_images, n_cameras,
                           refine_focal, device=device)
         out.append(Shard(store, graph, precision))

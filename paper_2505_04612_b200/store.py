@@ -73,9 +73,15 @@ class PointPairStore:
     """
 
     def __init__(self, x1, x2, lengths, pair_i, pair_j, active=None, device=None,
-                 chunk=CHUNK, order=None):
+                 chunk=CHUNK, order=None, sanitize=False):
         """x1, x2: (Z, 2) or (Z, 3) float arrays of all points, pairs in caller
-        order; lengths: points per pair (caller order)."""
+        order; lengths: points per pair (caller order).
+
+        sanitize=True zeroes the coordinates of non-finite points and clears
+        their active bit.  The IRLS moment passes need finite coordinates on
+        every slot; for irls_refine this is exactly the reference's behaviour
+        (a non-finite residual fails ``res <= th`` in the first prune,
+        ref/epipolar.py:283).  API stores (current_residuals) keep NaNs."""
         device = device or N.require_cuda()
         lengths = np.asarray(lengths, dtype=np.int64)
         P = len(lengths)
@@ -104,6 +110,17 @@ class PointPairStore:
 
         x1 = np.asarray(x1)
         x2 = np.asarray(x2)
+        self.sanitized = bool(sanitize)
+        if sanitize and len(x1):
+            bad = ~(np.isfinite(x1).all(axis=1) & np.isfinite(x2).all(axis=1))
+            if bad.any():
+                x1 = np.where(bad[:, None], 0.0, x1)
+                x2 = np.where(bad[:, None], 0.0, x2)
+                if x1.shape[1] == 3:
+                    x1[bad, 2] = 1.0
+                    x2[bad, 2] = 1.0
+                act = np.ones(len(x1), dtype=bool) if active is None else np.asarray(active, dtype=bool)
+                active = act & ~bad
         homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
         self.homogeneous = bool(homog)
         c1 = np.zeros((n_slots, 2), dtype=np.float32)
@@ -211,6 +228,7 @@ class PointPairStore:
         self.x2[slot] = x2.to(torch.float32)
         self.x1z = self.x2z = None
         self.homogeneous = False
+        self.sanitized = True  # device-generated coordinates are finite
         bits = torch.zeros(n_slots, dtype=torch.int64, device=device)
         bits[slot] = 1
         w = (bits.view(-1, 32) << torch.arange(32, device=device, dtype=torch.int64)).sum(1)
@@ -239,7 +257,7 @@ class PointPairStore:
         return torch.from_numpy(self.point_slot).to(self.device)
 
     @classmethod
-    def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False):
+    def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False, sanitize=False):
         """Build from EpipolarPair-like objects (reference or ours)."""
         lengths = np.array([len(p.x1) for p in pairs], dtype=np.int64)
         if len(pairs):
@@ -253,7 +271,7 @@ class PointPairStore:
             act = None
         i = np.array([p.i for p in pairs], dtype=np.int64)
         j = np.array([p.j for p in pairs], dtype=np.int64)
-        return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk)
+        return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk, sanitize=sanitize)
 
 
 def csr(keys, n_keys, payload):

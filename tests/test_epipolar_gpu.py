@@ -103,7 +103,7 @@ def test_hot_point_pass_matches_oracle(chunk, precision):
     rng = np.random.default_rng(1)
     st.unpack(st.pack() + rng.normal(scale=3e-3, size=st.pack().shape))
     dev = torch.device("cuda")
-    store = PointPairStore.from_pairs(pairs, device=dev, chunk=chunk)
+    store = PointPairStore.from_pairs(pairs, device=dev, chunk=chunk, sanitize=True)
     o = store.order
     ii, jj, ci, cj = E._pair_indices(st, pairs)
     graph = PairGraph(ii[o], jj[o], ci[o], cj[o], n, 2, True, device=dev)
@@ -147,7 +147,7 @@ def test_shifted_model_loss_grad_matches_oracle():
     rng = np.random.default_rng(2)
     st.unpack(st.pack() + rng.normal(scale=3e-3, size=st.pack().shape))
     dev = torch.device("cuda")
-    store = PointPairStore.from_pairs(pairs, device=dev)
+    store = PointPairStore.from_pairs(pairs, device=dev, sanitize=True)
     o = store.order
     ii, jj, ci, cj = E._pair_indices(st, pairs)
     graph = PairGraph(ii[o], jj[o], ci[o], cj[o], n, 2, True, device=dev)
@@ -276,12 +276,15 @@ def test_nonfinite_inactive_points_do_not_poison_moments(precision):
     n = len(poses.rotations)
     st = E.AdjustmentState.from_poses(poses, list(range(n)), 2, True)
     dev = torch.device("cuda")
-    store = PointPairStore.from_pairs(pairs, device=dev)
+    store = PointPairStore.from_pairs(pairs, device=dev, sanitize=True)
     o = store.order
     ii, jj, ci, cj = E._pair_indices(st, pairs)
     graph = PairGraph(ii[o], jj[o], ci[o], cj[o], n, 2, True, device=dev)
     eng = E.IrlsEngine(store, graph, torch.as_tensor(st.pack(), device=dev), Cfg(),
                        precision=precision)
+    with pytest.raises(ValueError, match="sanitized"):
+        E.IrlsEngine(PointPairStore.from_pairs(pairs, device=dev), graph,
+                     torch.as_tensor(st.pack(), device=dev), Cfg())
     eng._ghat()
     eng.point_pass(N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS, 0.02, 1, 0)
     P = len(pairs)
