@@ -110,7 +110,8 @@ SIGNATURES = {
 
 
 def lib_path():
-    return _build.LIB_PATH
+    # FASTMAP_B200_LIB: alternative build of the same ABI (kernel tuning runs)
+    return os.environ.get("FASTMAP_B200_LIB") or _build.LIB_PATH
 
 
 def lib():

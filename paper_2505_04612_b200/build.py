@@ -36,11 +36,12 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, extra=()):
+def build(force=False, verbose=False, extra=(), out=None):
     """Compile every CUDA source into LIB_PATH (skipped when up to date)."""
-    if not force and not _stale():
+    if out is None and not force and not _stale():
         return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
+    target = out or LIB_PATH
+    tmp = target + ".tmp"
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "-cudart", "static",
            "-I", os.path.join(REPO_DIR, "include"),
@@ -48,8 +49,8 @@ def build(force=False, verbose=False, extra=()):
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

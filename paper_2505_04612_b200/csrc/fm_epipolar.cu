@@ -34,6 +34,7 @@ struct EpiScratch {
   double* cpart;  // [n_cam_chunks]
   double* lpart;  // [loss blocks]
   double* sched;  // [2 + 2*kMaxSteps]: lr, scale, bc1[], bc2[]
+  unsigned int* ticket;  // camera-chunk completion counter (last block finalises)
 };
 
 int loss_blocks(int64_t P) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(P, 1024), 1), 1024); }
@@ -45,6 +46,7 @@ size_t scratch_need(const fm_pair_graph& g) {
   b += scratch_round((size_t)std::max(g.n_cam_chunks, 1) * sizeof(double));
   b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
   b += scratch_round((size_t)(2 + 2 * kMaxSteps) * sizeof(double));
+  b += scratch_round(sizeof(unsigned int));
   return b + 256;
 }
 
@@ -55,6 +57,7 @@ bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
   s.cpart = sc.take<double>((size_t)std::max(g.n_cam_chunks, 1));
   s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
   s.sched = sc.take<double>((size_t)(2 + 2 * kMaxSteps));
+  s.ticket = sc.take<unsigned int>(1);
   return p != nullptr && sc.ok();
 }
 
@@ -283,31 +286,77 @@ struct AdamArgs {
 // gradient (API) or Adam with lane q updating parameter q, and the new
 // rotation.  Blocks [img_blocks, ..): one block per camera chunk --
 // fixed-order partial sum of focal gradients (ref/epipolar.py:194-196).
+constexpr int kReduceBlock = 64;  // 2 warps: spreads small image counts over all SMs
+
 template <bool ADAM>
-__global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
-                                    const double* __restrict__ pg, double* __restrict__ grad,
-                                    double* __restrict__ R, double* __restrict__ cpart,
-                                    const int img_blocks, const AdamArgs ad, int32_t* flag) {
-  __shared__ double red[kCamBlock];
+__device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params,
+                             const double* __restrict__ cpart, double* __restrict__ grad,
+                             const AdamArgs& ad, int32_t* flag) {
+  // Executed by the last camera-chunk block: warp per camera, fixed-order
+  // lane-strided sum of the chunk partials + butterfly, then Adam.
+  const int lane = threadIdx.x & 31;
+  for (int c = threadIdx.x >> 5; c < g.n_cameras; c += kReduceBlock / 32) {
+    double acc = 0;
+    for (int k = g.cam_chunk_off[c] + lane; k < g.cam_chunk_off[c + 1]; k += 32) acc += __ldcg(cpart + k);
+    acc = warp_sum(acc);
+    if (lane != 0) continue;
+    const int idx = 9 * g.n_images + c;
+    if (!ADAM) {
+      grad[idx] = acc;
+      continue;
+    }
+    if (!isfinite(acc)) {
+      raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+      continue;
+    }
+    const double lr = ad.sched[0];
+    const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+    adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+  }
+}
+
+// One launch, two roles.  Blocks [0, img_blocks): warp per image --
+// fixed-order gather of the image's incidences, 6D VJP (every lane computes it
+// redundantly from the butterfly-reduced totals), then either the packed
+// gradient (API) or Adam with lane q updating parameter q, and the new
+// rotation.  Blocks [img_blocks, ..): one block per camera chunk --
+// fixed-order partial sum of focal gradients (ref/epipolar.py:194-196); the
+// last chunk block to finish (atomic ticket) sums the partials per camera in
+// chunk order and applies the focal update.
+template <bool ADAM>
+__global__ void __launch_bounds__(kReduceBlock)
+image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
+                    const double* __restrict__ pg, double* __restrict__ grad,
+                    double* __restrict__ R, double* __restrict__ cpart, unsigned int* ticket,
+                    const int img_blocks, const AdamArgs ad, int32_t* flag) {
+  __shared__ double red[kReduceBlock];
+  __shared__ bool last;
   const int64_t P = g.n_pairs;
   if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
     const int c = blockIdx.x - img_blocks;
     if (ADAM && *flag) return;
-    if (threadIdx.x < kCamBlock) {
-      double acc = 0;
-      const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
-      for (int e = lo + threadIdx.x; e < hi; e += kCamBlock) {
-        const int inc = g.cam_inc[e];
-        acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
-      }
-      red[threadIdx.x] = acc;
+    double acc = 0;
+    const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
+    for (int e = lo + threadIdx.x; e < hi; e += kReduceBlock) {
+      const int inc = g.cam_inc[e];
+      acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
     }
+    red[threadIdx.x] = acc;
     __syncthreads();
-    for (int st = kCamBlock / 2; st > 0; st >>= 1) {
+    for (int st = kReduceBlock / 2; st > 0; st >>= 1) {
       if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
       __syncthreads();
     }
-    if (threadIdx.x == 0) cpart[c] = red[0];
+    if (threadIdx.x == 0) {
+      cpart[c] = red[0];
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == (unsigned)(gridDim.x - img_blocks - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    cam_finalise<ADAM>(g, params, cpart, grad, ad, flag);
+    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next step
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -378,29 +427,6 @@ __global__ void image_reduce_kernel(const fm_pair_graph g, double* __restrict__ 
   if (lane < 9) R[9 * (int64_t)k + lane] = val;
 }
 
-template <bool ADAM>
-__global__ void cam_final_kernel(const fm_pair_graph g, double* __restrict__ params,
-                                 const double* __restrict__ cpart, double* __restrict__ grad,
-                                 const AdamArgs ad, int32_t* flag) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.n_cameras) return;
-  if (ADAM && *flag) return;
-  double acc = 0;
-  for (int k = g.cam_chunk_off[c]; k < g.cam_chunk_off[c + 1]; ++k) acc += cpart[k];
-  const int idx = 9 * g.n_images + c;
-  if (!ADAM) {
-    grad[idx] = acc;
-    return;
-  }
-  if (!isfinite(acc)) {
-    raise_flag(flag, FM_ERR_NONFINITE_GRAD);
-    return;
-  }
-  const double lr = ad.sched[0];
-  const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
-  adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
-}
-
 // Deterministic two-level sum of the per-pair loss terms.
 __global__ void loss_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
   __shared__ double red[256];
@@ -423,23 +449,24 @@ __global__ void loss_final_kernel(const double* __restrict__ part, int nb, doubl
   }
 }
 
-__global__ void set_sched_kernel(double* sched, double lr, double scale) {
+__global__ void set_sched_kernel(double* sched, double lr, double scale, unsigned int* ticket) {
   sched[0] = lr;
   sched[1] = scale;
+  *ticket = 0u;
 }
 
 int launch_pair_grad(const fm_pair_graph& g, const fm_quad_model& q, const double* params,
                      const EpiScratch& s, int32_t* flag, cudaStream_t st) {
-  const unsigned blocks = (unsigned)ceil_div(g.n_pairs, 128);
+  const unsigned blocks = (unsigned)ceil_div(g.n_pairs, 64);
   switch (q.kind) {
     case FM_QUAD_SHIFTED32:
-      pair_grad_kernel<FM_QUAD_SHIFTED32><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_SHIFTED32><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
       break;
     case FM_QUAD_W64:
-      pair_grad_kernel<FM_QUAD_W64><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_W64><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
       break;
     case FM_QUAD_MOM64:
-      pair_grad_kernel<FM_QUAD_MOM64><<<blocks, 128, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_MOM64><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
       break;
     default:
       return set_error(FM_ERR_INVALID, "unknown quadratic model kind %d", q.kind);
@@ -477,17 +504,12 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
     int rc = launch_pair_grad(g, q, params, s, flag, st);
     if (rc) return rc;
     AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
-    const int img_blocks = (int)ceil_div((int64_t)N * 32, 256);
+    const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
     const int cam_blocks = (g.refine_focal && g.n_cameras > 0) ? g.n_cam_chunks : 0;
     if (img_blocks + cam_blocks > 0) {
-      image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), 256, 0, st>>>(
-          g, params, s.pg, nullptr, s.R, s.cpart, img_blocks, ad, flag);
+      image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
+          g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag);
       FM_LAUNCHED(image_reduce_kernel);
-    }
-    if (g.refine_focal && g.n_cameras > 0) {
-      cam_final_kernel<true><<<(unsigned)ceil_div(g.n_cameras, 128), 128, 0, st>>>(
-          g, params, s.cpart, nullptr, ad, flag);
-      FM_LAUNCHED(cam_final_kernel);
     }
   }
   return FM_OK;
@@ -576,7 +598,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   const int N = g->n_images;
   const int64_t P = g->n_pairs;
   const size_t n_grad = (size_t)9 * N + (g->refine_focal ? g->n_cameras : 0);
-  set_sched_kernel<<<1, 1, 0, st>>>(s.sched, 0.0, scale);
+  set_sched_kernel<<<1, 1, 0, st>>>(s.sched, 0.0, scale, s.ticket);
   FM_LAUNCHED(set_sched_kernel);
   if (N > 0) {
     image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
@@ -591,18 +613,14 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   if (int rc = launch_pair_grad(*g, *q, params, s, nullptr, st)) return rc;
   AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, 0};
   {
-    const int img_blocks = (int)ceil_div((int64_t)N * 32, 256);
+    const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
     const int cam_blocks = (g->refine_focal && g->n_cameras > 0) ? g->n_cam_chunks : 0;
     if (img_blocks + cam_blocks > 0) {
-      image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), 256, 0, st>>>(
-          *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, img_blocks, none, flag);
+      image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
+          *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, s.ticket, img_blocks,
+          none, flag);
       FM_LAUNCHED(image_reduce_kernel);
     }
-  }
-  if (g->refine_focal && g->n_cameras > 0) {
-    cam_final_kernel<false><<<(unsigned)ceil_div(g->n_cameras, 128), 128, 0, st>>>(
-        *g, const_cast<double*>(params), s.cpart, grad_out, none, flag);
-    FM_LAUNCHED(cam_final_kernel);
   }
   const int nb = loss_blocks(P);
   loss_partial_kernel<<<nb, 256, 0, st>>>(s.pg + (size_t)23 * P, P, s.lpart);
@@ -625,6 +643,7 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
   cudaStream_t st = as_stream(stream);
   if (n_steps == 0) return FM_OK;
   const int N = g->n_images;
+  FM_CUDA(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned int), st));
   if (N > 0) {
     image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
     FM_LAUNCHED(image_rot_kernel);

@@ -256,12 +256,14 @@ struct HotAcc {
     cnt += keep;
     if (kL1) l1 += act ? ar : 0.0;
     if (kMom) {
-      // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); a per-point relative
-      // error of the weight keeps every term rank-1 exact.
-      // Coordinates of every slot are finite (the store builders zero and
-      // deactivate non-finite points), so a zero weight removes a dropped
-      // point exactly without selecting its coordinates.
-      const float wf = keep ? rcp_approx(fmaxf((float)ar, 1e-6f)) : 0.f;
+      // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58) from the rounded
+      // residual: a per-point relative error of the weight keeps every term
+      // rank-1 exact.  Coordinates of every slot are finite (the store
+      // builders zero and deactivate non-finite points), so a zero weight
+      // removes a dropped point exactly without selecting its coordinates.
+      const float rf = (float)r;
+      const float arf = fabsf(rf);
+      const float wf = keep ? rcp_approx(fmaxf(arf, 1e-6f)) : 0.f;
       const float2 Y1 = X1;
       const float2 Y2 = X2;
       if (MOM64) {
@@ -276,9 +278,10 @@ struct HotAcc {
           for (int j = 0; j < 6; ++j)
             M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
       } else {
-        const bool big = ar >= 1e-6;
-        const float wr = keep ? (big ? (r > 0 ? 1.f : -1.f) : (float)(r * 1e6)) : 0.f;
-        s0f += keep ? (big ? (float)ar : (float)(r * r * 1e6)) : 0.f;
+        // w r0 = sign(r) and w r0^2 = |r| unless clamped (|r| < 1e-6)
+        const bool big = arf >= 1e-6f;
+        const float wr = keep ? (big ? copysignf(1.f, rf) : rf * 1e6f) : 0.f;
+        s0f += keep ? (big ? arf : rf * rf * 1e6f) : 0.f;
         const float2 wX2 = __fmul2_rn(f2(wf), Y2);
         const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
         const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
@@ -302,13 +305,25 @@ struct HotAcc {
   }
 };
 
-// Per-lane ring: stage d holds the lane's 4 slots of x1 (2 chunks of 16 B),
-// x2 (2 chunks) and the mask word, laid out chunk-major so that a warp's
-// LDS.128 of chunk k touches 32 consecutive 16-byte words (conflict free).
+// Per-lane ring: stage d holds the lane's NPT slots of x1 and x2 (NPT/2
+// 16-byte chunks each) and the mask words, laid out chunk-major so that a
+// warp's LDS.128 of one chunk touches 32 consecutive 16-byte words (no bank
+// conflicts).
+#ifndef FM_HOT_NPT
+#define FM_HOT_NPT 4
+#endif
+#ifndef FM_HOT_GSM
+#define FM_HOT_GSM 1
+#endif
+#ifndef FM_HOT_MINB
+#define FM_HOT_MINB 1
+#endif
+constexpr int kNpt = FM_HOT_NPT;   // points per lane per iteration (2 or 4)
+constexpr bool kGsm = FM_HOT_GSM;  // ghat of the warp's items in shared memory
 struct LaneRing {
-  float4 c[kRing][4][32];   // [stage][chunk: x1 lo, x1 hi, x2 lo, x2 hi][lane]
-  uint32_t m[kRing][32];    // mask word of the lane's first slot pair
-  uint32_t m2[kRing][32];   // mask word of the lane's second slot pair
+  float4 c[kRing][kNpt][32];     // [stage][chunk: x1 (NPT/2), x2 (NPT/2)][lane]
+  uint32_t m[kRing][kNpt / 2][32];  // mask word of each slot pair
+  double G[32][9];                // ghat of the warp's items (kGsm)
 };
 
 template <int L>
@@ -325,7 +340,7 @@ __device__ __forceinline__ float group_sumf(float x) {
 }
 
 template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kGrpWarps * 32, 3)
+__global__ void __launch_bounds__(kGrpWarps * 32, FM_HOT_MINB)
 point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                const int32_t* __restrict__ prev_active, const fm_pass_out out,
                const PartialBufs part) {
@@ -334,7 +349,9 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
   constexpr bool kLin = kMom && !MOM64;
   constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
-  constexpr int IPW = 32 / L;  // items per warp
+  constexpr int IPW = 32 / L;        // items per warp
+  constexpr int kPairs = kNpt / 2;   // slot pairs (16-byte chunks per column) per lane
+  constexpr int kBlk = kNpt * L;     // slots per group iteration
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -343,42 +360,45 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   const int64_t P = s.n_pairs;
   const int64_t NI = s.n_items;
   const int g = lane % L;  // lane within the item group
-  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + lane / L;
+  const int q = lane / L;  // item within the warp
+  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + q;
   const bool has_item = item < NI;
 
   ItemDesc d{0, 0, 0, true};
   if (has_item) d = decode_item(__ldg(reinterpret_cast<const int4*>(s.item_desc) + item));
   const bool skip = has_item && kSkip && prev_active[d.n] == 0;
-  double G[9];
+  double G[kGsm ? 1 : 9];
+  if (kGsm) {
+    for (int k = g; k < 9; k += L) ring.G[q][k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+  } else {
 #pragma unroll
-  for (int k = 0; k < 9; ++k) G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
-  // iterations of this group: 4L-slot blocks of the item (same for its lanes)
+    for (int k = 0; k < (kGsm ? 1 : 9); ++k) G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+  }
+  // iterations of this group: kBlk-slot blocks of the item (same for its lanes)
   const int len = (has_item && !skip) ? d.len : 0;
-  const int nit = (len + 4 * L - 1) / (4 * L);
+  const int nit = (len + kBlk - 1) / kBlk;
   const int warp_it = __reduce_max_sync(0xffffffffu, nit);
   const int64_t hi = d.lo + len;
 
-  // Iteration `it` of a group covers the 4L-slot block at d.lo + 4L*it; lane g
-  // copies 16-byte chunks g and g + L of each column, so every copy
-  // instruction of the group reads whole 32-byte sectors, and owns slots
-  // {2g, 2g+1} and {2L+2g, 2L+2g+1} of the block.
+  // Iteration `it` of a group covers the kBlk-slot block at d.lo + kBlk*it;
+  // lane g copies 16-byte chunks g + L*j (j < NPT/2) of each column, so each
+  // copy instruction of the group reads whole 32-byte sectors; the lane owns
+  // slot pairs {2(g + L j), 2(g + L j) + 1}.
   auto issue = [&](int it) {
     const int st = it % kRing;
     if (it < nit) {
-      const int64_t blk = d.lo + (int64_t)4 * L * it;
+      const int64_t blk = d.lo + (int64_t)kBlk * it;
       const float4* x1 = reinterpret_cast<const float4*>(s.x1 + 2 * blk);
       const float4* x2 = reinterpret_cast<const float4*>(s.x2 + 2 * blk);
-      // chunks starting at or past the item end are not fetched (they may lie
-      // past the allocation); their stale stage bytes are finite and masked
-      if (blk + 2 * g < hi) {
-        cp_async16(&ring.c[st][0][lane], x1 + g);
-        cp_async16(&ring.c[st][2][lane], x2 + g);
-        cp_async4(&ring.m[st][lane], s.active + ((blk + 2 * g) >> 5));
-      }
-      if (blk + 2 * L + 2 * g < hi) {
-        cp_async16(&ring.c[st][1][lane], x1 + g + L);
-        cp_async16(&ring.c[st][3][lane], x2 + g + L);
-        cp_async4(&ring.m2[st][lane], s.active + ((blk + 2 * L + 2 * g) >> 5));
+#pragma unroll
+      for (int j = 0; j < kPairs; ++j) {
+        // chunks at or past the item end are not fetched (they may lie past
+        // the allocation); their stale stage bytes are finite and masked
+        if (blk + 2 * (g + L * j) < hi) {
+          cp_async16(&ring.c[st][j][lane], x1 + g + L * j);
+          cp_async16(&ring.c[st][kPairs + j][lane], x2 + g + L * j);
+          cp_async4(&ring.m[st][j][lane], s.active + ((blk + 2 * (g + L * j)) >> 5));
+        }
       }
     }
     cp_async_commit();
@@ -387,8 +407,9 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
 #pragma unroll
     for (int st = 0; st < kRing; ++st)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < kNpt; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  __syncwarp();
 #pragma unroll
   for (int it = 0; it < kRing - 1; ++it) issue(it);
 
@@ -400,31 +421,31 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
     cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
     const int st = it % kRing;
     if (it < nit) {
-      const int64_t blk = d.lo + (int64_t)4 * L * it;
-      const int64_t sa = blk + 2 * g;          // first slot pair
-      const int64_t sb = blk + 2 * L + 2 * g;  // second slot pair
-      const int sha = (int)(sa & 31), shb = (int)(sb & 31);
-      const int64_t la = hi - sa, lb = hi - sb;
-      const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
-      const unsigned vb = lb >= 2 ? 3u : (lb > 0 ? 1u : 0u);
-      const unsigned bits = ((ring.m[st][lane] >> sha) & va) | (((ring.m2[st][lane] >> shb) & vb) << 2);
-      const float4 a0 = ring.c[st][0][lane];
-      const float4 a1 = ring.c[st][1][lane];
-      const float4 b0 = ring.c[st][2][lane];
-      const float4 b1 = ring.c[st][3][lane];
-      const float2 X1[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
-                            make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
-      const float2 X2[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
-                            make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
-      unsigned keep_bits = 0;
+      const int64_t blk = d.lo + (int64_t)kBlk * it;
+      double Gl[9];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        keep_bits |= (unsigned)acc.point(G, X1[k], X2[k], (bits >> k) & 1u, thr) << k;
-      if (kPrune) {
-        const unsigned cleared = bits & ~keep_bits;
-        if (cleared & 3u) atomicAnd(&s.active[sa >> 5], ~((cleared & 3u) << sha));
-        if (cleared >> 2) atomicAnd(&s.active[sb >> 5], ~((cleared >> 2) << shb));
+      for (int k = 0; k < 9; ++k) Gl[k] = kGsm ? ring.G[q][k] : G[kGsm ? 0 : k];
+      unsigned keep_all = 0;
+#pragma unroll
+      for (int j = 0; j < kPairs; ++j) {
+        const int64_t sa = blk + 2 * (g + L * j);
+        const int sh = (int)(sa & 31);
+        const int64_t la = hi - sa;
+        const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
+        const unsigned bits = (ring.m[st][j][lane] >> sh) & va;
+        const float4 a = ring.c[st][j][lane];
+        const float4 b = ring.c[st][kPairs + j][lane];
+        unsigned keep_bits = (unsigned)acc.point(Gl, make_float2(a.x, a.y), make_float2(b.x, b.y),
+                                                 bits & 1u, thr);
+        keep_bits |= (unsigned)acc.point(Gl, make_float2(a.z, a.w), make_float2(b.z, b.w),
+                                         (bits >> 1) & 1u, thr) << 1;
+        if (kPrune) {
+          const unsigned cleared = bits & ~keep_bits;
+          if (cleared) atomicAnd(&s.active[sa >> 5], ~(cleared << sh));
+        }
+        keep_all |= keep_bits;
       }
+      (void)keep_all;
     }
   }
   cp_async_wait<0>();
@@ -781,22 +802,23 @@ int launch_generic(const fm_point_store& s, double thr, const double* ghat, cons
 constexpr unsigned kSkipD = FM_PASS_SKIP_DROPPED;
 constexpr unsigned kIrlsM = FM_PASS_MOMENTS | FM_PASS_IRLS;
 
-// Hot combinations (z == 1, fp32 moments): the passes of irls_refine.
+// Hot combinations (z == 1): the passes of irls_refine (rounds 0 / 1+,
+// IRLS iterations, final L1) and the API's L1 loss.
 #define FM_HOT_MODES(X)                                  \
   X(FM_PASS_PRUNE | kIrlsM)                              \
-  X(FM_PASS_PRUNE | kIrlsM | kSkipD)                     \
   X(FM_PASS_L1 | FM_PASS_PRUNE | kIrlsM)                 \
   X(FM_PASS_L1 | FM_PASS_PRUNE | kIrlsM | kSkipD)        \
-  X(kIrlsM)                                              \
   X(kIrlsM | kSkipD)                                     \
   X(FM_PASS_L1)                                          \
-  X(FM_PASS_L1 | kSkipD)                                 \
-  X(FM_PASS_PRUNE)                                       \
-  X(FM_PASS_PRUNE | kSkipD)
+  X(FM_PASS_L1 | kSkipD)
 
 // Generic combinations (API functions, any z, fp32 or fp64 accumulation).
 #define FM_GENERIC_MODES(X)                                          \
   FM_HOT_MODES(X)                                                    \
+  X(FM_PASS_PRUNE | kIrlsM | kSkipD)                                 \
+  X(kIrlsM)                                                          \
+  X(FM_PASS_PRUNE)                                                   \
+  X(FM_PASS_PRUNE | kSkipD)                                          \
   X(FM_PASS_ALL_POINTS | FM_PASS_RES_OUT)                            \
   X(FM_PASS_MOMENTS)                                                 \
   X(FM_PASS_MOMENTS | FM_PASS_ALL_POINTS)                            \

@@ -11,6 +11,7 @@ sc = scenes.generate(scenes.CONFIGS[cfgname], dev)
 store = scenes.device_store(sc, dev)
 graph, ids = scenes.device_graph(sc, dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+flush_rd = torch.ones(64 << 20, dtype=torch.float32, device=dev)  # 256 MB
 for prec in ["fp64", "fp32"]:
     params = torch.as_tensor(scenes.initial_params(sc, ids), device=dev)
     eng = E.IrlsEngine(store, graph, params, HotPathConfig(), precision=prec)
@@ -23,6 +24,8 @@ for prec in ["fp64", "fp32"]:
         ts = []
         for k in range(25):
             flush.fill_(k)
+            flush_rd.sum()
+            torch.cuda._sleep(400_000)
             a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
             a.record(); eng.point_pass(mode, 0.01, 0, 0); b.record()
             torch.cuda.synchronize()

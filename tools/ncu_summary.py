@@ -68,7 +68,7 @@ def main():
         total = sum(ops.values())
         print(f"\nSASS opcode mix ({total} warp instructions):\n")
         print(", ".join(f"{op} {100 * n / total:.1f}%" for op, n in ops.most_common(14)))
-        proof = [op for op in ("UBLKCP", "SYNCS", "UTMALDG", "DFMA", "FFMA2", "HMMA", "UTCHMMA") if ops.get(op)]
+        proof = [op for op in ("UBLKCP", "SYNCS", "UTMALDG", "LDGSTS", "DFMA", "FFMA2", "FADD2", "FMUL2", "HMMA", "UTCHMMA") if ops.get(op)]
         print(f"\nBlackwell evidence in SASS: {', '.join(proof)}")
     if len(sys.argv) > 2:
         rows = list(csv.reader(open(sys.argv[2])))
