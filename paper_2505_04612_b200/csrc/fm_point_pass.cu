@@ -166,6 +166,12 @@ constexpr int kRing = 6;        // stages per lane
 constexpr int kGrpWarps = 4;    // warps per block
 constexpr int kStageSlots = 128;  // (descriptor decode only)
 
+__device__ __forceinline__ float and_mask(float x, unsigned m) {
+  unsigned r;
+  asm("and.b32 %0, %1, %2;" : "=r"(r) : "r"(__float_as_uint(x)), "r"(m));
+  return __uint_as_float(r);
+}
+
 // x if keep else +0.0, as an integer AND so the compiler cannot hoist the
 // fp64 conversion above it (non-finite data on dropped points stays out).
 __device__ __forceinline__ float keep_or_zero(float x, unsigned keep_mask) {
@@ -242,7 +248,9 @@ struct HotAcc {
     cnt = 0;
   }
 
-  // one point pair; returns the post-prune keep flag
+  // one point pair; returns the post-prune keep flag.  Branch-free: the
+  // residual and weight are computed for every slot and masked afterwards, so
+  // the compiler can interleave the independent points of an iteration.
   __device__ __forceinline__ bool point(const double (&G)[9], float2 X1, float2 X2, bool act,
                                         double thr) {
     // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
@@ -252,7 +260,7 @@ struct HotAcc {
     const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
     const double r = fma(c, y0, fma(dd, y1, y2));
     const double ar = fabs(r);
-    const bool keep = kPrune ? (act && ar <= thr) : act;
+    const bool keep = kPrune ? (act & (ar <= thr)) : act;
     cnt += keep;
     if (kL1) l1 += act ? ar : 0.0;
     if (kMom) {
@@ -263,7 +271,10 @@ struct HotAcc {
       // removes a dropped point exactly without selecting its coordinates.
       const float rf = (float)r;
       const float arf = fabsf(rf);
-      const float wf = keep ? rcp_approx(fmaxf(arf, 1e-6f)) : 0.f;
+      const float wraw = rcp_approx(fmaxf(arf, 1e-6f));
+      // opaque AND (not a select) so the compiler cannot sink the reciprocal
+      // into a per-point branch and serialise the iteration's points
+      const float wf = and_mask(wraw, keep ? 0xffffffffu : 0u);
       const float2 Y1 = X1;
       const float2 Y2 = X2;
       if (MOM64) {
@@ -316,7 +327,7 @@ struct HotAcc {
 #define FM_HOT_GSM 1
 #endif
 #ifndef FM_HOT_MINB
-#define FM_HOT_MINB 1
+#define FM_HOT_MINB 3
 #endif
 constexpr int kNpt = FM_HOT_NPT;   // points per lane per iteration (2 or 4)
 constexpr bool kGsm = FM_HOT_GSM;  // ghat of the warp's items in shared memory

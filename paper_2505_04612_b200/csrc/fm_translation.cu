@@ -110,17 +110,20 @@ __global__ void tr_step_kernel(const fm_dir_graph g, const double* __restrict__ 
 #pragma unroll
       for (int k = 0; k < 3; ++k) delta[k] = side ? cv[b][k] - co[3 * b + k] : co[3 * b + k] - cv[b][k];
       const double len = fmax(sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]), 1e-8);
+      // one division per edge and run; the reference divides component-wise
+      // (ref/translation.py:116, :121) -- same value to within an ulp
+      const double inv = 1.0 / len;
       double u[3], r[3], gu[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        u[k] = delta[k] / len;
+        u[k] = delta[k] * inv;
         r[k] = u[k] - d[k];
         gu[k] = sgn(r[k]) * inv_m;
       }
       const double ug = u[0] * gu[0] + u[1] * gu[1] + u[2] * gu[2];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double gd = (gu[k] - u[k] * ug) / len;
+        const double gd = (gu[k] - u[k] * ug) * inv;
         acc[b][k] += side ? gd : -gd;
       }
       if (side == 0) lacc[b] += fabs(r[0]) + fabs(r[1]) + fabs(r[2]);
