@@ -36,6 +36,17 @@ BYTES_PER_POINT = 16.0 + 1.0 / 8.0      # fp32 (x1, y1, x2, y2) + 1 mask bit (re
 BYTES_PER_PAIR = 72.0 + 36 * 8 + 8 + 4 + 8 + 4 + 4 + 4 + 4  # ghat in, fp64 W moments/L1/count out, indices
 
 
+def ncu_traffic(config, precision):
+    """DRAM bytes (read + write) per launch of the timed pass, from the
+    committed ncu --set full capture of the same kernel and config
+    (profiles/traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return float(json.load(open(p))[config][precision]["dram_bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -45,32 +56,55 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML
+    every 5 ms; nvidia-smi fallback)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), float(mx), int(rs)))
+            self._stop.wait(0.005)
+
+    def _run_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        bits = [0x8, 0x40, 0x20, 0x4]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                                     text=True, timeout=5).stdout.strip().split(",")
+                rs = sum(b for b, v in zip(bits, out[2:]) if v.strip().lower() == "active")
+                self.samples.append((float(out[0]), float(out[1]), rs))
             except Exception:
                 pass
             self._stop.wait(0.1)
 
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
@@ -79,15 +113,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for name, bit in self.REASONS.items()
+                          if s[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples)}
 
 
 def dist_setup(n_gpus):
@@ -215,7 +246,7 @@ def run_ours(args, spec, world, rank, local):
     P = store.n_pairs
     lib = N.lib()
     with torch.cuda.stream(stream):
-        eng = E.IrlsEngine(store, graph, params, args.cfg)
+        eng = E.IrlsEngine(store, graph, params, args.cfg, precision=args.precision)
         eng._ghat()
     mode = N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -317,7 +348,7 @@ def run_ours(args, spec, world, rank, local):
         params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
         store.reset_active()
         with torch.cuda.stream(stream):
-            eng2 = E.IrlsEngine(store, graph, params0, args.cfg)
+            eng2 = E.IrlsEngine(store, graph, params0, args.cfg, precision=args.precision)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             l1h = eng2.run()
@@ -348,16 +379,20 @@ def run_ours(args, spec, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 coords+moments / f64 residual",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": ("f64 (residual, W moments, prune decisions) on f32 coordinates"
+                      if args.precision == "fp64" else
+                      "f32 W moments (shifted model) + f64 residual on f32 coordinates"),
             "data": "synthetic (device-generated ring scene, random-perturbed poses)",
             "config": {"workload": f"{args.config.upper()}: {spec.n_images} images, {P} image pairs, "
                                    f"{Z} point pairs per GPU (band {spec.band}, {spec.points_per_pair}"
                                    f" pts/pair)",
-                       "pass": "fused L1 + prune + IRLS W moments + linearisation gradient",
+                       "pass": "fused L1 + prune + IRLS W moments (irls_refine rounds 1-2 pass)",
+                       "precision": args.precision,
                        "l2": "flushed between steps (256 MB write + 256 MB read, outside the events) and inputs > L2",
                        "parallelism": f"dp{world} (point pairs sharded by image pair)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(args.config, args.precision),
                          "peak_kind": hbm_kind,
                          "algorithmic_bytes_per_launch": bytes_launch},
             "cpu_baseline": cpu,
@@ -415,12 +450,14 @@ def translation_bench(device, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-optimize", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="W-moment accumulation of the pass (irls_refine default: fp64)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     from paper_2505_04612_b200 import scenes

@@ -301,3 +301,25 @@ def test_nonfinite_inactive_points_do_not_poison_moments(precision):
     assert np.max(np.abs(W - ref["W"]) / scale) < (3e-7 if precision == "fp64" else 2e-5)
     assert np.array_equal(eng.buf.n_active[1].cpu().numpy()[:P], ref["n_active"])
     assert np.all(np.isfinite(eng.buf.l1.cpu().numpy()[:P]))
+
+
+def test_integration_stub(golden_small):
+    """The ctypes stub documented in INTEGRATION.md works as written."""
+    import os
+    import re
+
+    from paper_2505_04612_b200 import _native
+    from tests.conftest import ROOT
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"## 3\..*?```python\n(.*?)```", text, re.S).group(1)
+    os.environ["FASTMAP_B200_LIB"] = _native.lib_path()
+    ns = {}
+    try:
+        exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    finally:
+        os.environ.pop("FASTMAP_B200_LIB", None)
+    g = golden_small
+    pairs = pairs_from(g, "e0_", E.EpipolarPair)
+    p = pairs[0]
+    W = ns["precompute_weights_gpu"](p.x1, p.x2)
+    np.testing.assert_allclose(W, E.precompute_weights(p.x1, p.x2), rtol=1e-12, atol=1e-14)
