@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kPG = 24;          // per-pair gradient record: gRi 9, gRj 9, gdc 3, gphi_i, gphi_j, loss
 constexpr int kMaxSteps = 4096;  // steps per fm_epi_adam_steps call (bias-correction table)
-constexpr int kCamBlock = 128;
 
 struct EpiScratch {
   double* R;      // [N][9]

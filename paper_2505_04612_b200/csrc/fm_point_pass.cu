@@ -34,14 +34,6 @@ namespace {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kNumRed = 46;  // 36 moments + 9 vgrad + post-prune count
 
-__device__ __forceinline__ float4 ld_stream4(const float* p) {
-  float4 r;
-  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-      : "l"(p));
-  return r;
-}
-
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -49,33 +41,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 __device__ __forceinline__ float2 f2(float s) { return make_float2(s, s); }
-
-// Fixed-order warp transpose reduction of 48 floats.  Levels 16/8/4/2 halve
-// the per-lane set (24 + 12 + 6 + 3 shuffles), the last level is a butterfly
-// on the remaining 3 values.  Afterwards lane l holds the warp totals of
-// values [base, base+3), base = 24*b4 + 12*b3 + 6*b2 + 3*b1 (b_k = bit k of l);
-// lanes l and l^1 hold the same totals.
-template <typename T>
-__device__ __forceinline__ void warp_transpose_reduce48(T (&v)[48], int lane) {
-#pragma unroll
-  for (int level = 0; level < 4; ++level) {
-    const int off = 16 >> level;
-    const int half = 24 >> level;
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const T send = upper ? v[i] : v[i + half];
-      const T keep = upper ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 1);
-}
-
-__device__ __forceinline__ int red_base48(int lane) {
-  return 24 * ((lane >> 4) & 1) + 12 * ((lane >> 3) & 1) + 6 * ((lane >> 2) & 1) + 3 * ((lane >> 1) & 1);
-}
 
 // 64-value variant for the generic kernel: lane l ends with values 2l, 2l+1.
 template <typename T>
@@ -162,9 +127,11 @@ __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialB
 // is ill-conditioned and fp32 moments visibly move the optimum.
 // MOM64 = false (opt-in fast mode): fp32 moments with packed FFMA2 plus the
 // shifted-model linearisation terms vgrad / s0.
-constexpr int kRing = 6;        // stages per lane
+#ifndef FM_HOT_RING
+#define FM_HOT_RING 5
+#endif
+constexpr int kRing = FM_HOT_RING;  // stages per lane
 constexpr int kGrpWarps = 4;    // warps per block
-constexpr int kStageSlots = 128;  // (descriptor decode only)
 
 __device__ __forceinline__ float and_mask(float x, unsigned m) {
   unsigned r;
@@ -172,20 +139,24 @@ __device__ __forceinline__ float and_mask(float x, unsigned m) {
   return __uint_as_float(r);
 }
 
-// x if keep else +0.0, as an integer AND so the compiler cannot hoist the
-// fp64 conversion above it (non-finite data on dropped points stays out).
-__device__ __forceinline__ float keep_or_zero(float x, unsigned keep_mask) {
-  return __uint_as_float(__float_as_uint(x) & keep_mask);
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -228,6 +199,16 @@ __global__ void describe_items_kernel(const fm_point_store s, int32_t* __restric
   reinterpret_cast<int4*>(desc)[k] = q;
 }
 
+// What the moment stream needs of one point, produced by the residual head
+// one iteration earlier (software pipelining: the latency-bound head of
+// iteration it+1 -- shared-memory loads, conversions, the fp64 residual
+// chain, the reciprocal -- overlaps the independent DFMA stream of it).
+struct PtCarry {
+  float2 X1, X2;
+  float w;   // IRLS weight, +0 for dropped / pruned / invalid slots
+  float wr;  // w * r (fp32 shifted model only)
+};
+
 template <bool kPrune, bool kL1, bool kMom, bool MOM64>
 struct HotAcc {
   double M64[MOM64 ? 36 : 1];
@@ -248,11 +229,12 @@ struct HotAcc {
     cnt = 0;
   }
 
-  // one point pair; returns the post-prune keep flag.  Branch-free: the
-  // residual and weight are computed for every slot and masked afterwards, so
-  // the compiler can interleave the independent points of an iteration.
-  __device__ __forceinline__ bool point(const double (&G)[9], float2 X1, float2 X2, bool act,
-                                        double thr) {
+  // Residual head of one point pair: prune decision, count, L1, IRLS weight.
+  // Returns the post-prune keep flag.  Branch-free: the residual and weight
+  // are computed for every slot and masked afterwards, so the compiler can
+  // interleave the independent points of an iteration.
+  __device__ __forceinline__ bool head(const double (&G)[9], float2 X1, float2 X2, bool act,
+                                       double thr, PtCarry& C) {
     // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
     const double a = X1.x, bb = X1.y, c = X2.x, dd = X2.y;
     const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
@@ -263,6 +245,8 @@ struct HotAcc {
     const bool keep = kPrune ? (act & (ar <= thr)) : act;
     cnt += keep;
     if (kL1) l1 += act ? ar : 0.0;
+    C.X1 = X1;
+    C.X2 = X2;
     if (kMom) {
       // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58) from the rounded
       // residual: a per-point relative error of the weight keeps every term
@@ -274,45 +258,53 @@ struct HotAcc {
       const float wraw = rcp_approx(fmaxf(arf, 1e-6f));
       // opaque AND (not a select) so the compiler cannot sink the reciprocal
       // into a per-point branch and serialise the iteration's points
-      const float wf = and_mask(wraw, keep ? 0xffffffffu : 0u);
-      const float2 Y1 = X1;
-      const float2 Y2 = X2;
-      if (MOM64) {
-        const double w = wf;
-        const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
-        const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
-        const double wc = w * kc, wd = w * kd;
-        const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-          for (int j = 0; j < 6; ++j)
-            M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
-      } else {
+      C.w = and_mask(wraw, keep ? 0xffffffffu : 0u);
+      if (!MOM64) {
         // w r0 = sign(r) and w r0^2 = |r| unless clamped (|r| < 1e-6)
         const bool big = arf >= 1e-6f;
-        const float wr = keep ? (big ? copysignf(1.f, rf) : rf * 1e6f) : 0.f;
+        C.wr = keep ? (big ? copysignf(1.f, rf) : rf * 1e6f) : 0.f;
         s0f += keep ? (big ? arf : rf * rf * 1e6f) : 0.f;
-        const float2 wX2 = __fmul2_rn(f2(wf), Y2);
-        const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
-        const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
-        const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
-        const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
-#pragma unroll
-        for (int p = 0; p < 6; ++p) {
-          M2[MOM64 ? 0 : p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[MOM64 ? 0 : p * 3 + 0]);
-          M2[MOM64 ? 0 : p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[MOM64 ? 0 : p * 3 + 1]);
-          M2[MOM64 ? 0 : p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[MOM64 ? 0 : p * 3 + 2]);
-        }
-        const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
-        V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
-        V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
-        V2 = __ffma2_rn(f2(wr), Y1, V2);
-        V3 = __fadd2_rn(wrX2, V3);
-        v22 += wr;
       }
     }
     return keep;
+  }
+
+  // Moment stream of one point: W += w t t^T as the 36 Kronecker moments
+  // (plus the shifted-model vgrad terms in fp32 mode).
+  __device__ __forceinline__ void stream(const PtCarry& C) {
+    if (!kMom) return;
+    const float2 Y1 = C.X1, Y2 = C.X2;
+    if (MOM64) {
+      const double w = C.w;
+      const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
+      const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
+      const double wc = w * kc, wd = w * kd;
+      const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+          M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
+    } else {
+      const float wf = C.w, wr = C.wr;
+      const float2 wX2 = __fmul2_rn(f2(wf), Y2);
+      const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
+      const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
+      const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
+      const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        M2[MOM64 ? 0 : p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[MOM64 ? 0 : p * 3 + 0]);
+        M2[MOM64 ? 0 : p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[MOM64 ? 0 : p * 3 + 1]);
+        M2[MOM64 ? 0 : p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[MOM64 ? 0 : p * 3 + 2]);
+      }
+      const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
+      V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
+      V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
+      V2 = __ffma2_rn(f2(wr), Y1, V2);
+      V3 = __fadd2_rn(wrX2, V3);
+      v22 += wr;
+    }
   }
 };
 
@@ -324,7 +316,10 @@ struct HotAcc {
 #define FM_HOT_NPT 4
 #endif
 #ifndef FM_HOT_GSM
-#define FM_HOT_GSM 1
+#define FM_HOT_GSM 0
+#endif
+#ifndef FM_HOT_NOLOAD
+#define FM_HOT_NOLOAD 0  // tuning experiment only: skip the global loads
 #endif
 #ifndef FM_HOT_MINB
 #define FM_HOT_MINB 3
@@ -334,7 +329,7 @@ constexpr bool kGsm = FM_HOT_GSM;  // ghat of the warp's items in shared memory
 struct LaneRing {
   float4 c[kRing][kNpt][32];     // [stage][chunk: x1 (NPT/2), x2 (NPT/2)][lane]
   uint32_t m[kRing][kNpt / 2][32];  // mask word of each slot pair
-  double G[32][9];                // ghat of the warp's items (kGsm)
+  double G[kGsm ? 32 : 1][9];     // ghat of the warp's items (kGsm)
 };
 
 template <int L>
@@ -389,26 +384,37 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   const int len = (has_item && !skip) ? d.len : 0;
   const int nit = (len + kBlk - 1) / kBlk;
   const int warp_it = __reduce_max_sync(0xffffffffu, nit);
-  const int64_t hi = d.lo + len;
+  const int lo_lo = (int)(d.lo & 31);  // slot offsets below are item-relative int32
+  const float4* x1b = reinterpret_cast<const float4*>(s.x1 + 2 * d.lo) + g;
+  const float4* x2b = reinterpret_cast<const float4*>(s.x2 + 2 * d.lo) + g;
+  const uint32_t* mwb = reinterpret_cast<const uint32_t*>(s.active) + (d.lo >> 5);
+  uint32_t* mwb_w = reinterpret_cast<uint32_t*>(s.active) + (d.lo >> 5);
 
   // Iteration `it` of a group covers the kBlk-slot block at d.lo + kBlk*it;
   // lane g copies 16-byte chunks g + L*j (j < NPT/2) of each column, so each
   // copy instruction of the group reads whole 32-byte sectors; the lane owns
-  // slot pairs {2(g + L j), 2(g + L j) + 1}.
-  auto issue = [&](int it) {
-    const int st = it % kRing;
-    if (it < nit) {
-      const int64_t blk = d.lo + (int64_t)kBlk * it;
-      const float4* x1 = reinterpret_cast<const float4*>(s.x1 + 2 * blk);
-      const float4* x2 = reinterpret_cast<const float4*>(s.x2 + 2 * blk);
+  // slot pairs {2(g + L j), 2(g + L j) + 1}.  Every lane reads back only the
+  // ring slots it copied itself, so cp.async.wait_group suffices (no warp
+  // barrier).  Shared addresses are 32-bit and hoisted; the ring stage is a
+  // running index.
+  constexpr uint32_t kChunkB = 32 * 16;              // one chunk row of the warp
+  constexpr uint32_t kStageC = kNpt * kChunkB;       // coordinate bytes per stage
+  constexpr uint32_t kStageM = kPairs * 32 * 4;      // mask bytes per stage
+  const uint32_t ring_c = smem_u32(&ring.c[0][0][lane]);
+  const uint32_t ring_m = smem_u32(&ring.m[0][0][lane]);
+  auto issue = [&](int it, uint32_t st) {  // st = stage index
+    if (FM_HOT_NOLOAD == 0 && it < nit) {
+      const float4* p1 = x1b + (kBlk / 2) * it;
+      const float4* p2 = x2b + (kBlk / 2) * it;
 #pragma unroll
       for (int j = 0; j < kPairs; ++j) {
         // chunks at or past the item end are not fetched (they may lie past
         // the allocation); their stale stage bytes are finite and masked
-        if (blk + 2 * (g + L * j) < hi) {
-          cp_async16(&ring.c[st][j][lane], x1 + g + L * j);
-          cp_async16(&ring.c[st][kPairs + j][lane], x2 + g + L * j);
-          cp_async4(&ring.m[st][j][lane], s.active + ((blk + 2 * (g + L * j)) >> 5));
+        const int off = kBlk * it + 2 * (g + L * j);
+        if (off < len) {
+          cp_async16(ring_c + st * kStageC + j * kChunkB, p1 + L * j);
+          cp_async16(ring_c + st * kStageC + (kPairs + j) * kChunkB, p2 + L * j);
+          cp_async4(ring_m + st * kStageM + j * 128, mwb + ((lo_lo + off) >> 5));
         }
       }
     }
@@ -422,42 +428,43 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   }
   __syncwarp();
 #pragma unroll
-  for (int it = 0; it < kRing - 1; ++it) issue(it);
+  for (int it = 0; it < kRing - 1; ++it) issue(it, it);
 
   HotAcc<kPrune, kL1, kMom, MOM64> acc;
   acc.zero();
+  uint32_t st_issue = kRing - 1, st_read = 0;
 #pragma unroll 1
   for (int it = 0; it < warp_it; ++it) {
-    issue(it + kRing - 1);
+    issue(it + kRing - 1, st_issue);
+    st_issue = st_issue + 1 == kRing ? 0 : st_issue + 1;
     cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
-    const int st = it % kRing;
-    if (it < nit) {
-      const int64_t blk = d.lo + (int64_t)kBlk * it;
-      double Gl[9];
+    // Past the item end (it >= nit, or a lane group without an item) every
+    // slot-valid bit is 0: nothing counts, nothing is pruned, weights are +0.
+    double Gl[9];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) Gl[k] = kGsm ? ring.G[q][k] : G[kGsm ? 0 : k];
-      unsigned keep_all = 0;
+    for (int k = 0; k < 9; ++k) Gl[k] = kGsm ? ring.G[q][k] : G[kGsm ? 0 : k];
+    PtCarry C[kNpt];
 #pragma unroll
-      for (int j = 0; j < kPairs; ++j) {
-        const int64_t sa = blk + 2 * (g + L * j);
-        const int sh = (int)(sa & 31);
-        const int64_t la = hi - sa;
-        const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
-        const unsigned bits = (ring.m[st][j][lane] >> sh) & va;
-        const float4 a = ring.c[st][j][lane];
-        const float4 b = ring.c[st][kPairs + j][lane];
-        unsigned keep_bits = (unsigned)acc.point(Gl, make_float2(a.x, a.y), make_float2(b.x, b.y),
-                                                 bits & 1u, thr);
-        keep_bits |= (unsigned)acc.point(Gl, make_float2(a.z, a.w), make_float2(b.z, b.w),
-                                         (bits >> 1) & 1u, thr) << 1;
-        if (kPrune) {
-          const unsigned cleared = bits & ~keep_bits;
-          if (cleared) atomicAnd(&s.active[sa >> 5], ~(cleared << sh));
-        }
-        keep_all |= keep_bits;
+    for (int j = 0; j < kPairs; ++j) {
+      const int off = kBlk * it + 2 * (g + L * j);
+      const int sh = (lo_lo + off) & 31;
+      const int la = len - off;
+      const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
+      const unsigned bits = FM_HOT_NOLOAD ? va : (lds32(ring_m + st_read * kStageM + j * 128) >> sh) & va;
+      const float4 a = lds128(ring_c + st_read * kStageC + j * kChunkB);
+      const float4 b = lds128(ring_c + st_read * kStageC + (kPairs + j) * kChunkB);
+      unsigned keep_bits = (unsigned)acc.head(Gl, make_float2(a.x, a.y), make_float2(b.x, b.y),
+                                              bits & 1u, thr, C[2 * j]);
+      keep_bits |= (unsigned)acc.head(Gl, make_float2(a.z, a.w), make_float2(b.z, b.w),
+                                      (bits >> 1) & 1u, thr, C[2 * j + 1]) << 1;
+      if (kPrune) {
+        const unsigned cleared = bits & ~keep_bits;
+        if (cleared) atomicAnd(mwb_w + ((lo_lo + off) >> 5), ~(cleared << sh));
       }
-      (void)keep_all;
     }
+    st_read = st_read + 1 == kRing ? 0 : st_read + 1;
+#pragma unroll
+    for (int k = 0; k < kNpt; ++k) acc.stream(C[k]);
   }
   cp_async_wait<0>();
 
