@@ -66,6 +66,7 @@ class ClockSampler:
         self.index = index
         self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
 
     def _run_nvml(self):
@@ -73,17 +74,19 @@ class ClockSampler:
         pynvml.nvmlInit()
         h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
         mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self._ready.set()
         while not self._stop.is_set():
             sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.samples.append((float(sm), float(mx), int(rs)))
-            self._stop.wait(0.005)
+            self._stop.wait(0.001)
 
     def _run_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         bits = [0x8, 0x40, 0x20, 0x4]
+        self._ready.set()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
@@ -100,11 +103,13 @@ class ClockSampler:
             self._run_nvml()
         except Exception:
             self._run_smi()
+        finally:
+            self._ready.set()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.02)
+        self._ready.wait(timeout=30)  # NVML initialised: sampling covers the timed region
         return self
 
     def __exit__(self, *a):
@@ -456,8 +461,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-optimize", action="store_true")
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
-                    help="W-moment accumulation of the pass (irls_refine default: fp64)")
+    ap.add_argument("--precision", default="fp32", choices=["fp64", "fp32"],
+                    help="W-moment accumulation of the pass (irls_refine default: fp32)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     from paper_2505_04612_b200 import scenes

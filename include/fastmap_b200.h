@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 1
+#define FM_ABI_VERSION 2
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -68,8 +68,10 @@ int fm_device_count(void);
 /*
  * Structure of arrays (one (x, y) column per image side, 16 B per point pair),
  * image pairs sorted by (img_i, img_j) (the order of ref/tracks.py:104).  Pair n owns slots [pair_off[n], pair_off[n]+pair_len[n]);
- * pair_off[n] is a multiple of 4 so every 128-bit load belongs to one pair.
- * Padding slots hold zeros and a cleared active bit.  n_slots is a multiple of
+ * pair_off[n] is a multiple of slot_align (>= 4, a power of two) so every
+ * 128-bit load belongs to one pair; slot_align >= 16 selects the hot kernel,
+ * which moves whole 16-slot blocks without bounds checks.  Padding slots hold
+ * zeros and a cleared active bit.  n_slots is a multiple of
  * 128.  The per-point data replaces EpipolarPair.x1/x2/active
  * (ref/epipolar.py:19-36); `terms` is never materialised.
  *
@@ -95,6 +97,7 @@ typedef struct fm_point_store {
    * points, pair | single-item-pair << 31}, filled by fm_point_store_describe;
    * NULL = derived into scratch on every pass. */
   int32_t* item_desc;
+  int64_t slot_align;           /* alignment of pair_off (slots): 4 or a multiple of 16 */
 } fm_point_store;
 
 /* Fill store->item_desc from the pair / item arrays (one small kernel). */

@@ -43,6 +43,7 @@ FM_QUAD_MOM64 = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
+ABI_VERSION = 2
 _F64 = ctypes.c_double
 _SZ = ctypes.c_size_t
 
@@ -51,7 +52,7 @@ class PointStore(ctypes.Structure):
     _fields_ = [("n_pairs", _I64), ("n_slots", _I64), ("n_items", _I64), ("chunk", _I64),
                 ("pair_off", _P), ("pair_len", _P), ("pair_item_off", _P), ("item_pair", _P),
                 ("x1", _P), ("x2", _P), ("x1z", _P), ("x2z", _P), ("active", _P),
-                ("item_desc", _P)]
+                ("item_desc", _P), ("slot_align", _I64)]
 
 
 class PassOut(ctypes.Structure):
@@ -128,7 +129,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.fm_abi_version() != 1:
+        if handle.fm_abi_version() != ABI_VERSION:
             raise RuntimeError("FastMap B200 native library ABI mismatch")
         _LIB = handle
     return _LIB

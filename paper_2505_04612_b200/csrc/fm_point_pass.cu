@@ -70,31 +70,19 @@ struct PartialBufs {
   void* red;   // [kNumRed][n_items] of the accumulator type
   double* s0;  // [n_items]
   double* l1;  // [n_items]
+  int64_t cap; // items the buffers hold
 };
 
-// Hot-kernel accumulator order.  x2 products (rows) and x1 products (cols)
-// are both kept in the order {00, 01, 02, 12, 11, 22} so that pairs
-// (x^2, xy) = x*(x, y), (x, y) and (y^2, 1) are natural float2 registers.
-__device__ __forceinline__ int hot_perm(int k) { return k == 3 ? 4 : (k == 4 ? 3 : k); }
-
-// Canonical output index of hot accumulator slot v (0..45), or -1.
-// 0..35 moments (row-major 6x6 in hot order), 36..44 vgrad pairs, 45 count.
-__device__ __forceinline__ int hot_out_index(int v) {
-  if (v < 36) return hot_perm(v / 6) * 6 + hot_perm(v % 6);
-  switch (v) {  // V0=(v00,v01) V1=(v10,v11) V2=(v20,v21) V3=(v02,v12) v22
-    case 36: return 36 + 0;
-    case 37: return 36 + 1;
-    case 38: return 36 + 3;
-    case 39: return 36 + 4;
-    case 40: return 36 + 6;
-    case 41: return 36 + 7;
-    case 42: return 36 + 2;
-    case 43: return 36 + 5;
-    case 44: return 36 + 8;
-    case 45: return 45;
-    default: return -1;
-  }
+#ifdef FM_HOT_TRACE
+// Tuning build only: per-block {smid, start ns, end ns, items} of the last hot launch.
+__device__ unsigned long long g_hot_trace[16384][4];
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
+#endif
+
 
 __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialBufs& part, bool single,
                                           int64_t P, int64_t NI, int n, int64_t item, int k, float val,
@@ -113,25 +101,53 @@ __device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialB
 }
 
 // ------------------------------------------------------------------ hot kernel
-// z == 1.  A warp works on 32/L consecutive work items at once: L lanes per
-// item (an item is a <= chunk-slot slice of one image pair).  Each lane owns
-// every L-th 4-slot group of its item and streams it through a private
-// per-lane ring of kRing shared-memory stages with cp.async (LDGSTS, 16-byte
-// L2-only copies, one commit group per iteration), so kRing x 64 B per lane
-// are in flight without holding registers.  Per-item totals need only
-// log2(L) butterfly levels across the item's lanes (fixed order -> bitwise
-// reproducible), instead of a 32-lane reduction per item.
+// z == 1 stores whose pairs start on 16-slot boundaries (store->slot_align
+// >= 16; the slots between a pair's last point and the next boundary are
+// inactive padding).  Every work item is then a whole number of 16-slot
+// blocks, so the loop carries no per-slot bounds checks: the active mask alone
+// says which slots count.
 //
-// MOM64 = true (default, exact): the 36 Kronecker moments accumulate in fp64,
-// so W matches the reference's fp64 W to rounding -- the IRLS quadratic form
-// is ill-conditioned and fp32 moments visibly move the optimum.
-// MOM64 = false (opt-in fast mode): fp32 moments with packed FFMA2 plus the
-// shifted-model linearisation terms vgrad / s0.
+// A warp works on 32/L consecutive work items at once: L lanes per item
+// (L in {4, 8}).  Iteration `it` of a lane group covers the 16-slot block at
+// item.lo + 16*it; lane g owns the 16-byte chunks c = g + L*j (j < 8/L) of
+// each coordinate column, i.e. slots {2c, 2c+1} of the block, so each copy
+// instruction of a group reads whole 32-byte sectors.  The chunks stream
+// through a private per-lane ring of kRing shared-memory stages filled with
+// cp.async (LDGSTS, L2-only 16-byte copies, one commit group per iteration):
+// every lane reads back only what it copied itself, so cp.async.wait_group
+// suffices (no barriers).  Per-item totals need log2(L) butterfly levels
+// across the item's lanes (fixed order -> bitwise reproducible).
+//
+// Per point pair: the fp64 residual r = x2^T Ghat x1 (8 DFMA on converted
+// coordinates), the prune decision |r| <= th in fp64, the pre-prune L1 in
+// fp64, the IRLS weight 1/max(|r|, 1e-6) (fp32 reciprocal of the rounded
+// residual: a per-point relative error keeps every term rank-1 exact) masked
+// by the post-prune keep bit, and the 36 Kronecker moments
+//   mom[i][j] = sum w B_i A_j,  B = (c^2, cd, c, d^2, d, 1),
+//                               A = (a^2, ab, a, b^2, b, 1)
+// for x1 = (a, b), x2 = (c, d).
+// MOM64 = true (exact): the moments accumulate in fp64 (36 DFMA / point).
+// MOM64 = false (fast): fp32 moments in the "B-pair" form -- each A_j is a
+// scalar broadcast against the three natural float2 pairs
+//   (w c^2, w d^2) = (w c, w d) * (c, d),  (w c, w d),  (w c d, w)
+// so 15 packed FFMA2 + 3 FADD2 cover the 36 moments -- plus the shifted-model
+// linearisation terms vgrad = sum w r t and s0 = sum w r^2.
 #ifndef FM_HOT_RING
 #define FM_HOT_RING 5
 #endif
+#ifndef FM_HOT_UNROLL
+#define FM_HOT_UNROLL 1
+#endif
+#ifndef FM_HOT_MINB
+#define FM_HOT_MINB 4
+#endif
+#ifndef FM_HOT_MINB64
+#define FM_HOT_MINB64 3
+#endif
 constexpr int kRing = FM_HOT_RING;  // stages per lane
-constexpr int kGrpWarps = 4;    // warps per block
+constexpr int kUnroll = FM_HOT_UNROLL;  // main-loop unroll (points in flight per lane = 4 x kUnroll)
+constexpr int kGrpWarps = 4;        // warps per block
+constexpr int kBlkSlots = 16;       // slots per group iteration (= slot alignment)
 
 __device__ __forceinline__ float and_mask(float x, unsigned m) {
   unsigned r;
@@ -199,21 +215,33 @@ __global__ void describe_items_kernel(const fm_point_store s, int32_t* __restric
   reinterpret_cast<int4*>(desc)[k] = q;
 }
 
-// What the moment stream needs of one point, produced by the residual head
-// one iteration earlier (software pipelining: the latency-bound head of
-// iteration it+1 -- shared-memory loads, conversions, the fp64 residual
-// chain, the reciprocal -- overlaps the independent DFMA stream of it).
-struct PtCarry {
-  float2 X1, X2;
-  float w;   // IRLS weight, +0 for dropped / pruned / invalid slots
-  float wr;  // w * r (fp32 shifted model only)
-};
+#ifndef FM_HOT_NOLOAD
+#define FM_HOT_NOLOAD 0  // tuning experiment only: skip the coordinate/mask copies
+#endif
+#ifndef FM_HOT_F2F
+#define FM_HOT_F2F 0  // 1: plain F2F conversions in the residual head (reference variant)
+#endif
+constexpr double kUnscale = 0x1p896;  // 2^(1023 - 127)
+
+// fp32 -> fp64 on the integer pipe: the double whose bits are the fp32 bits
+// shifted right by 3 (sign restored) equals x * 2^-896 exactly for every finite
+// x -- normal, subnormal and signed zero -- because the fp32 exponent field
+// lands unbiased in the low 8 bits of the fp64 exponent field.  Stores on the
+// hot path hold finite coordinates only (slot_align >= 16 contract).
+__device__ __forceinline__ double scaled_f2d(float x) {
+  // hi: arithmetic shift keeps the sign in bit 31 and smears it over bits
+  // 30..28, which the mask clears; lo: the 3 low mantissa bits.
+  const int u = __float_as_int(x);
+  return __hiloint2double((u >> 3) & (int)0x8FFFFFFF, u << 29);
+}
 
 template <bool kPrune, bool kL1, bool kMom, bool MOM64>
 struct HotAcc {
+  // plain F2F conversions where the fp64 moments need the coordinates anyway
+  static constexpr bool kF2F = FM_HOT_F2F || (kMom && MOM64);
   double M64[MOM64 ? 36 : 1];
-  float2 M2[MOM64 ? 1 : 18];
-  float2 V0, V1, V2, V3;
+  float2 Mp[MOM64 ? 1 : 18];  // [j][k]: A_j x B-pair k, k: (B0,B3) (B2,B4) (B1,B5)
+  float2 V0, V1, V2, V3;      // (v00,v01) (v10,v11) (v20,v21) (v02,v12)
   float v22, s0f;
   double l1;
   int cnt;
@@ -222,115 +250,93 @@ struct HotAcc {
 #pragma unroll
     for (int k = 0; k < (MOM64 ? 36 : 1); ++k) M64[k] = 0.0;
 #pragma unroll
-    for (int k = 0; k < (MOM64 ? 1 : 18); ++k) M2[k] = f2(0.f);
+    for (int k = 0; k < (MOM64 ? 1 : 18); ++k) Mp[k] = f2(0.f);
     V0 = V1 = V2 = V3 = f2(0.f);
     v22 = s0f = 0.f;
     l1 = 0.0;
     cnt = 0;
   }
 
-  // Residual head of one point pair: prune decision, count, L1, IRLS weight.
-  // Returns the post-prune keep flag.  Branch-free: the residual and weight
-  // are computed for every slot and masked afterwards, so the compiler can
-  // interleave the independent points of an iteration.
-  __device__ __forceinline__ bool head(const double (&G)[9], float2 X1, float2 X2, bool act,
-                                       double thr, PtCarry& C) {
-    // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
-    const double a = X1.x, bb = X1.y, c = X2.x, dd = X2.y;
-    const double y0 = fma(G[0], a, fma(G[1], bb, G[2]));
-    const double y1 = fma(G[3], a, fma(G[4], bb, G[5]));
-    const double y2 = fma(G[6], a, fma(G[7], bb, G[8]));
-    const double r = fma(c, y0, fma(dd, y1, y2));
+  // One point pair; returns the post-prune keep flag.  Branch-free: the
+  // residual and weight are computed for every slot and masked afterwards.
+  __device__ __forceinline__ bool point(const double (&G)[9], float a, float b, float c, float d,
+                                        bool act, double thr) {
+    // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255).  The fp32
+    // coordinates enter as x 2^-896 built on the integer pipe (scaled_f2d);
+    // G's coordinate columns carry the inverse factor 2^896 and y0, y1 are
+    // rescaled by it, so every DFMA sees the same exact products and rounds
+    // exactly as with (double)x -- without the XU-bound F2F conversions.
+    double A, B, C, D, r;
+    if (kF2F) {  // exact fp64 moments reuse the converted coordinates
+      A = a; B = b; C = c; D = d;
+      const double y0 = fma(G[0], A, fma(G[1], B, G[2]));
+      const double y1 = fma(G[3], A, fma(G[4], B, G[5]));
+      const double y2 = fma(G[6], A, fma(G[7], B, G[8]));
+      r = fma(C, y0, fma(D, y1, y2));
+    } else {
+      const double As = scaled_f2d(a), Bs = scaled_f2d(b), Cs = scaled_f2d(c), Ds = scaled_f2d(d);
+      const double y0 = fma(G[0], As, fma(G[1], Bs, G[2])) * kUnscale;
+      const double y1 = fma(G[3], As, fma(G[4], Bs, G[5])) * kUnscale;
+      const double y2 = fma(G[6], As, fma(G[7], Bs, G[8]));
+      r = fma(Cs, y0, fma(Ds, y1, y2));
+      A = B = C = D = 0.0;
+    }
     const double ar = fabs(r);
-    const bool keep = kPrune ? (act & (ar <= thr)) : act;
-    cnt += keep;
+    const bool keep = (kPrune && !FM_HOT_NOLOAD) ? (act & (ar <= thr)) : act;
     if (kL1) l1 += act ? ar : 0.0;
-    C.X1 = X1;
-    C.X2 = X2;
-    if (kMom) {
-      // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58) from the rounded
-      // residual: a per-point relative error of the weight keeps every term
-      // rank-1 exact.  Coordinates of every slot are finite (the store
-      // builders zero and deactivate non-finite points), so a zero weight
-      // removes a dropped point exactly without selecting its coordinates.
-      const float rf = (float)r;
-      const float arf = fabsf(rf);
-      const float wraw = rcp_approx(fmaxf(arf, 1e-6f));
-      // opaque AND (not a select) so the compiler cannot sink the reciprocal
-      // into a per-point branch and serialise the iteration's points
-      C.w = and_mask(wraw, keep ? 0xffffffffu : 0u);
-      if (!MOM64) {
-        // w r0 = sign(r) and w r0^2 = |r| unless clamped (|r| < 1e-6)
-        const bool big = arf >= 1e-6f;
-        C.wr = keep ? (big ? copysignf(1.f, rf) : rf * 1e6f) : 0.f;
-        s0f += keep ? (big ? arf : rf * rf * 1e6f) : 0.f;
+    if (!kMom) return keep;
+    // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); the opaque AND (not a
+    // select) keeps the reciprocal out of a per-point branch.  Coordinates of
+    // every slot are finite (store builders zero and deactivate non-finite
+    // points), so w = +0 removes a dropped point exactly.
+    const float rf = (float)r;
+    const float w = and_mask(rcp_approx(fmaxf(fabsf(rf), 1e-6f)), keep ? 0xffffffffu : 0u);
+    if (MOM64) {
+      const double wd = w;
+      const double p = wd * C, q = wd * D;
+      const double Bv[6] = {p * C, p * D, p, q * D, q, wd};
+      const double Av[5] = {A * A, A * B, A, B * B, B};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) M64[MOM64 ? i * 6 + j : 0] = fma(Bv[i], Av[j], M64[MOM64 ? i * 6 + j : 0]);
+        M64[MOM64 ? i * 6 + 5 : 0] += Bv[i];
       }
+    } else {
+      const float2 X1 = make_float2(a, b), X2 = make_float2(c, d);
+      const float2 PQ = __fmul2_rn(f2(w), X2);         // (w c, w d)
+      const float2 Bp[3] = {__fmul2_rn(PQ, X2),        // (w c^2, w d^2)
+                            PQ,                        // (w c, w d)
+                            make_float2(PQ.x * d, w)}; // (w c d, w)
+      const float2 AA = __fmul2_rn(f2(a), X1);         // (a^2, a b)
+      const float Av[5] = {AA.x, AA.y, a, b * b, b};
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          Mp[MOM64 ? 0 : j * 3 + k] = __ffma2_rn(f2(Av[j]), Bp[k], Mp[MOM64 ? 0 : j * 3 + k]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) Mp[MOM64 ? 0 : 15 + k] = __fadd2_rn(Bp[k], Mp[MOM64 ? 0 : 15 + k]);
+      // shifted-model terms: w r0 (= sign(r0) unless clamped), w r0^2
+      const float wr = w * rf;
+      s0f = fmaf(wr, rf, s0f);
+      const float2 S = __fmul2_rn(f2(wr), X2);
+      V0 = __ffma2_rn(f2(S.x), X1, V0);
+      V1 = __ffma2_rn(f2(S.y), X1, V1);
+      V2 = __ffma2_rn(f2(wr), X1, V2);
+      V3 = __fadd2_rn(S, V3);
+      v22 += wr;
     }
     return keep;
   }
-
-  // Moment stream of one point: W += w t t^T as the 36 Kronecker moments
-  // (plus the shifted-model vgrad terms in fp32 mode).
-  __device__ __forceinline__ void stream(const PtCarry& C) {
-    if (!kMom) return;
-    const float2 Y1 = C.X1, Y2 = C.X2;
-    if (MOM64) {
-      const double w = C.w;
-      const double ka = Y1.x, kb = Y1.y, kc = Y2.x, kd = Y2.y;
-      const double A[6] = {ka * ka, ka * kb, ka, kb * kb, kb, 1.0};
-      const double wc = w * kc, wd = w * kd;
-      const double B[6] = {wc * kc, wc * kd, wc, wd * kd, wd, w};
-#pragma unroll
-      for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int j = 0; j < 6; ++j)
-          M64[MOM64 ? i * 6 + j : 0] = fma(B[i], A[j], M64[MOM64 ? i * 6 + j : 0]);
-    } else {
-      const float wf = C.w, wr = C.wr;
-      const float2 wX2 = __fmul2_rn(f2(wf), Y2);
-      const float B[6] = {wX2.x * Y2.x, wX2.x * Y2.y, wX2.x, wX2.y * Y2.y, wX2.y, wf};
-      const float2 A0 = __fmul2_rn(f2(Y1.x), Y1);
-      const float2 A2 = make_float2(Y1.y * Y1.y, 1.f);
-      const float Brow[6] = {B[0], B[1], B[2], B[4], B[3], B[5]};
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        M2[MOM64 ? 0 : p * 3 + 0] = __ffma2_rn(f2(Brow[p]), A0, M2[MOM64 ? 0 : p * 3 + 0]);
-        M2[MOM64 ? 0 : p * 3 + 1] = __ffma2_rn(f2(Brow[p]), Y1, M2[MOM64 ? 0 : p * 3 + 1]);
-        M2[MOM64 ? 0 : p * 3 + 2] = __ffma2_rn(f2(Brow[p]), A2, M2[MOM64 ? 0 : p * 3 + 2]);
-      }
-      const float2 wrX2 = __fmul2_rn(f2(wr), Y2);
-      V0 = __ffma2_rn(f2(wrX2.x), Y1, V0);
-      V1 = __ffma2_rn(f2(wrX2.y), Y1, V1);
-      V2 = __ffma2_rn(f2(wr), Y1, V2);
-      V3 = __fadd2_rn(wrX2, V3);
-      v22 += wr;
-    }
-  }
 };
 
-// Per-lane ring: stage d holds the lane's NPT slots of x1 and x2 (NPT/2
-// 16-byte chunks each) and the mask words, laid out chunk-major so that a
-// warp's LDS.128 of one chunk touches 32 consecutive 16-byte words (no bank
-// conflicts).
-#ifndef FM_HOT_NPT
-#define FM_HOT_NPT 4
-#endif
-#ifndef FM_HOT_GSM
-#define FM_HOT_GSM 0
-#endif
-#ifndef FM_HOT_NOLOAD
-#define FM_HOT_NOLOAD 0  // tuning experiment only: skip the global loads
-#endif
-#ifndef FM_HOT_MINB
-#define FM_HOT_MINB 3
-#endif
-constexpr int kNpt = FM_HOT_NPT;   // points per lane per iteration (2 or 4)
-constexpr bool kGsm = FM_HOT_GSM;  // ghat of the warp's items in shared memory
-struct LaneRing {
-  float4 c[kRing][kNpt][32];     // [stage][chunk: x1 (NPT/2), x2 (NPT/2)][lane]
-  uint32_t m[kRing][kNpt / 2][32];  // mask word of each slot pair
-  double G[kGsm ? 32 : 1][9];     // ghat of the warp's items (kGsm)
-};
+// Canonical moment index (row i = B, column j = A) of hot fp32 slot v (0..35).
+__device__ __forceinline__ int hot_mom_index(int v) {
+  const int j = (v >> 1) / 3, k = (v >> 1) % 3, h = v & 1;
+  constexpr int kRow[3][2] = {{0, 3}, {2, 4}, {1, 5}};
+  return kRow[k][h] * 6 + j;
+}
 
 template <int L>
 __device__ __forceinline__ double group_sum(double x) {
@@ -338,15 +344,45 @@ __device__ __forceinline__ double group_sum(double x) {
   for (int off = 1; off < L; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
   return x;
 }
-template <int L>
-__device__ __forceinline__ float group_sumf(float x) {
+
+// Transpose-reduce of N values (N % L == 0) across the L lanes of an aligned
+// lane group: every level halves the values a lane carries (it keeps one half,
+// sends the other to its partner), so log2(L) levels cost N/2 + N/4 + ...
+// shuffles instead of N log2(L).  Afterwards lane g of the group holds the
+// group sums of values [g N/L, (g+1) N/L) in v[0 .. N/L).  Fixed order ->
+// bitwise reproducible.
+template <int L, int N, typename T>
+__device__ __forceinline__ void group_transpose_reduce(T (&v)[N], int lane) {
+  static_assert(N % L == 0, "N must be a multiple of L");
 #pragma unroll
-  for (int off = 1; off < L; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-  return x;
+  for (int lvl = 0; (1 << lvl) < L; ++lvl) {
+    const int o = L >> (lvl + 1);
+    const int half = N >> (lvl + 1);
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const T send = upper ? v[i] : v[i + half];
+      const T keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
 }
 
+// Per-lane ring: stage d holds the lane's two chunks of x1 then of x2
+// (chunk-major: a warp's LDS.128 of one chunk row touches 32 consecutive
+// 16-byte words) and the mask word of the lane's block.
+struct LaneRing {
+  float4 c[kRing][4][32];
+  uint32_t m[kRing][32];
+};
+
+// L = 4 S lanes per work item: S sub-groups of 4 lanes; iteration `it`
+// covers blocks S*it .. S*it + S - 1 of the item, sub-group sg takes block
+// S*it + sg, and its lane h the 16-byte chunks h and h + 4 of each column
+// (slots {2h, 2h+1, 2h+8, 2h+9}): every copy instruction of a sub-group reads
+// whole 32-byte sectors.
 template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kGrpWarps * 32, FM_HOT_MINB)
+__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
 point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                const int32_t* __restrict__ prev_active, const fm_pass_out out,
                const PartialBufs part) {
@@ -355,68 +391,59 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
   constexpr bool kLin = kMom && !MOM64;
   constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
-  constexpr int IPW = 32 / L;        // items per warp
-  constexpr int kPairs = kNpt / 2;   // slot pairs (16-byte chunks per column) per lane
-  constexpr int kBlk = kNpt * L;     // slots per group iteration
+  constexpr int IPW = 32 / L;  // items per warp
+  constexpr int S = L / 4;     // blocks per iteration
+  static_assert(L == 4 || L == 8 || L == 16, "L in {4, 8, 16}");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   LaneRing& ring = reinterpret_cast<LaneRing*>(smem_raw)[wib];
+#ifdef FM_HOT_TRACE
+  const unsigned long long t_start = globaltimer();
+#endif
   const int64_t P = s.n_pairs;
-  const int64_t NI = s.n_items;
   const int g = lane % L;  // lane within the item group
-  const int q = lane / L;  // item within the warp
-  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + q;
-  const bool has_item = item < NI;
+  const int sg = g >> 2;   // sub-group: block offset within an iteration
+  const int h = g & 3;     // lane within the sub-group
+  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + lane / L;
+  const bool has_item = item < s.n_items;
+  const int64_t NI = s.n_items;
 
   ItemDesc d{0, 0, 0, true};
   if (has_item) d = decode_item(__ldg(reinterpret_cast<const int4*>(s.item_desc) + item));
   const bool skip = has_item && kSkip && prev_active[d.n] == 0;
-  double G[kGsm ? 1 : 9];
-  if (kGsm) {
-    for (int k = g; k < 9; k += L) ring.G[q][k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
-  } else {
+  double G[9];
 #pragma unroll
-    for (int k = 0; k < (kGsm ? 1 : 9); ++k) G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+  for (int k = 0; k < 9; ++k) {
+    G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+    if (!HotAcc<kPrune, kL1, kMom, MOM64>::kF2F && k % 3 != 2) G[k] *= kUnscale;  // coordinate columns (exact)
   }
-  // iterations of this group: kBlk-slot blocks of the item (same for its lanes)
-  const int len = (has_item && !skip) ? d.len : 0;
-  const int nit = (len + kBlk - 1) / kBlk;
+  const int nblk = (has_item && !skip) ? (d.len + kBlkSlots - 1) / kBlkSlots : 0;
+  const int nit = (nblk + S - 1) / S;
   const int warp_it = __reduce_max_sync(0xffffffffu, nit);
-  const int lo_lo = (int)(d.lo & 31);  // slot offsets below are item-relative int32
-  const float4* x1b = reinterpret_cast<const float4*>(s.x1 + 2 * d.lo) + g;
-  const float4* x2b = reinterpret_cast<const float4*>(s.x2 + 2 * d.lo) + g;
+
+  // 16 slots = 128 B = 8 float4 per column per block
+  const float4* x1b = reinterpret_cast<const float4*>(s.x1 + 2 * d.lo) + 8 * sg + h;
+  const float4* x2b = reinterpret_cast<const float4*>(s.x2 + 2 * d.lo) + 8 * sg + h;
+  const int half0 = (int)(d.lo & 16) + kBlkSlots * sg;  // bit of block sg relative to word lo/32
   const uint32_t* mwb = reinterpret_cast<const uint32_t*>(s.active) + (d.lo >> 5);
   uint32_t* mwb_w = reinterpret_cast<uint32_t*>(s.active) + (d.lo >> 5);
 
-  // Iteration `it` of a group covers the kBlk-slot block at d.lo + kBlk*it;
-  // lane g copies 16-byte chunks g + L*j (j < NPT/2) of each column, so each
-  // copy instruction of the group reads whole 32-byte sectors; the lane owns
-  // slot pairs {2(g + L j), 2(g + L j) + 1}.  Every lane reads back only the
-  // ring slots it copied itself, so cp.async.wait_group suffices (no warp
-  // barrier).  Shared addresses are 32-bit and hoisted; the ring stage is a
-  // running index.
-  constexpr uint32_t kChunkB = 32 * 16;              // one chunk row of the warp
-  constexpr uint32_t kStageC = kNpt * kChunkB;       // coordinate bytes per stage
-  constexpr uint32_t kStageM = kPairs * 32 * 4;      // mask bytes per stage
+  constexpr uint32_t kChunkB = 32 * 16;  // one chunk row of the warp
+  constexpr uint32_t kStageC = 4 * kChunkB;
+  constexpr uint32_t kStageM = 32 * 4;
   const uint32_t ring_c = smem_u32(&ring.c[0][0][lane]);
-  const uint32_t ring_m = smem_u32(&ring.m[0][0][lane]);
-  auto issue = [&](int it, uint32_t st) {  // st = stage index
-    if (FM_HOT_NOLOAD == 0 && it < nit) {
-      const float4* p1 = x1b + (kBlk / 2) * it;
-      const float4* p2 = x2b + (kBlk / 2) * it;
-#pragma unroll
-      for (int j = 0; j < kPairs; ++j) {
-        // chunks at or past the item end are not fetched (they may lie past
-        // the allocation); their stale stage bytes are finite and masked
-        const int off = kBlk * it + 2 * (g + L * j);
-        if (off < len) {
-          cp_async16(ring_c + st * kStageC + j * kChunkB, p1 + L * j);
-          cp_async16(ring_c + st * kStageC + (kPairs + j) * kChunkB, p2 + L * j);
-          cp_async4(ring_m + st * kStageM + j * 128, mwb + ((lo_lo + off) >> 5));
-        }
-      }
+  const uint32_t ring_m = smem_u32(&ring.m[0][lane]);
+  auto issue = [&](int it, uint32_t st) {
+    if (!FM_HOT_NOLOAD && S * it + sg < nblk) {
+      const float4* p1 = x1b + 8 * S * it;
+      const float4* p2 = x2b + 8 * S * it;
+      cp_async16(ring_c + st * kStageC, p1);
+      cp_async16(ring_c + st * kStageC + kChunkB, p1 + 4);
+      cp_async16(ring_c + st * kStageC + 2 * kChunkB, p2);
+      cp_async16(ring_c + st * kStageC + 3 * kChunkB, p2 + 4);
+      cp_async4(ring_m + st * kStageM, mwb + ((half0 + kBlkSlots * S * it) >> 5));
     }
     cp_async_commit();
   };
@@ -424,7 +451,7 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
 #pragma unroll
     for (int st = 0; st < kRing; ++st)
 #pragma unroll
-      for (int c = 0; c < kNpt; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < 4; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncwarp();
 #pragma unroll
@@ -433,91 +460,101 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   HotAcc<kPrune, kL1, kMom, MOM64> acc;
   acc.zero();
   uint32_t st_issue = kRing - 1, st_read = 0;
-#pragma unroll 1
+#pragma unroll kUnroll
   for (int it = 0; it < warp_it; ++it) {
     issue(it + kRing - 1, st_issue);
     st_issue = st_issue + 1 == kRing ? 0 : st_issue + 1;
     cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
-    // Past the item end (it >= nit, or a lane group without an item) every
-    // slot-valid bit is 0: nothing counts, nothing is pruned, weights are +0.
-    double Gl[9];
+    // a block past the item end reads mask 0: nothing counts, nothing is
+    // pruned, weights are +0 (its stale ring bytes are finite)
+    const int pos = half0 + kBlkSlots * S * it;  // block's first bit, relative to word lo/32
+    const uint32_t blk = (S * it + sg < nblk) ? (FM_HOT_NOLOAD ? 0xffffu : lds32(ring_m + st_read * kStageM) >> (pos & 31)) : 0u;
+    uint32_t cleared = 0;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Gl[k] = kGsm ? ring.G[q][k] : G[kGsm ? 0 : k];
-    PtCarry C[kNpt];
-#pragma unroll
-    for (int j = 0; j < kPairs; ++j) {
-      const int off = kBlk * it + 2 * (g + L * j);
-      const int sh = (lo_lo + off) & 31;
-      const int la = len - off;
-      const unsigned va = la >= 2 ? 3u : (la > 0 ? 1u : 0u);
-      const unsigned bits = FM_HOT_NOLOAD ? va : (lds32(ring_m + st_read * kStageM + j * 128) >> sh) & va;
-      const float4 a = lds128(ring_c + st_read * kStageC + j * kChunkB);
-      const float4 b = lds128(ring_c + st_read * kStageC + (kPairs + j) * kChunkB);
-      unsigned keep_bits = (unsigned)acc.head(Gl, make_float2(a.x, a.y), make_float2(b.x, b.y),
-                                              bits & 1u, thr, C[2 * j]);
-      keep_bits |= (unsigned)acc.head(Gl, make_float2(a.z, a.w), make_float2(b.z, b.w),
-                                      (bits >> 1) & 1u, thr, C[2 * j + 1]) << 1;
-      if (kPrune) {
-        const unsigned cleared = bits & ~keep_bits;
-        if (cleared) atomicAnd(mwb_w + ((lo_lo + off) >> 5), ~(cleared << sh));
-      }
+    for (int j = 0; j < 2; ++j) {
+      const int c2 = 2 * h + 8 * j;  // first slot of the chunk within the block
+      const unsigned bits = (blk >> c2) & 3u;
+      const float4 x1 = lds128(ring_c + st_read * kStageC + j * kChunkB);
+      const float4 x2 = lds128(ring_c + st_read * kStageC + (2 + j) * kChunkB);
+      unsigned keep = (unsigned)acc.point(G, x1.x, x1.y, x2.x, x2.y, bits & 1u, thr);
+      keep |= (unsigned)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bits >> 1) & 1u, thr) << 1;
+      acc.cnt += __popc(keep);
+      if (kPrune) cleared |= (bits & ~keep) << c2;
     }
+    if (kPrune && cleared) atomicAnd(mwb_w + (pos >> 5), ~(cleared << (pos & 31)));
     st_read = st_read + 1 == kRing ? 0 : st_read + 1;
-#pragma unroll
-    for (int k = 0; k < kNpt; ++k) acc.stream(C[k]);
   }
   cp_async_wait<0>();
+#ifdef FM_HOT_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 16384) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_hot_trace[blockIdx.x][0] = smid;
+    g_hot_trace[blockIdx.x][1] = t_start;
+    g_hot_trace[blockIdx.x][2] = globaltimer();
+  }
+#endif
 
   // ------------------------------------------------------------------ reduce
-  // log2(L) butterfly levels within the item's lanes; lane g then writes
-  // outputs k = g, g + L, ... (consecutive items -> coalesced SoA stores)
+  // transpose-reduce within the item's lanes; lane g then writes its N/L
+  // outputs (consecutive items -> neighbouring SoA stores)
   const bool single = d.single;
   if (kMom && MOM64) {
-    double v[38];
+    constexpr int N = L <= 8 ? 40 : 48;  // 36 moments, count, l1, padding
+    double v[N];
 #pragma unroll
-    for (int k = 0; k < 36; ++k) v[k] = group_sum<L>(acc.M64[MOM64 ? k : 0]);
-    v[36] = group_sum<L>((double)acc.cnt);
-    v[37] = group_sum<L>(acc.l1);
+    for (int k = 0; k < 36; ++k) v[k] = acc.M64[MOM64 ? k : 0];
+    v[36] = (double)acc.cnt;
+    v[37] = acc.l1;
+#pragma unroll
+    for (int k = 38; k < N; ++k) v[k] = 0.0;
+    group_transpose_reduce<L>(v, lane);
     if (has_item) {
 #pragma unroll
-      for (int k = 0; k < 38; ++k) {
-        if (k % L != g) continue;
+      for (int i = 0; i < N / L; ++i) {
+        const int k = g * (N / L) + i;
         if (!single) {
-          if (k < 36) static_cast<double*>(part.red)[k * NI + item] = v[k];
-          else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = v[k];
-          else part.l1[item] = v[k];
+          if (k < 36) static_cast<double*>(part.red)[k * NI + item] = v[i];
+          else if (k == 36) static_cast<double*>(part.red)[45 * NI + item] = v[i];
+          else if (k == 37) part.l1[item] = v[i];
         } else if (k < 36) {
-          out.mom64[k * P + d.n] = v[k];
+          out.mom64[k * P + d.n] = v[i];
         } else if (k == 36) {
-          if (out.n_active) out.n_active[d.n] = (int32_t)v[k];
-        } else if (kL1 && out.l1) {
-          out.l1[d.n] = v[k];
+          if (out.n_active) out.n_active[d.n] = (int32_t)v[i];
+        } else if (k == 37) {
+          if (kL1 && out.l1) out.l1[d.n] = v[i];
         }
       }
     }
   } else if (kMom) {
-    float v[47];
+    constexpr int N = 48;  // 36 moments (hot order), 9 vgrad, count, s0, padding
+    float v[N];
 #pragma unroll
     for (int k = 0; k < 18; ++k) {
-      v[2 * k] = group_sumf<L>(acc.M2[MOM64 ? 0 : k].x);
-      v[2 * k + 1] = group_sumf<L>(acc.M2[MOM64 ? 0 : k].y);
+      v[2 * k] = acc.Mp[MOM64 ? 0 : k].x;
+      v[2 * k + 1] = acc.Mp[MOM64 ? 0 : k].y;
     }
-    const float vv[11] = {acc.V0.x, acc.V0.y, acc.V1.x, acc.V1.y, acc.V2.x, acc.V2.y,
-                          acc.V3.x, acc.V3.y, acc.v22, (float)acc.cnt, acc.s0f};
-#pragma unroll
-    for (int k = 0; k < 11; ++k) v[36 + k] = group_sumf<L>(vv[k]);
+    // vgrad canonical order v[p*3+q]: 00 01 02 10 11 12 20 21 22
+    v[36] = acc.V0.x; v[37] = acc.V0.y; v[38] = acc.V3.x;
+    v[39] = acc.V1.x; v[40] = acc.V1.y; v[41] = acc.V3.y;
+    v[42] = acc.V2.x; v[43] = acc.V2.y; v[44] = acc.v22;
+    v[45] = (float)acc.cnt;
+    v[46] = acc.s0f;
+    v[47] = 0.f;
+    group_transpose_reduce<L>(v, lane);
     const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
     if (has_item) {
 #pragma unroll
-      for (int vi = 0; vi < 47; ++vi) {
-        if (vi % L != g) continue;
+      for (int i = 0; i < N / L; ++i) {
+        const int vi = g * (N / L) + i;
         if (vi == 46) {
-          if (single) out.s0[d.n] = (double)v[vi];
-          else part.s0[item] = (double)v[vi];
-          continue;
+          if (single) out.s0[d.n] = (double)v[i];
+          else part.s0[item] = (double)v[i];
+        } else if (vi < 46) {
+          const int k = vi < 36 ? hot_mom_index(vi) : vi;
+          store_red(out, part, single, P, NI, d.n, item, k, v[i], kLin);
         }
-        const int k = hot_out_index(vi);
-        if (k >= 0) store_red(out, part, single, P, NI, d.n, item, k, v[vi], kLin);
       }
       if (kL1 && g == 0) {
         if (single) {
@@ -535,11 +572,16 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
         if (out.n_active) out.n_active[d.n] = cnt;
         if (kL1 && out.l1) out.l1[d.n] = l1;
       } else {
-        static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
+        if (MOM64) static_cast<double*>(part.red)[45 * NI + item] = (double)cnt;
+        else static_cast<float*>(part.red)[45 * NI + item] = (float)cnt;
         if (kL1) part.l1[item] = l1;
       }
     }
   }
+#ifdef FM_HOT_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 16384) g_hot_trace[blockIdx.x][3] = globaltimer();
+#endif
 }
 
 // -------------------------------------------------------------- generic kernel
@@ -732,6 +774,7 @@ __global__ void combine_kernel(const fm_point_store s, const fm_pass_out out,
   }
 }
 
+
 template <unsigned MODE, bool MOM64, int L>
 int hot_blocks_per_sm(int* out) {
   static int cached = 0;
@@ -765,32 +808,34 @@ int launch_hot_l(const fm_point_store& s, double thr, const double* ghat, const 
   return FM_OK;
 }
 
-// Lanes per item L: blocks are one-shot, so the last wave of a launch is
-// partially filled.  Score each L by (work / slots-time) of its wave count
-// and a per-item reduction cost of log2(L) butterfly levels; short items
-// (< 4L slots per lane-iteration) also waste lanes.
+// Lanes per item L in {4, 8, 16}: blocks are one-shot, so the last wave of
+// a launch is partially filled.  Score each L by the filled fraction of its
+// waves and a per-item reduction cost (log2(L) transpose-reduce levels plus a
+// per-iteration cost for blocks an item leaves idle in its last iteration).
 template <unsigned MODE, bool MOM64>
 int launch_hot(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
                const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
-  int b4 = 1, b8 = 1, b16 = 1;
-  if (int rc = hot_blocks_per_sm<MODE, MOM64, 4>(&b4)) return rc;
-  if (int rc = hot_blocks_per_sm<MODE, MOM64, 8>(&b8)) return rc;
-  if (int rc = hot_blocks_per_sm<MODE, MOM64, 16>(&b16)) return rc;
-  const double mean_len = s.n_items ? (double)s.n_slots / (double)s.n_items : 0.0;
+  int bps[3] = {1, 1, 1};
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 4>(&bps[0])) return rc;
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 8>(&bps[1])) return rc;
+  if (int rc = hot_blocks_per_sm<MODE, MOM64, 16>(&bps[2])) return rc;
+  const double mean_blk = s.n_items ? (double)s.n_slots / kBlkSlots / (double)s.n_items : 0.0;
   const int Ls[3] = {4, 8, 16};
-  const int bps[3] = {b4, b8, b16};
   double best = -1.0;
   int pick = 4;
   for (int k = 0; k < 3; ++k) {
     const int L = Ls[k];
+    const double S = L / 4;
     const double blocks = std::ceil((double)s.n_items / (32.0 / L) / kGrpWarps);
     const double resident = (double)bps[k] * sm_count();
     const double waves = blocks / resident;
     const double fill = waves / std::ceil(waves);
-    const double lane_use = std::min(1.0, mean_len / (4.0 * L)) ;
-    const double red = 1.0 / (1.0 + 0.02 * (k + 2) * 400.0 / std::max(mean_len, 1.0));
-    const double score = fill * lane_use * red;
-    if (score > best * 1.03) {
+    // per-item work in iterations (rounded up to S blocks) + reduction (~4 iterations per level)
+    const double iters = std::ceil(std::max(mean_blk, 1.0) / S);
+    const double useful = std::max(mean_blk, 1.0) / S;
+    const double cost = iters + 1.5 * k + 1.0;
+    const double score = fill * useful / cost;
+    if (score > best * 1.02) {
       best = score;
       pick = L;
     }
@@ -882,6 +927,13 @@ using namespace fm;
 
 extern "C" {
 
+#ifdef FM_HOT_TRACE
+int fm_debug_hot_trace(void* host_out) {
+  FM_CUDA(cudaMemcpyFromSymbol(host_out, g_hot_trace, sizeof(g_hot_trace)));
+  return FM_OK;
+}
+#endif
+
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store) {
   if (!store) return 0;
   const size_t ni = (size_t)store->n_items;
@@ -925,7 +977,7 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE(f64 ? out->mom64 != nullptr : out->mom32 != nullptr, "moment output missing");
     if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
   }
-  PartialBufs part{nullptr, nullptr, nullptr};
+  PartialBufs part{nullptr, nullptr, nullptr, 0};
   cudaStream_t st = as_stream(stream);
   fm_point_store s2 = s;  // with item descriptors
   {
@@ -934,6 +986,7 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
       part.red = sc.take<double>((size_t)s.n_items * kNumRed);
       part.s0 = sc.take<double>((size_t)s.n_items);
       part.l1 = sc.take<double>((size_t)s.n_items);
+      part.cap = s.n_items;
     }
     if (!s.item_desc) {
       s2.item_desc = sc.take<int32_t>((size_t)s.n_items * 4);
@@ -942,7 +995,7 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE((sc.used == 0 || scratch) && sc.ok(), "point-pass scratch too small (%zu < %zu)",
                scratch_bytes, sc.used);
   }
-  if (!homog) {
+  if (!homog && s.slot_align >= kBlkSlots && s.slot_align % kBlkSlots == 0) {
     // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
     const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
     bool handled = false;

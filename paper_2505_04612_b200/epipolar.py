@@ -32,6 +32,10 @@ from .optim import matrix_to_rot6d, skew  # noqa: F401
 from .store import PairGraph, PointPairStore
 
 _HUBER_EPS = 1e-6
+# Moment precision of the IRLS point passes: "fp32" = fp32 Kronecker moments
+# about the linearisation point (shifted quadratic model) with
+# exact fp64 residuals / prune decisions; "fp64" = exact fp64 moments.
+DEFAULT_PRECISION = "fp32"
 
 SYM = [[0, 1, 2], [1, 3, 4], [2, 4, 5]]
 
@@ -309,10 +313,12 @@ def prune_thresholds(cfg):
 class IrlsBuffers:
     """Device buffers of one irls_refine run (per image pair, store order).
 
-    precision "fp64" (default): exact fp64 W moments, unshifted model.
-    precision "fp32": fp32 moments + shifted-model terms (fast mode)."""
+    precision "fp32" (default, DEFAULT_PRECISION): fp32 moments + the
+    shifted-model terms (exact fp64 residuals and prune decisions).
+    precision "fp64": exact fp64 W moments, unshifted model."""
 
-    def __init__(self, P, device, precision="fp64"):
+    def __init__(self, P, device, precision=None):
+        precision = precision or DEFAULT_PRECISION
         Pm = max(P, 1)
         self.precision = precision
         self.ghat0 = torch.zeros((9, Pm), dtype=torch.float64, device=device)
@@ -351,7 +357,8 @@ class IrlsEngine:
     over an already-built store and pair graph.  Used by ``irls_refine`` and
     directly by the benchmark (store built on the device)."""
 
-    def __init__(self, store, graph, params, cfg, use_graph=True, precision="fp64"):
+    def __init__(self, store, graph, params, cfg, use_graph=True, precision=None):
+        precision = precision or DEFAULT_PRECISION
         if not getattr(store, "sanitized", False):
             raise ValueError("IrlsEngine needs a sanitized store (finite coordinates on every "
                              "slot; build it with sanitize=True)")
@@ -442,7 +449,7 @@ class IrlsEngine:
         return l1_history
 
 
-def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True, precision="fp64"):
+def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True, precision=None):
     """Scheduled IRLS refinement of global poses (and optionally focals)
     (ref/epipolar.py:265-319).  Mutates pair ``active`` masks during pruning.
     Returns (poses, focal_scale per camera, report dict)."""
@@ -455,7 +462,8 @@ def irls_refine(poses, pairs, cfg, n_cameras=1, use_graph=True, precision="fp64"
     graph = PairGraph(idx_i[o], idx_j[o], cam_i[o], cam_j[o], len(image_ids), n_cameras,
                       cfg.refine_focal, device=device)
     params = torch.as_tensor(state.pack(), device=device)
-    engine = IrlsEngine(store, graph, params, cfg, use_graph=use_graph, precision=precision)
+    engine = IrlsEngine(store, graph, params, cfg, use_graph=use_graph,
+                        precision=precision or DEFAULT_PRECISION)
     try:
         l1_history = engine.run()
     finally:

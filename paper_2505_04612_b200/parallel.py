@@ -64,7 +64,7 @@ class NoComm:
 class Shard:
     """One store + pair graph (global image / camera indexing)."""
 
-    def __init__(self, store, graph, precision="fp64"):
+    def __init__(self, store, graph, precision=None):
         self.store = store
         self.graph = graph
         self.device = store.device
@@ -192,7 +192,7 @@ class ShardedIrlsEngine:
 
 
 def make_shards(x1, x2, lengths, ij, cams, n_images, n_cameras, refine_focal, bounds, device,
-                precision="fp64", ranks=None):
+                precision=None, ranks=None):
     """Build the shards [bounds[k], bounds[k+1]) of a (sorted) pair list.
 
     x1, x2: host arrays (Z, 2|3); lengths, ij (P, 2) dense image indices,

@@ -4,7 +4,7 @@
   (ref/epipolar.py:19-36) re-laid out as a structure of arrays in HBM: fp32
   ``(x, y)`` columns for each image side, a 1-bit active mask, image pairs
   sorted by ``(i, j)`` (stable, so duplicates keep caller order), each pair
-  starting on a 4-slot boundary.  ``terms`` (72 B/point in the reference) is
+  starting on a 16-slot boundary (SLOT_ALIGN).  ``terms`` (72 B/point in the reference) is
   never stored: the kernels rebuild ``flatten(x2 x1^T)`` in registers.
 * :class:`PairGraph` -- image-pair -> dense-image / camera indices plus the
   incidence lists that make per-image and per-camera gradient sums
@@ -24,6 +24,7 @@ import torch
 from . import _native as N
 
 CHUNK = 8192          # slots per work item (multiple of 128)
+SLOT_ALIGN = 16       # pair start alignment (slots): whole 16-slot blocks for the hot kernel
 CAM_CHUNK = 4096      # incidences per camera-reduction chunk
 
 
@@ -43,14 +44,14 @@ def pair_order(i, j):
 
 
 def slot_layout(lengths, chunk=CHUNK):
-    """4-aligned slot offsets and work items for per-pair point counts.
+    """SLOT_ALIGN-aligned slot offsets and work items for per-pair point counts.
 
     Returns (pair_off [P+1] int64, n_slots, pair_item_off [P+1] int32,
     item_pair [n_items] int32).
     """
     lengths = np.asarray(lengths, dtype=np.int64)
     P = len(lengths)
-    padded = (lengths + 3) // 4 * 4
+    padded = (lengths + SLOT_ALIGN - 1) // SLOT_ALIGN * SLOT_ALIGN
     pair_off = np.zeros(P + 1, dtype=np.int64)
     np.cumsum(padded, out=pair_off[1:])
     n_slots = int((pair_off[-1] + 127) // 128 * 128)
@@ -159,7 +160,7 @@ class PointPairStore:
                 x1=self.x1.data_ptr(), x2=self.x2.data_ptr(),
                 x1z=self.x1z.data_ptr() if self.x1z is not None else None,
                 x2z=self.x2z.data_ptr() if self.x2z is not None else None,
-                active=self.active.data_ptr(), item_desc=None)
+                active=self.active.data_ptr(), item_desc=None, slot_align=SLOT_ALIGN)
             self.item_desc_d = torch.empty((max(self.n_items, 1), 4), dtype=torch.int32,
                                            device=self.device)
             self._struct.item_desc = self.item_desc_d.data_ptr()

@@ -10,7 +10,9 @@ modes = {"irls": N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED,
 mode, prec = sys.argv[1], sys.argv[2]
 cfg = sys.argv[3] if len(sys.argv) > 3 else "c2"
 dev = torch.device("cuda")
-sc = scenes.generate(scenes.CONFIGS[cfg], dev)
+spec = scenes.CONFIGS[cfg] if cfg in scenes.CONFIGS else scenes.SceneSpec(
+    **dict(zip(("n_images", "band", "points_per_pair"), (int(x) for x in cfg.split(",")))))
+sc = scenes.generate(spec, dev)
 store = scenes.device_store(sc, dev)
 graph, ids = scenes.device_graph(sc, dev)
 params = torch.as_tensor(scenes.initial_params(sc, ids), device=dev)

@@ -63,6 +63,38 @@ __global__ void ffma_k(float* out, float a, float b) {
   if (s == 1.2345f) out[0] = s;
 }
 
+// 8 FFMA2 chains + 8 scalar FFMA chains: does scalar FFMA use a pipe FFMA2 leaves free?
+__global__ void mix_k(float* out, float2 a, float2 b) {
+  float2 x[8];
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { x[k] = make_float2(threadIdx.x + k, k); y[k] = threadIdx.x - k; }
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { x[k] = __ffma2_rn(x[k], a, b); y[k] = fmaf(y[k], a.x, b.x); }
+  }
+  float s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k].x + x[k].y + y[k];
+  if (s == 1.2345f) out[0] = s;
+}
+
+// fp32 -> fp64 conversions with no other work (XU rate)
+__global__ void cvt_k(double* out, float a) {
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = 0;
+  float f = a + threadIdx.x;
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { x[k] = (double)f; f = __int_as_float(__float_as_int(f) ^ (k + 1)); }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += x[k];
+  if (s == 1.2345) out[0] = s;
+}
+
 int main() {
   int sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -91,6 +123,8 @@ int main() {
     run("F2F+DADD", [&](int b, int t) { f2f_k<<<b, t>>>((double*)buf, 1.0000001f); }, 16, sms * 4, threads);
     run("FFMA2(x2)", [&](int b, int t) { ffma2_k<<<b, t>>>((float2*)buf, make_float2(1.0000001f, 1.0f), make_float2(1e-9f, 0.f)); }, 32, sms * 4, threads);
     run("FFMA", [&](int b, int t) { ffma_k<<<b, t>>>((float*)buf, 1.0000001f, 1e-9f); }, 16, sms * 4, threads);
+    run("FFMA2+FFMA", [&](int b, int t) { mix_k<<<b, t>>>((float*)buf, make_float2(1.0000001f, 1.0f), make_float2(1e-9f, 0.f)); }, 24, sms * 4, threads);
+    run("F2F only", [&](int b, int t) { cvt_k<<<b, t>>>((double*)buf, 1.0000001f); }, 16, sms * 4, threads);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -1,5 +1,5 @@
 """Opcode histogram of the main loop (largest backward-branch body) of a kernel.
-    python tools/sass_loop.py <cubin|so> <kernel-name-substring>"""
+    python tools/sass_loop.py <cubin|so|o> <kernel-name-substring>"""
 import collections, re, subprocess, sys
 sass = subprocess.run(["cuobjdump", "-sass", sys.argv[1]], capture_output=True, text=True).stdout.split("\n")
 st = [i for i, l in enumerate(sass) if "Function :" in l and sys.argv[2] in l][0]
@@ -24,3 +24,5 @@ for t in body:
     c[op] += 1
 print(f"loop {best[0]:#x}-{best[1]:#x}: {len(body)} instructions")
 print(", ".join(f"{k} {v}" for k, v in c.most_common()))
+if len(sys.argv) > 3:
+    print("\n".join(body))
