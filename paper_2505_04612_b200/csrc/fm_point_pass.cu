@@ -331,11 +331,14 @@ struct HotAcc {
   }
 };
 
-// Canonical moment index (row i = B, column j = A) of hot fp32 slot v (0..35).
+// Canonical moment index (row i = B, column j = A) of hot fp32 slot v (0..35):
+// slot v = 2 (3 j + k) + h holds B-pair k's half h against A_j, and the
+// B-pairs are (B0, B3), (B2, B4), (B1, B5).
 __device__ __forceinline__ int hot_mom_index(int v) {
-  const int j = (v >> 1) / 3, k = (v >> 1) % 3, h = v & 1;
-  constexpr int kRow[3][2] = {{0, 3}, {2, 4}, {1, 5}};
-  return kRow[k][h] * 6 + j;
+  const int m = v >> 1, h = v & 1;
+  const int j = m / 3, k = m - 3 * j;
+  const int row = k == 0 ? 3 * h : (k == 1 ? 2 + 2 * h : 1 + 4 * h);
+  return row * 6 + j;
 }
 
 template <int L>
@@ -412,14 +415,17 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
 
   ItemDesc d{0, 0, 0, true};
   if (has_item) d = decode_item(__ldg(reinterpret_cast<const int4*>(s.item_desc) + item));
-  const bool skip = has_item && kSkip && prev_active[d.n] == 0;
+  // one item per pair (the common case): item == pair, so the pair loads need
+  // not wait for the descriptor (one dependent global-load latency less)
+  const int64_t pn = (NI == P) ? item : d.n;
+  const bool skip = has_item && kSkip && __ldg(prev_active + pn) == 0;
   double G[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    G[k] = (has_item && !skip) ? ghat[k * P + d.n] : 0.0;
+    G[k] = has_item ? __ldg(ghat + k * P + pn) : 0.0;
     if (!HotAcc<kPrune, kL1, kMom, MOM64>::kF2F && k % 3 != 2) G[k] *= kUnscale;  // coordinate columns (exact)
   }
-  const int nblk = (has_item && !skip) ? (d.len + kBlkSlots - 1) / kBlkSlots : 0;
+  const int nblk = (has_item && !skip) ? (d.len + kBlkSlots - 1) / kBlkSlots : 0;  // skipped: no work
   const int nit = (nblk + S - 1) / S;
   const int warp_it = __reduce_max_sync(0xffffffffu, nit);
 
@@ -545,16 +551,25 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
     group_transpose_reduce<L>(v, lane);
     const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
     if (has_item) {
+      // destination of each of the lane's N/L sums: a float column (moment,
+      // vgrad or partial), the int count or the fp64 s0
 #pragma unroll
       for (int i = 0; i < N / L; ++i) {
         const int vi = g * (N / L) + i;
-        if (vi == 46) {
-          if (single) out.s0[d.n] = (double)v[i];
-          else part.s0[item] = (double)v[i];
-        } else if (vi < 46) {
-          const int k = vi < 36 ? hot_mom_index(vi) : vi;
-          store_red(out, part, single, P, NI, d.n, item, k, v[i], kLin);
+        const int k = vi < 36 ? hot_mom_index(vi) : vi;
+        float* col = nullptr;
+        int64_t at = d.n;
+        if (!single) {
+          col = k < 46 ? static_cast<float*>(part.red) + (int64_t)k * NI : nullptr;
+          at = item;
+        } else if (k < 36) {
+          col = out.mom32 + (int64_t)k * P;
+        } else if (k < 45 && kLin) {
+          col = out.vgrad + (int64_t)(k - 36) * P;
         }
+        if (col) col[at] = v[i];
+        if (single && k == 45 && out.n_active) out.n_active[d.n] = (int32_t)v[i];
+        if (k == 46) (single ? out.s0 : part.s0)[at] = (double)v[i];
       }
       if (kL1 && g == 0) {
         if (single) {

@@ -323,3 +323,18 @@ def test_integration_stub(golden_small):
     p = pairs[0]
     W = ns["precompute_weights_gpu"](p.x1, p.x2)
     np.testing.assert_allclose(W, E.precompute_weights(p.x1, p.x2), rtol=1e-12, atol=1e-14)
+
+
+def test_l1_loss_with_nonfinite_active_point_is_nan(golden_small):
+    """An active NaN coordinate makes the reference's l1 loss NaN
+    (ref/epipolar.py:156-160); such stores leave the hot kernel (whose
+    integer-pipe fp32->fp64 conversion is exact for finite values only)."""
+    g = golden_small
+    pairs = pairs_from(g, "e0_", E.EpipolarPair)
+    st = _state(g, "e0_")
+    loss, Z = E.epipolar_loss(st, pairs, mode="l1")
+    np.testing.assert_allclose(loss, g["e0_loss_l1"][0], rtol=1e-12)
+    k = int(np.nonzero(pairs[0].active)[0][0])
+    pairs[0].x1[k, 0] = np.nan
+    loss, Z = E.epipolar_loss(st, pairs, mode="l1")
+    assert np.isnan(loss)
