@@ -22,10 +22,10 @@ namespace fm {
 
 namespace {
 
-constexpr int kGroup = 4;
 constexpr int kGraphSteps = 200;  // steps per captured CUDA graph (even: keeps ping-pong parity)
 
 struct TrScratch {
+  double4* rec;   // [2m] incidence records {direction, (other node) | side << 31}
   double* buf;    // [n][B][3] ping-pong partner of the caller's centres
   double* m;      // [n][B][3]
   double* v;      // [n][B][3]
@@ -35,15 +35,16 @@ struct TrScratch {
 };
 
 size_t tr_need(int32_t n, int64_t m, int32_t B) {
-  (void)m;
   const size_t nb3 = (size_t)n * B * 3;
-  return 3 * scratch_round(nb3 * sizeof(double)) + 2 * scratch_round((size_t)n * B * sizeof(double)) +
+  return scratch_round((size_t)2 * m * sizeof(double4)) +
+         3 * scratch_round(nb3 * sizeof(double)) + 2 * scratch_round((size_t)n * B * sizeof(double)) +
          scratch_round(2 * kGraphSteps * sizeof(double)) + 256;
 }
 
-bool tr_carve(int32_t n, int32_t B, void* p, size_t bytes, TrScratch& s) {
+bool tr_carve(int32_t n, int64_t m, int32_t B, void* p, size_t bytes, TrScratch& s) {
   Scratch sc(p, bytes);
   const size_t nb3 = (size_t)n * B * 3;
+  s.rec = sc.take<double4>((size_t)2 * m);
   s.buf = sc.take<double>(nb3);
   s.m = sc.take<double>(nb3);
   s.v = sc.take<double>(nb3);
@@ -62,109 +63,149 @@ __device__ __forceinline__ T warp_sum(T x) {
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : (x == 0 ? 0.0 : x)); }
 
+// 1/sqrt(q) for normal q > 0: hardware approximation + two Newton steps
+// (~1 ulp; no slow-path call)
+__device__ __forceinline__ double rsqrt_nr(double q) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  const double h = 0.5 * q;
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  return y;
+}
+
+// np.sign for finite x on the integer pipe: +-1 with x's sign bit, 0 for +-0
+// (a NaN residual yields +-1 here; the NaN loss it comes with raises anyway)
+__device__ __forceinline__ double sign_or_zero(double x) {
+  const int hi = __double2hiint(x);
+  const int one = 0x3FF00000 | (hi & (int)0x80000000);
+  return __hiloint2double(x != 0.0 ? one : 0, 0);
+}
+
 enum TrMode { kTrAdam = 0, kTrGrad = 1 };
 
-// One warp per (node, run group).  kTrAdam: Adam step cur -> nxt.
-// kTrGrad: write the gradient (API translation_loss_and_grad).
-template <int MODE>
-__global__ void tr_step_kernel(const fm_dir_graph g, const double* __restrict__ cur,
+// Incidence records in node-incidence order: the edge's direction and the
+// other endpoint (bit 31: v is the edge's j), so a step gathers one 32-byte
+// record per incidence instead of chasing incidence -> edge -> endpoints.
+__global__ void tr_incidence_kernel(const fm_dir_graph g, double4* __restrict__ rec) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 2 * g.n_edges) return;
+  const int inc = g.node_inc[e];
+  const int64_t edge = inc >> 1;
+  const int side = inc & 1;  // 0: v is i, 1: v is j
+  const int o = side ? g.edge_i[edge] : g.edge_j[edge];
+  rec[e] = make_double4(g.dirs[3 * edge], g.dirs[3 * edge + 1], g.dirs[3 * edge + 2],
+                        __longlong_as_double((long long)(uint32_t)o | ((long long)side << 31)));
+}
+
+// One warp per (node, group of R runs); lane = R * slot + run: the warp
+// walks the node's incidences 32/R at a time, every lane evaluates one
+// (incidence, run) term, so the R lanes of an incidence read the record once
+// (broadcast) and the R runs' centres of the other endpoint as one contiguous
+// 24R-byte segment.  Two incidences per lane are in flight (the step is a
+// chain of dependent L2 gathers).  Fixed-order butterflies over the slots.
+// kTrAdam: Adam step cur -> nxt.  kTrGrad: write the gradient (API).
+//
+// Per term, with e = c_o - c_v, s = +1 if v is the edge's i else -1 and the
+// reference's u = s e / |e|, r = u - d, g_u = sign(r) / m
+// (ref/translation.py:112-125): writing w = e / |e| and d' = s d,
+// r = s (w - d'), so |r| = |w - d'|, sign(r) = s sign(w - d') and the node's
+// gradient term -s g_delta = -(sign(w - d') - w (w . sign(w - d'))) / (m |e|)
+// carries no sign of its own -- one formula for both endpoints, 1/m once.
+template <int MODE, int R>
+__global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
+                               const double* __restrict__ cur,
                                double* __restrict__ nxt, double* __restrict__ am,
                                double* __restrict__ av, double* __restrict__ lpart, int B,
                                double lr, double b1, double b2, double eps,
                                const double* __restrict__ bc, int step, int32_t* flag) {
+  constexpr int kSlots = 32 / R;
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int groups = (B + kGroup - 1) / kGroup;
+  const int groups = (B + R - 1) / R;
   if (w >= (int64_t)g.n_nodes * groups) return;
   if (MODE == kTrAdam && *flag) return;
   const int v = (int)(w / groups);
-  const int b0 = (int)(w % groups) * kGroup;
-  const int nb = min(kGroup, B - b0);
+  const int rb = lane % R, slot = lane / R;
+  const int b = (int)(w % groups) * R + rb;  // this lane's run
+  const bool run_ok = b < B;
+  const int bl = run_ok ? b : B - 1;          // idle lanes mirror a valid run
   const double inv_m = 1.0 / (double)g.n_edges;
 
-  double cv[kGroup][3];
+  double cv[3];
 #pragma unroll
-  for (int b = 0; b < kGroup; ++b)
+  for (int k = 0; k < 3; ++k) cv[k] = cur[((int64_t)v * B + bl) * 3 + k];
+  double acc[3] = {0.0, 0.0, 0.0}, lacc = 0.0;
+  auto term = [&](const double4 r, const double co[3]) {
+    const bool vj = (__double_as_longlong(r.w) >> 31) & 1;  // v is the edge's j
+    const double dp[3] = {vj ? -r.x : r.x, vj ? -r.y : r.y, vj ? -r.z : r.z};
+    double e[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) cv[b][k] = b < nb ? cur[((int64_t)v * B + b0 + b) * 3 + k] : 0.0;
-
-  double acc[kGroup][3], lacc[kGroup];
-#pragma unroll
-  for (int b = 0; b < kGroup; ++b) {
-    lacc[b] = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) acc[b][k] = 0;
-  }
-  const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const int inc = g.node_inc[e];
-    const int64_t edge = inc >> 1;
-    const int side = inc & 1;  // 0: v is i, 1: v is j
-    const int o = side ? g.edge_i[edge] : g.edge_j[edge];
-    const double d[3] = {g.dirs[3 * edge], g.dirs[3 * edge + 1], g.dirs[3 * edge + 2]};
-    const double* co = cur + ((int64_t)o * B + b0) * 3;
-#pragma unroll
-    for (int b = 0; b < kGroup; ++b) {
-      if (b >= nb) break;
-      double delta[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) delta[k] = side ? cv[b][k] - co[3 * b + k] : co[3 * b + k] - cv[b][k];
-      const double len = fmax(sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]), 1e-8);
-      // one division per edge and run; the reference divides component-wise
-      // (ref/translation.py:116, :121) -- same value to within an ulp
-      const double inv = 1.0 / len;
-      double u[3], r[3], gu[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        u[k] = delta[k] * inv;
-        r[k] = u[k] - d[k];
-        gu[k] = sgn(r[k]) * inv_m;
-      }
-      const double ug = u[0] * gu[0] + u[1] * gu[1] + u[2] * gu[2];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double gd = (gu[k] - u[k] * ug) * inv;
-        acc[b][k] += side ? gd : -gd;
-      }
-      if (side == 0) lacc[b] += fabs(r[0]) + fabs(r[1]) + fabs(r[2]);
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < kGroup; ++b) {
-    lacc[b] = warp_sum(lacc[b]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) acc[b][k] = warp_sum(acc[b][k]);
-  }
-  // lane b finalises run b0+b
-#pragma unroll
-  for (int b = 0; b < kGroup; ++b) {
-    if (lane != b || b >= nb) continue;
-    const int64_t base = ((int64_t)v * B + b0 + b) * 3;
-    lpart[(int64_t)v * B + b0 + b] = lacc[b];
-    if (MODE == kTrGrad) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) nxt[base + k] = acc[b][k];
-      continue;
-    }
-    if (!isfinite(lacc[b])) {
-      atomicMax(flag, FM_ERR_NONFINITE_TRANSLATION);
-      continue;
-    }
-    if (!(isfinite(acc[b][0]) && isfinite(acc[b][1]) && isfinite(acc[b][2]))) {
-      atomicMax(flag, FM_ERR_NONFINITE_GRAD);
-      continue;
-    }
-    const double c1 = bc[step], c2 = bc[kGraphSteps + step];
+    for (int k = 0; k < 3; ++k) e[k] = co[k] - cv[k];
+    const double q = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+    // 1 / max(|e|, 1e-8) as one fp64 reciprocal square root (the reference
+    // divides each component by the clamped norm, ref/translation.py:115-121;
+    // same value to within an ulp)
+    const double inv = q > 1e-16 ? rsqrt_nr(q) : 1e8;
+    double wv[3], sg[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double gk = acc[b][k];
-      const double mk = __dadd_rn(__dmul_rn(b1, am[base + k]), __dmul_rn(1.0 - b1, gk));
-      const double vk = __dadd_rn(__dmul_rn(b2, av[base + k]), __dmul_rn(1.0 - b2, __dmul_rn(gk, gk)));
-      am[base + k] = mk;
-      av[base + k] = vk;
-      nxt[base + k] = __dsub_rn(cv[b][k], __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
-                                                    __dadd_rn(sqrt(__ddiv_rn(vk, c2)), eps)));
+      wv[k] = e[k] * inv;
+      sg[k] = sign_or_zero(wv[k] - dp[k]);
     }
+    const double wg = wv[0] * sg[0] + wv[1] * sg[1] + wv[2] * sg[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[k] -= (sg[k] - wv[k] * wg) * inv;
+    if (!vj) lacc += fabs(wv[0] - dp[0]) + fabs(wv[1] - dp[1]) + fabs(wv[2] - dp[2]);
+  };
+  const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
+  for (int e = e0 + slot; e < e1; e += 2 * kSlots) {
+    const bool two = e + kSlots < e1;
+    const double4 r1 = rec[e];
+    const double4 r2 = rec[two ? e + kSlots : e];
+    const int o1 = (int)(__double_as_longlong(r1.w) & 0x7fffffff);
+    const int o2 = (int)(__double_as_longlong(r2.w) & 0x7fffffff);
+    const double* p1 = cur + ((int64_t)o1 * B + bl) * 3;
+    const double* p2 = cur + ((int64_t)o2 * B + bl) * 3;
+    const double c1[3] = {__ldg(p1), __ldg(p1 + 1), __ldg(p1 + 2)};
+    const double c2[3] = {__ldg(p2), __ldg(p2 + 1), __ldg(p2 + 2)};
+    term(r1, c1);
+    if (two) term(r2, c2);
+  }
+#pragma unroll
+  for (int off = R; off < 32; off <<= 1) {
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, off);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+  }
+  if (slot != 0 || !run_ok) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) acc[k] *= inv_m;
+  const int64_t base = ((int64_t)v * B + b) * 3;
+  lpart[(int64_t)v * B + b] = lacc;
+  if (MODE == kTrGrad) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nxt[base + k] = acc[k];
+    return;
+  }
+  if (!isfinite(lacc)) {
+    atomicMax(flag, FM_ERR_NONFINITE_TRANSLATION);
+    return;
+  }
+  if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
+    atomicMax(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  const double c1 = bc[step], c2 = bc[kGraphSteps + step];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double gk = acc[k];
+    const double mk = __dadd_rn(__dmul_rn(b1, am[base + k]), __dmul_rn(1.0 - b1, gk));
+    const double vk = __dadd_rn(__dmul_rn(b2, av[base + k]), __dmul_rn(1.0 - b2, __dmul_rn(gk, gk)));
+    am[base + k] = mk;
+    av[base + k] = vk;
+    nxt[base + k] = __dsub_rn(cv[k], __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
+                                               __dadd_rn(sqrt(__ddiv_rn(vk, c2)), eps)));
   }
 }
 
@@ -273,16 +314,33 @@ int check_dir_graph(const fm_dir_graph* g, int32_t B) {
 
 unsigned warp_blocks(int64_t warps) { return (unsigned)ceil_div(warps * 32, 256); }
 
+// runs per warp: 4 (B >= 4), else B rounded up to a power of two
+int run_group(int B) { return B >= 4 ? 4 : (B >= 2 ? 2 : 1); }
+
+int build_incidence(const fm_dir_graph& g, const TrScratch& s, cudaStream_t st) {
+  if (g.n_edges == 0) return FM_OK;
+  tr_incidence_kernel<<<(unsigned)ceil_div(2 * g.n_edges, 256), 256, 0, st>>>(g, s.rec);
+  FM_LAUNCHED(tr_incidence_kernel);
+  return FM_OK;
+}
+
 int enqueue_tr_steps(const fm_dir_graph& g, double* c0, double* c1, const TrScratch& s, int B,
                      int steps, double lr, double b1, double b2, double eps, int32_t* flag,
                      cudaStream_t st) {
-  const int groups = (B + kGroup - 1) / kGroup;
-  const unsigned blocks = warp_blocks((int64_t)g.n_nodes * groups);
+  const int R = run_group(B);
+  const unsigned blocks = warp_blocks((int64_t)g.n_nodes * ((B + R - 1) / R));
   for (int k = 0; k < steps; ++k) {
     const double* cur = (k & 1) ? c1 : c0;
     double* nxt = (k & 1) ? c0 : c1;
-    tr_step_kernel<kTrAdam><<<blocks, 256, 0, st>>>(g, cur, nxt, s.m, s.v, s.lpart, B, lr, b1, b2,
-                                                    eps, s.bc, k, flag);
+    if (R == 1)
+      tr_step_kernel<kTrAdam, 1><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
+                                                         b1, b2, eps, s.bc, k, flag);
+    else if (R == 2)
+      tr_step_kernel<kTrAdam, 2><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
+                                                         b1, b2, eps, s.bc, k, flag);
+    else
+      tr_step_kernel<kTrAdam, 4><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
+                                                         b1, b2, eps, s.bc, k, flag);
     FM_LAUNCHED(tr_step_kernel);
   }
   return FM_OK;
@@ -311,13 +369,22 @@ int fm_tr_loss_grad(const fm_dir_graph* g, const double* centers, int32_t B, dou
                     double* grad_out, void* scratch, size_t scratch_bytes, void* stream) {
   if (int rc = check_dir_graph(g, B)) return rc;
   TrScratch s;
-  FM_REQUIRE(tr_carve(g->n_nodes, B, scratch, scratch_bytes, s), "translation scratch too small");
+  FM_REQUIRE(tr_carve(g->n_nodes, g->n_edges, B, scratch, scratch_bytes, s), "translation scratch too small");
   FM_REQUIRE(g->n_edges > 0, "graph has no edges");
   cudaStream_t st = as_stream(stream);
-  const int groups = (B + kGroup - 1) / kGroup;
   if (g->n_nodes == 0) return FM_OK;
-  tr_step_kernel<kTrGrad><<<warp_blocks((int64_t)g->n_nodes * groups), 256, 0, st>>>(
-      *g, centers, grad_out, nullptr, nullptr, s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
+  if (int rc = build_incidence(*g, s, st)) return rc;
+  const int R = run_group(B);
+  const unsigned blocks = warp_blocks((int64_t)g->n_nodes * ((B + R - 1) / R));
+  if (R == 1)
+    tr_step_kernel<kTrGrad, 1><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
+                                                       s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
+  else if (R == 2)
+    tr_step_kernel<kTrGrad, 2><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
+                                                       s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
+  else
+    tr_step_kernel<kTrGrad, 4><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
+                                                       s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
   FM_LAUNCHED(tr_step_kernel);
   tr_loss_kernel<<<B, 256, 0, st>>>(s.lpart, g->n_nodes, B, g->n_edges, loss_out);
   FM_LAUNCHED(tr_loss_kernel);
@@ -332,13 +399,14 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
   FM_REQUIRE(steps >= 0, "negative step count");
   FM_REQUIRE(g->n_edges > 0, "graph has no edges");
   TrScratch s;
-  FM_REQUIRE(tr_carve(g->n_nodes, B, scratch, scratch_bytes, s), "translation scratch too small");
+  FM_REQUIRE(tr_carve(g->n_nodes, g->n_edges, B, scratch, scratch_bytes, s), "translation scratch too small");
   cudaStream_t st = as_stream(stream);
   const int n = g->n_nodes;
   const size_t nb3 = (size_t)n * B * 3;
   if (n == 0 || steps == 0) return FM_OK;
   FM_CUDA(cudaMemsetAsync(s.m, 0, nb3 * sizeof(double), st));
   FM_CUDA(cudaMemsetAsync(s.v, 0, nb3 * sizeof(double), st));
+  if (int rc = build_incidence(*g, s, st)) return rc;
   std::vector<double> bc(2 * kGraphSteps, 1.0);
   int done = 0;
   // steps in graph-sized chunks; every chunk starts from `centers` (even length)
@@ -430,7 +498,7 @@ int fm_tr_merge(const fm_dir_graph* g, double* centers, int32_t B, double* merge
                 void* scratch, size_t scratch_bytes, void* stream) {
   if (int rc = check_dir_graph(g, B)) return rc;
   TrScratch s;
-  FM_REQUIRE(tr_carve(g->n_nodes, B, scratch, scratch_bytes, s), "translation scratch too small");
+  FM_REQUIRE(tr_carve(g->n_nodes, g->n_edges, B, scratch, scratch_bytes, s), "translation scratch too small");
   cudaStream_t st = as_stream(stream);
   const int n = g->n_nodes;
   if (n == 0) return FM_OK;
