@@ -159,18 +159,21 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
     if (!vj) lacc += fabs(wv[0] - dp[0]) + fabs(wv[1] - dp[1]) + fabs(wv[2] - dp[2]);
   };
   const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
-  for (int e = e0 + slot; e < e1; e += 2 * kSlots) {
-    const bool two = e + kSlots < e1;
-    const double4 r1 = rec[e];
-    const double4 r2 = rec[two ? e + kSlots : e];
-    const int o1 = (int)(__double_as_longlong(r1.w) & 0x7fffffff);
-    const int o2 = (int)(__double_as_longlong(r2.w) & 0x7fffffff);
-    const double* p1 = cur + ((int64_t)o1 * B + bl) * 3;
-    const double* p2 = cur + ((int64_t)o2 * B + bl) * 3;
-    const double c1[3] = {__ldg(p1), __ldg(p1 + 1), __ldg(p1 + 2)};
-    const double c2[3] = {__ldg(p2), __ldg(p2 + 1), __ldg(p2 + 2)};
-    term(r1, c1);
-    if (two) term(r2, c2);
+  constexpr int kIF = 2;  // incidences in flight per lane (4: more registers, half the warps)
+  for (int e = e0 + slot; e < e1; e += kIF * kSlots) {
+    double4 r[kIF];
+#pragma unroll
+    for (int f = 0; f < kIF; ++f) r[f] = rec[e + f * kSlots < e1 ? e + f * kSlots : e];
+    double c[kIF][3];
+#pragma unroll
+    for (int f = 0; f < kIF; ++f) {
+      const double* p = cur + ((int64_t)(__double_as_longlong(r[f].w) & 0x7fffffff) * B + bl) * 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) c[f][k] = __ldg(p + k);
+    }
+#pragma unroll
+    for (int f = 0; f < kIF; ++f)
+      if (e + f * kSlots < e1) term(r[f], c[f]);
   }
 #pragma unroll
   for (int off = R; off < 32; off <<= 1) {
