@@ -349,6 +349,11 @@ def run_ours(args, spec, world, rank, local):
 
     # ------------------------------------------- SfM optimize time (rank 0)
     extra = {}
+    if not args.skip_optimize and world > 1:
+        # config 3 with the 16 random starts split over the ranks (collective)
+        tr = translation_bench(device, stream, sharded=True)
+        if rank == 0:
+            extra["sfm_optimize"] = {"translation_sharded_over_ranks": world, **tr}
     if rank == 0 and not args.skip_optimize:
         params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
         store.reset_active()
@@ -359,10 +364,11 @@ def run_ours(args, spec, world, rank, local):
             l1h = eng2.run()
             torch.cuda.synchronize()
             t_irls = time.perf_counter() - t0
-        extra["sfm_optimize"] = {"irls_refine_s": t_irls, "l1_history": l1h,
-                                 "dropped_pairs": eng2.dropped, "active_pairs": eng2.kept,
-                                 "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"}
-        extra["sfm_optimize"].update(translation_bench(device, stream))
+        extra.setdefault("sfm_optimize", {}).update(
+            {"irls_refine_s": t_irls, "l1_history": l1h, "dropped_pairs": eng2.dropped,
+             "active_pairs": eng2.kept, "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"})
+        if world == 1:
+            extra["sfm_optimize"].update(translation_bench(device, stream))
 
     # ---------------------------------------------------- CPU baseline
     cpu = None
@@ -410,10 +416,12 @@ def run_ours(args, spec, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def translation_bench(device, stream):
+def translation_bench(device, stream, sharded=False):
     """BASELINE configs[2]: 16 batched inits, 2k nodes / 200k edges, 6000
-    steps each + merge + final 6000-step run (ref/translation.py:169-186)."""
+    steps each + merge + final 6000-step run (ref/translation.py:169-186).
+    sharded: the starts split over the torch.distributed ranks (collective)."""
     import torch
+    from paper_2505_04612_b200 import parallel as P_
     from paper_2505_04612_b200 import translation as T
     rng = np.random.default_rng(0)
     n, m = 2000, 200_000
@@ -442,10 +450,20 @@ def translation_bench(device, stream):
     with torch.cuda.stream(stream):
         T.align_centers(g, C, seed=0, steps=200)  # warm-up (graph upload, capture)
         torch.cuda.synchronize()
+        if sharded:
+            import torch.distributed as dist
+            dist.barrier()
         t0 = time.perf_counter()
-        centers, loss = T.multi_init_align(g, C, seed=0)
+        if sharded:
+            centers, loss = P_.multi_init_align_sharded(g, C, seed=0)
+        else:
+            centers, loss = T.multi_init_align(g, C, seed=0)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if sharded:
+            t = torch.tensor([dt], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
     evals = (16 + 1) * 6000 * m
     return {"multi_init_align_s": dt, "translation_loss": loss,
             "translation_config": "C3: 2000 nodes, 200000 edges, 16 inits x 6000 steps + final",

@@ -317,8 +317,11 @@ int check_dir_graph(const fm_dir_graph* g, int32_t B) {
 
 unsigned warp_blocks(int64_t warps) { return (unsigned)ceil_div(warps * 32, 256); }
 
-// runs per warp: 4 (B >= 4), else B rounded up to a power of two
-int run_group(int B) { return B >= 4 ? 4 : (B >= 2 ? 2 : 1); }
+// runs per warp: 4 for every batch (idle lanes when B % 4 != 0), 1 for a
+// single run.  A run's summation order depends only on R, so a run's
+// trajectory is the same in any batch of >= 2 runs -- the multi-init runs
+// sharded over ranks reproduce the single-GPU batch bit for bit.
+int run_group(int B) { return B >= 2 ? 4 : 1; }
 
 int build_incidence(const fm_dir_graph& g, const TrScratch& s, cudaStream_t st) {
   if (g.n_edges == 0) return FM_OK;
@@ -337,9 +340,6 @@ int enqueue_tr_steps(const fm_dir_graph& g, double* c0, double* c1, const TrScra
     double* nxt = (k & 1) ? c0 : c1;
     if (R == 1)
       tr_step_kernel<kTrAdam, 1><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
-                                                         b1, b2, eps, s.bc, k, flag);
-    else if (R == 2)
-      tr_step_kernel<kTrAdam, 2><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
                                                          b1, b2, eps, s.bc, k, flag);
     else
       tr_step_kernel<kTrAdam, 4><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
@@ -381,9 +381,6 @@ int fm_tr_loss_grad(const fm_dir_graph* g, const double* centers, int32_t B, dou
   const unsigned blocks = warp_blocks((int64_t)g->n_nodes * ((B + R - 1) / R));
   if (R == 1)
     tr_step_kernel<kTrGrad, 1><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
-                                                       s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
-  else if (R == 2)
-    tr_step_kernel<kTrGrad, 2><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
                                                        s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
   else
     tr_step_kernel<kTrGrad, 4><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,

@@ -55,10 +55,31 @@ class TorchComm:
             self.dist.all_reduce(t, group=self.group)
         return t
 
+    @property
+    def world(self):
+        return self.dist.get_world_size(self.group) if self.dist.is_initialized() else 1
+
+    @property
+    def rank(self):
+        return self.dist.get_rank(self.group) if self.dist.is_initialized() else 0
+
+    def allgather(self, t):
+        """Equal-shaped tensors of every rank, in rank order."""
+        if self.world == 1:
+            return [t]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t.contiguous(), group=self.group)
+        return out
+
 
 class NoComm:
+    world, rank = 1, 0
+
     def allreduce_(self, t):
         return t
+
+    def allgather(self, t):
+        return [t]
 
 
 class Shard:
@@ -213,3 +234,44 @@ def make_shards(x1, x2, lengths, ij, cams, n_images, n_cameras, refine_focal, bo
 
 
 __all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NoComm", "make_shards"]
+
+
+def init_blocks(n_inits, world):
+    """Contiguous blocks of the random starts per rank: rank r runs starts
+    [b[r], b[r+1]) (the last ranks may get one fewer)."""
+    return np.array([n_inits * r // world for r in range(world + 1)], dtype=np.int64)
+
+
+def multi_init_align_sharded(graph, cfg, seed=0, comm=None):
+    """multi_init_align (ref/translation.py:169-186) with the B random starts
+    split into contiguous blocks over the ranks (independent runs,
+    no exchange per step).  Each rank descends its block as one batch; one
+    all-gather of the final centres (padded to the largest block) assembles
+    the B runs in start order on every rank; the merge and the final descent
+    then run replicated, so every rank returns the same result.  A run's
+    trajectory does not depend on its batch (fm_tr_align), so the result is
+    bitwise the single-GPU multi_init_align whenever every block holds >= 2
+    starts."""
+    from . import translation as T
+    comm = comm or TorchComm()
+    B = cfg.translation_inits
+    if B == 1 or comm.world == 1:
+        return T.multi_init_align(graph, cfg, seed=seed)
+    dg = T.device_graph(graph)
+    b = init_blocks(B, comm.world)
+    lo, hi = int(b[comm.rank]), int(b[comm.rank + 1])
+    local = T.init_runs(graph, cfg, seed, range(lo, hi), dg) if hi > lo else \
+        torch.zeros((graph.n, 0, 3), dtype=torch.float64, device=dg.device)
+    runs = gather_blocks(local, b, comm)
+    return T.merge_and_finish(graph, cfg, runs, dg)
+
+
+def gather_blocks(local, b, comm):
+    """All-gather per-rank blocks (n, b[r+1]-b[r], k) along dim 1 in rank
+    order; blocks are zero-padded to the widest for the collective."""
+    width = int(np.max(np.diff(b)))
+    pad = torch.zeros((local.shape[0], width) + tuple(local.shape[2:]), dtype=local.dtype,
+                      device=local.device)
+    pad[:, :local.shape[1]] = local
+    parts = comm.allgather(pad)
+    return torch.cat([p[:, :int(b[r + 1] - b[r])] for r, p in enumerate(parts)], dim=1)

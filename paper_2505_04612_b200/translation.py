@@ -140,21 +140,25 @@ def per_node_residuals(centers, graph):
     return out.cpu().numpy()
 
 
-def multi_init_inits(n, inits, seed):
-    """The reference's random starts of runs seed..seed+inits-1, node-major
-    (n, inits, 3) (ref/translation.py:140-142, :179-180)."""
-    return np.stack([np.random.default_rng(seed + k).standard_normal((n, 3))
-                     for k in range(inits)], axis=1)
+def init_runs(graph, cfg, seed, ks, dg=None):
+    """Descents of the random starts seed + k, k in ks, as one batch; returns
+    the final centres (n, len(ks), 3) on the device.  A run's trajectory does
+    not depend on which other runs share its batch (fm_tr_align), so
+    batches of any split reproduce the full batch."""
+    dg = dg or device_graph(graph)
+    init = np.stack([np.random.default_rng(seed + k).standard_normal((graph.n, 3)) for k in ks],
+                    axis=1)
+    runs, _ = _align(dg, init, cfg, cfg.translation_steps)
+    return runs
 
 
-def multi_init_align(graph, cfg, seed=0, return_choice=False):
-    """Independent random-seed runs merged per image, then a final descent
-    (ref/translation.py:169-186).  All runs execute as one batched descent."""
-    if cfg.translation_inits == 1:
-        return align_centers(graph, cfg, seed=seed)
-    dg = device_graph(graph)
-    B = cfg.translation_inits
-    runs, _ = _align(dg, multi_init_inits(graph.n, B, seed), cfg, cfg.translation_steps)
+def merge_and_finish(graph, cfg, runs, dg=None, return_choice=False):
+    """Canonicalise the runs (n, B, 3), take per node the run with the lowest
+    mean incident residual (first minimum), and descend from the merged
+    centres (ref/translation.py:181-186)."""
+    dg = dg or device_graph(graph)
+    B = runs.shape[1]
+    runs = runs.contiguous()
     merged = torch.empty((graph.n, 1, 3), dtype=torch.float64, device=dg.device)
     choice = torch.empty(graph.n, dtype=torch.int32, device=dg.device)
     scratch = dg.scratch(B)
@@ -165,6 +169,17 @@ def multi_init_align(graph, cfg, seed=0, return_choice=False):
     if return_choice:
         return out + (choice.cpu().numpy(),)
     return out
+
+
+def multi_init_align(graph, cfg, seed=0, return_choice=False):
+    """Independent random-seed runs merged per image, then a final descent
+    (ref/translation.py:169-186).  All runs execute as one batched descent
+    (parallel.multi_init_align_sharded splits them over ranks)."""
+    if cfg.translation_inits == 1:
+        return align_centers(graph, cfg, seed=seed)
+    dg = device_graph(graph)
+    runs = init_runs(graph, cfg, seed, range(cfg.translation_inits), dg)
+    return merge_and_finish(graph, cfg, runs, dg, return_choice)
 
 
 __all__ = ["world_direction", "DirectionGraph", "translation_loss_and_grad", "canonicalize",

@@ -99,3 +99,44 @@ def test_sharded_allreduce_equals_single_process(golden_small):
                                   cams, out["W"], Z)
     np.testing.assert_allclose(total[-1], loss, rtol=1e-12)
     np.testing.assert_allclose(total[:-1], grad, rtol=1e-10, atol=1e-13 * np.abs(grad).max())
+
+
+def _gather_worker(rank, world, port, n_inits, result_q):
+    """Per-rank stand-in for the translation starts of
+    parallel.multi_init_align_sharded: rank r holds the 'runs' of its block
+    of starts (here the reference's seeded random starts themselves)."""
+    from paper_2505_04612_b200.parallel import TorchComm, gather_blocks, init_blocks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = TorchComm()
+    assert comm.world == world and comm.rank == rank
+    b = init_blocks(n_inits, world)
+    local = np.stack([np.random.default_rng(7 + k).standard_normal((11, 3))
+                      for k in range(b[rank], b[rank + 1])], axis=1).reshape(11, -1, 3)
+    runs = gather_blocks(torch.as_tensor(local), b, comm)
+    result_q.put((rank, runs.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_translation_starts_gather_in_order(world):
+    """The all-gather of per-rank start blocks (uneven: 7 starts) assembles
+    every run in start order on every rank."""
+    n_inits = 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n_inits, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = np.stack([np.random.default_rng(7 + k).standard_normal((11, 3)) for k in range(n_inits)],
+                    axis=1)
+    for _, runs in got:
+        assert np.array_equal(runs, full)

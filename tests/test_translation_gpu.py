@@ -8,6 +8,7 @@ canonical shape."""
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import fastmap_oracle as O
 from tests.helpers import Cfg
@@ -78,3 +79,35 @@ def test_config1_multi_init(golden_c1):
     b = O.canonicalize(g["c1_tr_centers"])
     s, R, t = O.umeyama(a, b)
     assert np.max(np.linalg.norm(a @ (s * R).T + t - b, axis=1)) < 1e-2
+
+
+def test_sharded_inits_reproduce_the_batch():
+    """Runs do not depend on their batch: starts split into blocks (as
+    parallel.multi_init_align_sharded does over ranks) give bitwise the same
+    runs, merge and final descent as the single batch."""
+    from paper_2505_04612_b200 import parallel as P_
+
+    rng = np.random.default_rng(5)
+    n, m = 40, 300
+    c = rng.normal(size=(n, 3))
+    e = set()
+    while len(e) < m:
+        i, j = rng.integers(0, n, size=2)
+        if i != j:
+            e.add((min(i, j), max(i, j)))
+    e = np.array(sorted(e))
+    d = c[e[:, 1]] - c[e[:, 0]]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    g = T.DirectionGraph(n=n, edges_i=e[:, 0], edges_j=e[:, 1], directions=d)
+
+    class C:
+        translation_lr, translation_steps, translation_inits = 1e-2, 300, 7
+        adam_beta1, adam_beta2, adam_eps = 0.9, 0.999, 1e-8
+    full = T.init_runs(g, C, 3, range(7))
+    for world in (2, 3):
+        b = P_.init_blocks(7, world)
+        parts = [T.init_runs(g, C, 3, range(b[r], b[r + 1])) for r in range(world)]
+        assert torch.equal(torch.cat(parts, dim=1), full)
+    c1, l1 = T.multi_init_align(g, C, seed=3)
+    c2, l2 = T.merge_and_finish(g, C, torch.cat(parts, dim=1))
+    assert np.array_equal(c1, c2) and l1 == l2
