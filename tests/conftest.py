@@ -23,3 +23,8 @@ def golden_small():
 @pytest.fixture(scope="session")
 def golden_c1():
     return dict(np.load(os.path.join(GOLDEN, "golden_config1.npz")))
+
+
+@pytest.fixture(scope="session")
+def golden_pipeline():
+    return dict(np.load(os.path.join(GOLDEN, "golden_pipeline.npz")))
