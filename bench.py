@@ -134,7 +134,12 @@ def dist_setup(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # FM_DIST_BACKEND=gloo: functional check of the multi-rank path with
+        # several ranks sharing one GPU (NCCL refuses duplicate devices)
+        backend = os.environ.get("FM_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
+    if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
     return world, rank, local
 
 
