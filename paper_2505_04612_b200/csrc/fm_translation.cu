@@ -15,6 +15,7 @@
 #include <vector>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "fm_common.cuh"
 
@@ -321,7 +322,10 @@ unsigned warp_blocks(int64_t warps) { return (unsigned)ceil_div(warps * 32, 256)
 // single run.  A run's summation order depends only on R, so a run's
 // trajectory is the same in any batch of >= 2 runs -- the multi-init runs
 // sharded over ranks reproduce the single-GPU batch bit for bit.
-int run_group(int B) { return B >= 2 ? 4 : 1; }
+int run_group(int B) {
+  if (const char* env = getenv("FM_TR_R")) return B >= 2 ? atoi(env) : 1;  // tuning override
+  return B >= 2 ? 4 : 1;
+}
 
 int build_incidence(const fm_dir_graph& g, const TrScratch& s, cudaStream_t st) {
   if (g.n_edges == 0) return FM_OK;
@@ -340,6 +344,12 @@ int enqueue_tr_steps(const fm_dir_graph& g, double* c0, double* c1, const TrScra
     double* nxt = (k & 1) ? c0 : c1;
     if (R == 1)
       tr_step_kernel<kTrAdam, 1><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
+                                                         b1, b2, eps, s.bc, k, flag);
+    else if (R == 2)
+      tr_step_kernel<kTrAdam, 2><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
+                                                         b1, b2, eps, s.bc, k, flag);
+    else if (R == 8)
+      tr_step_kernel<kTrAdam, 8><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
                                                          b1, b2, eps, s.bc, k, flag);
     else
       tr_step_kernel<kTrAdam, 4><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
