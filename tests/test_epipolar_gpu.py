@@ -90,13 +90,17 @@ def random_scene(n_images=8, n_points=700, seed=0, noise=2e-3):
     return Poses(rots, centers), [pairs[q] for q in perm]
 
 
+@pytest.mark.parametrize("lanes", ["4", "8", "16"])
 @pytest.mark.parametrize("chunk,precision", [(8192, "fp64"), (128, "fp64"), (8192, "fp32"),
                                              (128, "fp32")])
-def test_hot_point_pass_matches_oracle(chunk, precision):
-    """Fused prune + IRLS moments + L1 (hot kernel, bulk-copy pipeline) vs the
-    fp64 oracle; chunk=128 splits pairs over several work items (combine path).
-    fp64 moments: W within 3e-7 (the IRLS weight uses a rounded reciprocal,
-    a per-point multiplicative error); fp32 moments: 2e-5."""
+def test_hot_point_pass_matches_oracle(chunk, precision, lanes, monkeypatch):
+    """Fused prune + IRLS moments + L1 (hot kernel) vs the fp64 oracle, for
+    every lane-group width L (FM_HOT_L: 1, 2 or 4 sub-groups per item, so
+    items whose block count is not a multiple of the sub-groups exercise the
+    idle-block path); chunk=128 splits pairs over several work items (combine
+    path).  fp64 moments: W within 3e-7 (the IRLS weight uses a rounded
+    reciprocal, a per-point multiplicative error); fp32 moments: 2e-5."""
+    monkeypatch.setenv("FM_HOT_L", lanes)
     poses, pairs = random_scene(seed=3)
     n = len(poses.rotations)
     st = E.AdjustmentState.from_poses(poses, list(range(n)), 2, True)
