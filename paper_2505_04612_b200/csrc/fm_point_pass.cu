@@ -84,21 +84,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #endif
 
 
-__device__ __forceinline__ void store_red(const fm_pass_out& out, const PartialBufs& part, bool single,
-                                          int64_t P, int64_t NI, int n, int64_t item, int k, float val,
-                                          bool lin) {
-  if (!single) {
-    static_cast<float*>(part.red)[k * NI + item] = val;
-    return;
-  }
-  if (k < 36) {
-    out.mom32[k * P + n] = val;
-  } else if (k < 45) {
-    if (lin) out.vgrad[(k - 36) * P + n] = val;
-  } else if (out.n_active) {
-    out.n_active[n] = (int32_t)val;
-  }
-}
 
 // ------------------------------------------------------------------ hot kernel
 // z == 1 stores whose pairs start on 16-slot boundaries (store->slot_align
@@ -218,27 +203,8 @@ __global__ void describe_items_kernel(const fm_point_store s, int32_t* __restric
 #ifndef FM_HOT_NOLOAD
 #define FM_HOT_NOLOAD 0  // tuning experiment only: skip the coordinate/mask copies
 #endif
-#ifndef FM_HOT_F2F
-#define FM_HOT_F2F 0  // 1: plain F2F conversions in the residual head (reference variant)
-#endif
-constexpr double kUnscale = 0x1p896;  // 2^(1023 - 127)
-
-// fp32 -> fp64 on the integer pipe: the double whose bits are the fp32 bits
-// shifted right by 3 (sign restored) equals x * 2^-896 exactly for every finite
-// x -- normal, subnormal and signed zero -- because the fp32 exponent field
-// lands unbiased in the low 8 bits of the fp64 exponent field.  Stores on the
-// hot path hold finite coordinates only (slot_align >= 16 contract).
-__device__ __forceinline__ double scaled_f2d(float x) {
-  // hi: arithmetic shift keeps the sign in bit 31 and smears it over bits
-  // 30..28, which the mask clears; lo: the 3 low mantissa bits.
-  const int u = __float_as_int(x);
-  return __hiloint2double((u >> 3) & (int)0x8FFFFFFF, u << 29);
-}
-
 template <bool kPrune, bool kL1, bool kMom, bool MOM64>
 struct HotAcc {
-  // plain F2F conversions where the fp64 moments need the coordinates anyway
-  static constexpr bool kF2F = FM_HOT_F2F || (kMom && MOM64);
   double M64[MOM64 ? 36 : 1];
   float2 Mp[MOM64 ? 1 : 18];  // [j][k]: A_j x B-pair k, k: (B0,B3) (B2,B4) (B1,B5)
   float2 V0, V1, V2, V3;      // (v00,v01) (v10,v11) (v20,v21) (v02,v12)
@@ -261,26 +227,12 @@ struct HotAcc {
   // residual and weight are computed for every slot and masked afterwards.
   __device__ __forceinline__ bool point(const double (&G)[9], float a, float b, float c, float d,
                                         bool act, double thr) {
-    // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255).  The fp32
-    // coordinates enter as x 2^-896 built on the integer pipe (scaled_f2d);
-    // G's coordinate columns carry the inverse factor 2^896 and y0, y1 are
-    // rescaled by it, so every DFMA sees the same exact products and rounds
-    // exactly as with (double)x -- without the XU-bound F2F conversions.
-    double A, B, C, D, r;
-    if (kF2F) {  // exact fp64 moments reuse the converted coordinates
-      A = a; B = b; C = c; D = d;
-      const double y0 = fma(G[0], A, fma(G[1], B, G[2]));
-      const double y1 = fma(G[3], A, fma(G[4], B, G[5]));
-      const double y2 = fma(G[6], A, fma(G[7], B, G[8]));
-      r = fma(C, y0, fma(D, y1, y2));
-    } else {
-      const double As = scaled_f2d(a), Bs = scaled_f2d(b), Cs = scaled_f2d(c), Ds = scaled_f2d(d);
-      const double y0 = fma(G[0], As, fma(G[1], Bs, G[2])) * kUnscale;
-      const double y1 = fma(G[3], As, fma(G[4], Bs, G[5])) * kUnscale;
-      const double y2 = fma(G[6], As, fma(G[7], Bs, G[8]));
-      r = fma(Cs, y0, fma(Ds, y1, y2));
-      A = B = C = D = 0.0;
-    }
+    // residual r = x2^T Ghat x1 in fp64 (ref/epipolar.py:255)
+    const double A = a, B = b, C = c, D = d;
+    const double y0 = fma(G[0], A, fma(G[1], B, G[2]));
+    const double y1 = fma(G[3], A, fma(G[4], B, G[5]));
+    const double y2 = fma(G[6], A, fma(G[7], B, G[8]));
+    const double r = fma(C, y0, fma(D, y1, y2));
     const double ar = fabs(r);
     const bool keep = (kPrune && !FM_HOT_NOLOAD) ? (act & (ar <= thr)) : act;
     if (kL1) l1 += act ? ar : 0.0;
@@ -421,10 +373,7 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   const bool skip = has_item && kSkip && __ldg(prev_active + pn) == 0;
   double G[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    G[k] = has_item ? __ldg(ghat + k * P + pn) : 0.0;
-    if (!HotAcc<kPrune, kL1, kMom, MOM64>::kF2F && k % 3 != 2) G[k] *= kUnscale;  // coordinate columns (exact)
-  }
+  for (int k = 0; k < 9; ++k) G[k] = has_item ? __ldg(ghat + k * P + pn) : 0.0;
   const int nblk = (has_item && !skip) ? (d.len + kBlkSlots - 1) / kBlkSlots : 0;  // skipped: no work
   const int nit = (nblk + S - 1) / S;
   const int warp_it = __reduce_max_sync(0xffffffffu, nit);

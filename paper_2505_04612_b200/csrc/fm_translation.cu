@@ -62,8 +62,6 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
-__device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : (x == 0 ? 0.0 : x)); }
-
 // 1/sqrt(q) for normal q > 0: hardware approximation + two Newton steps
 // (~1 ulp; no slow-path call)
 __device__ __forceinline__ double rsqrt_nr(double q) {

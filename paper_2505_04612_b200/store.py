@@ -25,7 +25,6 @@ from . import _native as N
 
 CHUNK = 8192          # slots per work item (multiple of 128)
 SLOT_ALIGN = 16       # pair start alignment (slots): whole 16-slot blocks for the hot kernel
-HOT_MAX_COORD = 1e30  # hot-kernel coordinate bound (finite, no fp64 overflow in the 2^896 scaling)
 CAM_CHUNK = 4096      # incidences per camera-reduction chunk
 
 
@@ -125,10 +124,6 @@ class PointPairStore:
                 active = act & ~bad
         homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
         self.homogeneous = bool(homog)
-        # the hot kernel builds fp64 coordinates on the integer pipe, exact for
-        # finite fp32 values only; other stores take the generic kernel
-        self.hot_ok = bool(len(x1) == 0 or (np.all(np.abs(x1[:, :2]) < HOT_MAX_COORD) and
-                                             np.all(np.abs(x2[:, :2]) < HOT_MAX_COORD)))
         c1 = np.zeros((n_slots, 2), dtype=np.float32)
         c2 = np.zeros((n_slots, 2), dtype=np.float32)
         c1[self.point_slot] = x1[:, :2]
@@ -165,8 +160,7 @@ class PointPairStore:
                 x1=self.x1.data_ptr(), x2=self.x2.data_ptr(),
                 x1z=self.x1z.data_ptr() if self.x1z is not None else None,
                 x2z=self.x2z.data_ptr() if self.x2z is not None else None,
-                active=self.active.data_ptr(), item_desc=None,
-                slot_align=SLOT_ALIGN if self.hot_ok else 4)
+                active=self.active.data_ptr(), item_desc=None, slot_align=SLOT_ALIGN)
             self.item_desc_d = torch.empty((max(self.n_items, 1), 4), dtype=torch.int32,
                                            device=self.device)
             self._struct.item_desc = self.item_desc_d.data_ptr()
@@ -236,8 +230,6 @@ class PointPairStore:
         self.x1z = self.x2z = None
         self.homogeneous = False
         self.sanitized = True  # device-generated coordinates are finite
-        self.hot_ok = bool((self.x1.abs().max() < HOT_MAX_COORD).item() and
-                           (self.x2.abs().max() < HOT_MAX_COORD).item()) if n_slots else True
         bits = torch.zeros(n_slots, dtype=torch.int64, device=device)
         bits[slot] = 1
         w = (bits.view(-1, 32) << torch.arange(32, device=device, dtype=torch.int64)).sum(1)

@@ -331,8 +331,7 @@ def test_integration_stub(golden_small):
 
 def test_l1_loss_with_nonfinite_active_point_is_nan(golden_small):
     """An active NaN coordinate makes the reference's l1 loss NaN
-    (ref/epipolar.py:156-160); such stores leave the hot kernel (whose
-    integer-pipe fp32->fp64 conversion is exact for finite values only)."""
+    (ref/epipolar.py:156-160); the hot L1 pass propagates it."""
     g = golden_small
     pairs = pairs_from(g, "e0_", E.EpipolarPair)
     st = _state(g, "e0_")
