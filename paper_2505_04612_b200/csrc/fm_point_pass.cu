@@ -71,6 +71,7 @@ struct PartialBufs {
   double* s0;  // [n_items]
   double* l1;  // [n_items]
   int64_t cap; // items the buffers hold
+  unsigned int* ctr;  // [2] work counters of the persistent launch (zero at rest), or NULL
 };
 
 #ifdef FM_HOT_TRACE
@@ -337,10 +338,10 @@ struct LaneRing {
 // (slots {2h, 2h+1, 2h+8, 2h+9}): every copy instruction of a sub-group reads
 // whole 32-byte sectors.
 template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
-point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
-               const int32_t* __restrict__ prev_active, const fm_pass_out out,
-               const PartialBufs part) {
+__device__ __forceinline__ void hot_body(const fm_point_store& s, const double* __restrict__ ghat,
+                                         const double thr, const int32_t* __restrict__ prev_active,
+                                         const fm_pass_out& out, const PartialBufs& part,
+                                         const int64_t group, const int64_t item_base) {
   constexpr bool kPrune = MODE & FM_PASS_PRUNE;
   constexpr bool kL1 = MODE & FM_PASS_L1;
   constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
@@ -361,7 +362,7 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   const int g = lane % L;  // lane within the item group
   const int sg = g >> 2;   // sub-group: block offset within an iteration
   const int h = g & 3;     // lane within the sub-group
-  const int64_t item = ((int64_t)blockIdx.x * kGrpWarps + wib) * IPW + lane / L;
+  const int64_t item = item_base + group * IPW + lane / L;  // group: the warp's item group
   const bool has_item = item < s.n_items;
   const int64_t NI = s.n_items;
 
@@ -465,7 +466,25 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
 #pragma unroll
     for (int k = 38; k < N; ++k) v[k] = 0.0;
     group_transpose_reduce<L>(v, lane);
-    if (has_item) {
+    if (NI == P) {  // staged, row-coalesced stores (see the fp32 path)
+      double* stage = reinterpret_cast<double*>(&ring.c[0][0][0]);
+      const int q = lane / L;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < N / L; ++i) stage[(g * (N / L) + i) * IPW + q] = v[i];
+      __syncwarp();
+      const int64_t n0 = item - q;
+#pragma unroll 1
+      for (int t = lane; t < 38 * IPW; t += 32) {
+        const int k = t / IPW;
+        const int64_t n = n0 + (t % IPW);
+        if (n >= P) continue;
+        const double val = stage[t];
+        if (k < 36) out.mom64[(int64_t)k * P + n] = val;
+        else if (k == 36) { if (out.n_active) out.n_active[n] = (int32_t)val; }
+        else if (kL1 && out.l1) out.l1[n] = val;
+      }
+    } else if (has_item) {
 #pragma unroll
       for (int i = 0; i < N / L; ++i) {
         const int k = g * (N / L) + i;
@@ -499,7 +518,32 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
     v[47] = 0.f;
     group_transpose_reduce<L>(v, lane);
     const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
-    if (has_item) {
+    if (NI == P) {
+      // every item is a whole pair (item == pair): stage the warp's sums in
+      // its idle ring and write each output row as IPW consecutive pairs --
+      // a handful of sectors per store instead of one per lane
+      float* stage = reinterpret_cast<float*>(&ring.c[0][0][0]);
+      double* stage_l1 = reinterpret_cast<double*>(stage + N * IPW);
+      const int q = lane / L;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < N / L; ++i) stage[(g * (N / L) + i) * IPW + q] = v[i];
+      if (g == 0) stage_l1[q] = l1;
+      __syncwarp();
+      const int64_t n0 = item - q;  // first pair of the warp
+#pragma unroll 1
+      for (int t = lane; t < 47 * IPW; t += 32) {
+        const int vi = t / IPW;
+        const int64_t n = n0 + (t % IPW);
+        if (n >= P) continue;
+        const float val = stage[t];
+        if (vi < 36) out.mom32[(int64_t)hot_mom_index(vi) * P + n] = val;
+        else if (vi < 45) { if (kLin) out.vgrad[(int64_t)(vi - 36) * P + n] = val; }
+        else if (vi == 45) { if (out.n_active) out.n_active[n] = (int32_t)val; }
+        else out.s0[n] = (double)val;
+      }
+      if (kL1 && out.l1 && lane < IPW && n0 + lane < P) out.l1[n0 + lane] = stage_l1[lane];
+    } else if (has_item) {
       // destination of each of the lane's N/L sums: a float column (moment,
       // vgrad or partial), the int count or the fp64 s0
 #pragma unroll
@@ -546,6 +590,60 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < 16384) g_hot_trace[blockIdx.x][3] = globaltimer();
 #endif
+}
+
+template <unsigned MODE, bool MOM64, int L>
+__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
+point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const double thr,
+               const int32_t* __restrict__ prev_active, const fm_pass_out out,
+               const PartialBufs part) {
+  hot_body<MODE, MOM64, L>(s, ghat, thr, prev_active, out, part,
+                           (int64_t)blockIdx.x * kGrpWarps + (threadIdx.x >> 5), 0);
+}
+
+// Persistent variant: one launch of resident blocks; every warp takes the
+// next item group from a global counter until none is left, so warps the
+// scheduler starves simply process fewer groups and the launch ends ~one
+// group after the queue drains.  counters[0] = next group, counters[1] =
+// finished warps; the last warp to finish re-zeroes both (zero at rest).
+template <unsigned MODE, bool MOM64, int L>
+__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
+point_pass_hot_dyn(const fm_point_store s, const double* __restrict__ ghat, const double thr,
+                   const int32_t* __restrict__ prev_active, const fm_pass_out out,
+                   const PartialBufs part, unsigned int* __restrict__ counters, const int64_t n_groups) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int grp = 0;
+    if (lane == 0) grp = atomicAdd(counters, 1u);
+    grp = __shfl_sync(0xffffffffu, grp, 0);
+    if ((int64_t)grp >= n_groups) break;
+    hot_body<MODE, MOM64, L>(s, ghat, thr, prev_active, out, part, grp, 0);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const unsigned int total = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(counters + 1, 1u) == total - 1) {
+      counters[0] = 0;
+      counters[1] = 0;
+    }
+  }
+}
+
+// Tail-shortened launch: items [0, n1) with L1 lanes per item (the most
+// efficient width, in whole waves), the rest with L2 > L1 lanes per item in
+// the blocks the scheduler dispatches last -- a tail item then takes
+// L1/L2 of the time, so the low-occupancy end of the launch shrinks.
+template <unsigned MODE, bool MOM64, int L1, int L2>
+__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
+point_pass_hot_mixed(const fm_point_store s, const double* __restrict__ ghat, const double thr,
+                     const int32_t* __restrict__ prev_active, const fm_pass_out out,
+                     const PartialBufs part, const int64_t nb1, const int64_t n1) {
+  if ((int64_t)blockIdx.x < nb1)
+    hot_body<MODE, MOM64, L1>(s, ghat, thr, prev_active, out, part,
+                              (int64_t)blockIdx.x * kGrpWarps + (threadIdx.x >> 5), 0);
+  else
+    hot_body<MODE, MOM64, L2>(s, ghat, thr, prev_active, out, part,
+                              ((int64_t)blockIdx.x - nb1) * kGrpWarps + (threadIdx.x >> 5), n1);
 }
 
 // -------------------------------------------------------------- generic kernel
@@ -772,6 +870,54 @@ int launch_hot_l(const fm_point_store& s, double thr, const double* ghat, const 
   return FM_OK;
 }
 
+template <unsigned MODE, bool MOM64, int L1, int L2>
+int launch_hot_mixed(const fm_point_store& s, double thr, const double* ghat,
+                     const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
+                     cudaStream_t stream, int64_t n1) {
+  const size_t smem = kGrpWarps * sizeof(LaneRing);
+  static bool attr = false;
+  if (!attr) {
+    FM_CUDA(cudaFuncSetAttribute(point_pass_hot_mixed<MODE, MOM64, L1, L2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t nb1 = n1 / (kGrpWarps * (32 / L1));
+  const int64_t nb2 = ceil_div(ceil_div(s.n_items - n1, 32 / L2), kGrpWarps);
+  point_pass_hot_mixed<MODE, MOM64, L1, L2><<<(unsigned)(nb1 + nb2), kGrpWarps * 32, smem, stream>>>(
+      s, ghat, thr, prev_active, out, part, nb1, n1);
+  FM_LAUNCHED(point_pass_hot_mixed);
+  if (s.n_items > s.n_pairs) {
+    combine_kernel<MOM64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
+                                                                                        !MOM64);
+    FM_LAUNCHED(combine_kernel);
+  }
+  return FM_OK;
+}
+
+template <unsigned MODE, bool MOM64, int L>
+int launch_hot_dyn(const fm_point_store& s, double thr, const double* ghat,
+                   const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
+                   cudaStream_t stream, unsigned int* counters, int bps) {
+  const size_t smem = kGrpWarps * sizeof(LaneRing);
+  static bool attr = false;
+  if (!attr) {
+    FM_CUDA(cudaFuncSetAttribute(point_pass_hot_dyn<MODE, MOM64, L>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t groups = ceil_div(s.n_items, 32 / L);
+  const int64_t grid = std::min<int64_t>((int64_t)bps * sm_count(), ceil_div(groups, kGrpWarps));
+  point_pass_hot_dyn<MODE, MOM64, L><<<(unsigned)grid, kGrpWarps * 32, smem, stream>>>(
+      s, ghat, thr, prev_active, out, part, counters, groups);
+  FM_LAUNCHED(point_pass_hot_dyn);
+  if (s.n_items > s.n_pairs) {
+    combine_kernel<MOM64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
+                                                                                        !MOM64);
+    FM_LAUNCHED(combine_kernel);
+  }
+  return FM_OK;
+}
+
 // Lanes per item L in {4, 8, 16}: blocks are one-shot, so the last wave of
 // a launch is partially filled.  Score each L by the filled fraction of its
 // waves and a per-item reduction cost (log2(L) transpose-reduce levels plus a
@@ -804,7 +950,24 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
       pick = L;
     }
   }
+  // Whole waves of L = 4 items, the rest of the launch at L = 16 (see
+  // point_pass_hot_mixed) when that rest is under one wave.
+  {
+    const int64_t G4 = (int64_t)bps[0] * sm_count() * kGrpWarps * 8;  // items per L=4 wave
+    const int64_t n1 = (s.n_items / G4) * G4;
+    const char* env_mix = getenv("FM_HOT_MIX");
+    const bool mix = env_mix ? atoi(env_mix) != 0 : true;
+    if (mix && !getenv("FM_HOT_L") && !getenv("FM_HOT_DYN") && n1 > 0 && s.n_items > n1 && mean_blk >= 8)
+      return launch_hot_mixed<MODE, MOM64, 4, 16>(s, thr, ghat, prev_active, out, part, stream, n1);
+  }
   if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
+  if (const char* env = getenv("FM_HOT_DYN")) {
+    if (atoi(env) && part.ctr) {
+      if (pick == 16) return launch_hot_dyn<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[2]);
+      if (pick == 8) return launch_hot_dyn<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[1]);
+      return launch_hot_dyn<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[0]);
+    }
+  }
   if (pick == 16) return launch_hot_l<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream);
   if (pick == 8) return launch_hot_l<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream);
   return launch_hot_l<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);
@@ -941,11 +1104,14 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE(f64 ? out->mom64 != nullptr : out->mom32 != nullptr, "moment output missing");
     if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
   }
-  PartialBufs part{nullptr, nullptr, nullptr, 0};
+  PartialBufs part{nullptr, nullptr, nullptr, 0, nullptr};
   cudaStream_t st = as_stream(stream);
   fm_point_store s2 = s;  // with item descriptors
   {
     Scratch sc(scratch, scratch_bytes);
+    // first 256 bytes: the persistent launch's work counters (the caller
+    // zeroes the scratch once; every launch leaves them zero)
+    if (scratch) part.ctr = sc.take<unsigned int>(2);
     if (s.n_items > s.n_pairs) {
       part.red = sc.take<double>((size_t)s.n_items * kNumRed);
       part.s0 = sc.take<double>((size_t)s.n_items);

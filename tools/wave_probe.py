@@ -22,9 +22,15 @@ for n_img, band, ppp in cases:
         eng = E.IrlsEngine(store, graph, params, HotPathConfig(), precision=prec)
         eng._ghat()
         res = {}
-        for L in ["plan", "4", "8"]:
-            os.environ["FM_HOT_PLAN"] = "1" if L == "plan" else "0"
-            os.environ["FM_HOT_L"] = "4" if L == "plan" else L
+        for L in ["auto", "4", "8", "d4", "d8"]:
+            os.environ.pop("FM_HOT_DYN", None)
+            if L == "auto":
+                os.environ.pop("FM_HOT_L", None)
+            elif L.startswith("d"):
+                os.environ["FM_HOT_DYN"] = "1"
+                os.environ["FM_HOT_L"] = L[1:]
+            else:
+                os.environ["FM_HOT_L"] = L
             eng.buf.n_active[0].fill_(1)
             ts = []
             for k in range(15):
@@ -38,7 +44,8 @@ for n_img, band, ppp in cases:
             res[f"L{L}_us"] = round(t, 2)
             res[f"L{L}_ps_per_pt"] = round(t * 1e6 / store.n_points, 3)
         os.environ.pop("FM_HOT_L", None)
-        os.environ.pop("FM_HOT_PLAN", None)
+        os.environ.pop("FM_HOT_DYN", None)
+
         print(json.dumps({"pairs": store.n_pairs, "ppp": ppp, "items": store.n_items, "prec": prec, **res}), flush=True)
     del eng, store, sc, graph
     torch.cuda.empty_cache()
