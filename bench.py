@@ -79,7 +79,7 @@ class ClockSampler:
             sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.samples.append((float(sm), float(mx), int(rs)))
-            self._stop.wait(0.001)
+            self._stop.wait(0.0002)
 
     def _run_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"

@@ -132,7 +132,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #endif
 constexpr int kRing = FM_HOT_RING;  // stages per lane
 constexpr int kUnroll = FM_HOT_UNROLL;  // main-loop unroll (points in flight per lane = 4 x kUnroll)
-constexpr int kGrpWarps = 4;        // warps per block
+constexpr int kGrpWarps = 4;  // warps per block (8 or 16: slower, measured)
 constexpr int kBlkSlots = 16;       // slots per group iteration (= slot alignment)
 
 __device__ __forceinline__ float and_mask(float x, unsigned m) {

@@ -10,12 +10,14 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 flush_rd = torch.ones(64 << 20, dtype=torch.float32, device=dev)  # clean lines after the dirty fill
 full = N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED
 l1 = N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED
-for ppp in [int(x) for x in (sys.argv[1:] or ["100", "200", "400", "800", "1600"])]:
-    spec = scenes.SceneSpec(n_images=500, band=50, points_per_pair=ppp)
+for arg in (sys.argv[1:] or ["100", "200", "400", "800", "1600"]):
+    parts = [int(x) for x in arg.split(",")]
+    n_img, band, ppp = (500, 50, parts[0]) if len(parts) == 1 else parts
+    spec = scenes.SceneSpec(n_images=n_img, band=band, points_per_pair=ppp)
     sc = scenes.generate(spec, dev); store = scenes.device_store(sc, dev); graph, ids = scenes.device_graph(sc, dev)
     params = torch.as_tensor(scenes.initial_params(sc, ids), device=dev)
     eng = E.IrlsEngine(store, graph, params, HotPathConfig(), precision="fp32"); eng._ghat()
-    out = {"ppp": ppp, "points": store.n_points}
+    out = {"pairs": store.n_pairs, "ppp": ppp, "points": store.n_points}
     for name, mode in (("full", full), ("l1", l1)):
         eng.buf.n_active[0].fill_(1)
         ts = []
