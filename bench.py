@@ -355,10 +355,13 @@ def run_ours(args, spec, world, rank, local):
     # ------------------------------------------- SfM optimize time (rank 0)
     extra = {}
     if not args.skip_optimize and world > 1:
-        # config 3 with the 16 random starts split over the ranks (collective)
+        # config 3 with the 16 random starts split over the ranks, and the
+        # rank-0 scene's irls_refine with its point pairs sharded over the
+        # ranks (NCCL all-reduce of the per-image gradient per Adam step)
         tr = translation_bench(device, stream, sharded=True)
+        ep = sharded_irls_bench(spec, args, device, stream, world, rank)
         if rank == 0:
-            extra["sfm_optimize"] = {"translation_sharded_over_ranks": world, **tr}
+            extra["sfm_optimize"] = {"translation_sharded_over_ranks": world, **tr, **ep}
     if rank == 0 and not args.skip_optimize:
         params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
         store.reset_active()
@@ -419,6 +422,44 @@ def run_ours(args, spec, world, rank, local):
             **extra,
         }
         print(json.dumps(line), flush=True)
+
+
+def sharded_irls_bench(spec, args, device, stream, world, rank):
+    """irls_refine of the rank-0 C2 scene with its image pairs split into
+    contiguous point-balanced ranges over the ranks (parallel.ShardedIrlsEngine:
+    local passes, one all-reduce of the packed gradient per Adam step)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_04612_b200 import parallel as P_
+    from paper_2505_04612_b200 import scenes
+    from paper_2505_04612_b200.store import PairGraph, PointPairStore
+    with torch.cuda.stream(stream):
+        sc = scenes.generate(spec, device)  # every rank: the same (rank-0) scene
+        lengths = sc["lengths"]
+        b = P_.partition_pairs(lengths, world)
+        start = np.concatenate([[0], np.cumsum(lengths)])
+        lo, hi = int(b[rank]), int(b[rank + 1])
+        ij = sc["ij"]
+        ids = np.unique(ij)
+        ii, jj = np.searchsorted(ids, ij[:, 0]), np.searchsorted(ids, ij[:, 1])
+        store = PointPairStore.from_device(sc["x1"][start[lo]:start[hi]], sc["x2"][start[lo]:start[hi]],
+                                           lengths[lo:hi], device=device)
+        zeros = np.zeros(hi - lo, dtype=np.int64)
+        graph = PairGraph(ii[lo:hi], jj[lo:hi], zeros, zeros, len(ids), 1, True, device=device)
+        del sc
+        params = torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids), device=device)
+        eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params, args.cfg,
+                                   comm=P_.TorchComm())
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        l1h = eng.run()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"irls_refine_sharded_s": float(t.item()), "irls_sharded_l1_history": l1h,
+            "irls_sharded_over_ranks": world, "irls_sharded_pairs_rank0": hi - lo}
 
 
 def translation_bench(device, stream, sharded=False):

@@ -155,9 +155,10 @@ class ShardedIrlsEngine:
             else:
                 total += torch.cat([sh.grad, sh.loss])
         self.comm.allreduce_(total)
-        if not torch.isfinite(total[-1]):
-            self.aflag.fill_(N.FM_ERR_NONFINITE_LOSS)
-            return
+        # non-finite loss -> device flag (raised at the end of the IRLS
+        # iteration, like the graphed single-store engine); no host sync
+        bad = ~torch.isfinite(total[-1:])
+        self.aflag.masked_fill_(bad & (self.aflag == 0), N.FM_ERR_NONFINITE_LOSS)
         g = total[:-1].contiguous()
         N.check(self.lib.fm_adam_step(N.ptr(self.params), N.ptr(self.m), N.ptr(self.v), N.ptr(g),
                                       self.params.numel(), t, lr, cfg.adam_beta1, cfg.adam_beta2,
@@ -233,7 +234,6 @@ def make_shards(x1, x2, lengths, ij, cams, n_images, n_cameras, refine_focal, bo
     return out
 
 
-__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NoComm", "make_shards"]
 
 
 def init_blocks(n_inits, world):
@@ -275,3 +275,7 @@ def gather_blocks(local, b, comm):
     pad[:, :local.shape[1]] = local
     parts = comm.allgather(pad)
     return torch.cat([p[:, :int(b[r + 1] - b[r])] for r, p in enumerate(parts)], dim=1)
+
+
+__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NoComm", "make_shards",
+           "init_blocks", "gather_blocks", "multi_init_align_sharded"]

@@ -93,6 +93,14 @@ def pair_list(spec):
     return ij[order]
 
 
+def generate_poses(spec):
+    """The scene's GT and perturbed poses alone (host; as generate() draws them)."""
+    rng = np.random.default_rng(spec.seed)
+    rots, centers = ring_poses(spec.n_images)
+    R_in, c_in = perturb_poses(rots, centers, spec, rng)
+    return dict(R_gt=rots, c_gt=centers, R_in=R_in, c_in=c_in)
+
+
 def generate(spec, device, pair_slice=None):
     """Device tensors of a scene: x1, x2 (Z, 2) float32 in (i, j) pair order,
     per-pair lengths (host int64), pair ids (host), GT and perturbed poses."""
