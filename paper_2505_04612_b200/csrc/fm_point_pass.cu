@@ -957,7 +957,10 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     const int64_t n1 = (s.n_items / G4) * G4;
     const char* env_mix = getenv("FM_HOT_MIX");
     const bool mix = env_mix ? atoi(env_mix) != 0 : true;
-    if (mix && !getenv("FM_HOT_L") && !getenv("FM_HOT_DYN") && n1 > 0 && s.n_items > n1 && mean_blk >= 8)
+    // (moment passes only: the light L1 pass runs faster with one width)
+    constexpr bool kMomPass = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
+    if (kMomPass && mix && !getenv("FM_HOT_L") && !getenv("FM_HOT_DYN") && n1 > 0 &&
+        s.n_items > n1 && mean_blk >= 8)
       return launch_hot_mixed<MODE, MOM64, 4, 16>(s, thr, ghat, prev_active, out, part, stream, n1);
   }
   if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
