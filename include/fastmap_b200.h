@@ -304,6 +304,29 @@ int fm_tr_merge(const fm_dir_graph* g, double* centers, int32_t n_runs,
                 double* merged, int32_t* choice, void* scratch,
                 size_t scratch_bytes, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* relative-translation sphere search (SURVEY 8f "next" #1)                  */
+/* ------------------------------------------------------------------------ */
+/*
+ * Mean absolute epipolar error of every candidate direction of one image pair
+ * (ref/translation.py:52-55, `_mean_epipolar_errors`):
+ *   errors[c] = (1/M) sum_m | x2_m^T [d_c]_x R x1_m |
+ * x1, x2: [M][3] normalized homogeneous points (fp64), R: [3][3] relative
+ * rotation (frame i -> j, row-major), dirs: [C][3] unit candidates.
+ */
+int fm_sphere_errors(const double* x1, const double* x2, int64_t M, const double* R,
+                     const double* dirs, int32_t C, double* errors_out, void* stream);
+
+/*
+ * Cheirality counts of a relative pose and its mirrored translation
+ * (ref/twoview.py:246-253 `_positive_depth_count` on (R, t) and (R, -t)):
+ * each point pair triangulated by the linear (DLT) method -- the right
+ * singular vector of the 4x4 system for its smallest singular value -- and
+ * counted when in front of both cameras.  counts_out: 2 int32 (t, -t).
+ */
+int fm_depth_counts(const double* R, const double* t, const double* x1,
+                    const double* x2, int64_t M, int32_t* counts_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,8 +48,10 @@ def install(fastmap_module=None):
                  "current_residuals", "irls_refine", "poses_from_state"):
         swap(ref_epi, name, getattr(epipolar, name))
     for name in ("translation_loss_and_grad", "canonicalize", "align_centers",
-                 "per_node_residuals", "multi_init_align"):
+                 "per_node_residuals", "multi_init_align", "reestimate_relative"):
         swap(ref_tr, name, getattr(translation, name))
+    # raise the reference's PairRejected, which ref/pipeline.py:210 catches
+    swap(translation, "PairRejected", ref_tr.PairRejected)
     for name in ("rot6d_to_matrix", "rot6d_jacobian"):
         swap(ref_opt, name, getattr(optim, name))
     return saved

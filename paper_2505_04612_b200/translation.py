@@ -9,6 +9,12 @@ lock-step as one batched descent (one read of every edge serves all runs),
 merges them on the device (``fm_tr_merge``) and finishes with the final
 descent.  The random starts are drawn with the reference's own seeded numpy
 generator, so run k starts from bit-identical centres.
+
+``reestimate_relative`` (ref/translation.py:19-95, SURVEY 8f "next" #1) is
+the per-image-pair sphere search that produces the graph's directions: the
+candidate lattices are the reference's (same numpy expressions), the mean
+epipolar errors of every candidate run on the device (``fm_sphere_errors``)
+and so do the cheirality counts (``fm_depth_counts``).
 """
 
 import ctypes
@@ -21,6 +27,86 @@ from . import _native as N
 from .store import DirGraphDevice
 
 _NORM_EPS = 1e-8
+_GOLDEN_ANGLE = np.pi * (3.0 - np.sqrt(5.0))
+
+
+class PairRejected(ValueError):
+    """The pair carries no usable translation signal (ref/translation.py:19-20).
+    install() rebinds this name to the reference's class, so the pipeline's
+    ``except translation.PairRejected`` catches ours."""
+
+
+def fibonacci_sphere(n):
+    """The reference's deterministic unit-sphere lattice of n points
+    (ref/translation.py:23-29)."""
+    k = np.arange(n, dtype=np.float64) + 0.5
+    z = 1.0 - 2.0 * k / n
+    r = np.sqrt(np.maximum(1.0 - z * z, 0.0))
+    phi = _GOLDEN_ANGLE * k
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+
+
+def _cap_samples(axis, radius, n):
+    """Spiral of n directions within angle `radius` of `axis`
+    (ref/translation.py:32-49)."""
+    k = np.arange(n, dtype=np.float64) + 0.5
+    theta = radius * np.sqrt(k / n)
+    phi = _GOLDEN_ANGLE * k
+    local = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)],
+                     axis=1)
+    axis = axis / np.linalg.norm(axis)
+    ref = np.array([1.0, 0.0, 0.0]) if abs(axis[2]) > 0.9 else np.array([0.0, 0.0, 1.0])
+    u = np.cross(ref, axis)
+    u /= np.linalg.norm(u)
+    v = np.cross(axis, u)
+    return local @ np.stack([u, v, axis], axis=1).T
+
+
+def reestimate_relative(x1, x2, rel_rotation, cfg):
+    """Unit relative translation of an image pair by sphere search
+    (ref/translation.py:58-95): mean |x2^T [t]_x R x1| over a Fibonacci
+    lattice of cfg.sphere_samples directions, refined cfg.sphere_refine_levels
+    times on shrinking caps around the best, sign by cheirality on the first
+    200 points.  Raises PairRejected for empty, flat (near-zero baseline) or
+    cheirality-tied pairs, with the reference's messages."""
+    x1 = np.asarray(x1, dtype=np.float64)
+    x2 = np.asarray(x2, dtype=np.float64)
+    if len(x1) == 0:
+        raise PairRejected("no inlier point pairs")
+    device = N.require_cuda()
+    lib = N.lib()
+    X1 = torch.as_tensor(np.ascontiguousarray(x1.reshape(-1, 3)), device=device)
+    X2 = torch.as_tensor(np.ascontiguousarray(x2.reshape(-1, 3)), device=device)
+    R = torch.as_tensor(np.ascontiguousarray(rel_rotation, dtype=np.float64), device=device)
+    n = int(cfg.sphere_samples)
+
+    def errors(cands):
+        d = torch.as_tensor(np.ascontiguousarray(cands), device=device)
+        e = torch.empty(len(cands), dtype=torch.float64, device=device)
+        N.check(lib.fm_sphere_errors(N.ptr(X1), N.ptr(X2), len(x1), N.ptr(R), N.ptr(d), len(cands),
+                                     N.ptr(e), N.stream_handle()))
+        return e.cpu().numpy()
+
+    cands = fibonacci_sphere(n)
+    err = errors(cands)
+    med = float(np.median(err))
+    if med < 1e-15 or np.min(err) > 0.9 * med:
+        raise PairRejected("flat epipolar landscape (near-zero baseline)")
+    best = cands[int(np.argmin(err))]
+    radius = 2.0 * np.sqrt(4.0 * np.pi / n)
+    for _ in range(int(cfg.sphere_refine_levels)):
+        cands = _cap_samples(best, radius, n)
+        best = cands[int(np.argmin(errors(cands)))]
+        radius *= 2.0 * np.sqrt(np.pi / n)
+    m = min(len(x1), 200)
+    t = torch.as_tensor(np.ascontiguousarray(best), device=device)
+    counts = torch.empty(2, dtype=torch.int32, device=device)
+    N.check(lib.fm_depth_counts(N.ptr(R), N.ptr(t), N.ptr(X1), N.ptr(X2), m, N.ptr(counts),
+                                N.stream_handle()))
+    pos, neg = (int(v) for v in counts.cpu().numpy())
+    if pos == neg:
+        raise PairRejected("cheirality tie")
+    return best if pos > neg else -best
 
 
 def world_direction(t_ij, R_j):
@@ -182,5 +268,6 @@ def multi_init_align(graph, cfg, seed=0, return_choice=False):
     return merge_and_finish(graph, cfg, runs, dg, return_choice)
 
 
-__all__ = ["world_direction", "DirectionGraph", "translation_loss_and_grad", "canonicalize",
+__all__ = ["PairRejected", "fibonacci_sphere", "reestimate_relative", "world_direction",
+           "DirectionGraph", "translation_loss_and_grad", "canonicalize",
            "align_centers", "per_node_residuals", "multi_init_align", "TranslationL1Loss"]

@@ -36,6 +36,22 @@ def main():
     match_set, gt = synth.generate(spec)
     d = {}
     orig_mia, orig_irls = translation.multi_init_align, pipeline.irls_refine
+    orig_rr = translation.reestimate_relative
+    rr_calls = []
+    rr_seconds = []
+
+    def rr(x1, x2, rel_rotation, cfg):
+        # ref/pipeline.py:209 -- the sphere search of every candidate pair
+        try:
+            t0 = time.perf_counter()
+            t = orig_rr(x1, x2, rel_rotation, cfg)
+            rr_seconds.append(time.perf_counter() - t0)
+            rr_calls.append((np.asarray(x1), np.asarray(x2), np.asarray(rel_rotation), t, ""))
+            return t
+        except translation.PairRejected as exc:
+            rr_calls.append((np.asarray(x1), np.asarray(x2), np.asarray(rel_rotation), np.zeros(3),
+                             str(exc)))
+            raise
 
     def mia(graph, cfg, seed=0):
         t0 = time.perf_counter()
@@ -75,17 +91,54 @@ def main():
         return out, fs, rep
 
     translation.multi_init_align, pipeline.irls_refine = mia, irls
+    translation.reestimate_relative = rr
     try:
         t0 = time.perf_counter()
         scene, _ = pipeline.run_pipeline(match_set, PipelineConfig(), seed=0)
         total = time.perf_counter() - t0
     finally:
         translation.multi_init_align, pipeline.irls_refine = orig_mia, orig_irls
+        translation.reestimate_relative = orig_rr
+    # sphere-search calls: all outcomes; the points of the first 80 calls
+    keep = rr_calls[:80]
+    cfg = PipelineConfig()
+    d.update(rr_len=np.array([len(c[0]) for c in keep], dtype=np.int32),
+             rr_x1=np.concatenate([c[0] for c in keep]), rr_x2=np.concatenate([c[1] for c in keep]),
+             rr_R=np.stack([c[2] for c in keep]), rr_t=np.stack([c[3] for c in keep]),
+             rr_msg=np.array([c[4] for c in keep]),
+             rr_cfg=np.array([cfg.sphere_samples, cfg.sphere_refine_levels]),
+             rr_n_calls=np.array([len(rr_calls)]),
+             rr_n_rejected=np.array([sum(1 for c in rr_calls if c[4])]),
+             rr_ref_seconds_per_call=np.array([np.mean(rr_seconds)]))
     table = metrics.evaluate(scene.poses, gt.poses)
     d.update(gt_R=gt.poses.rotations, gt_c=gt.poses.centers,
              final_metrics=np.array([table["ATE"], table["RRA@1"], table["RTA@3"]]),
              pipeline_seconds=np.array([total]))
+    # synthetic sphere-search cases for the rejection paths: a noise-free pure
+    # rotation (flat landscape) and a small generic pair
+    rng = np.random.default_rng(11)
+    ang = 0.3
+    Rz = np.array([[np.cos(ang), -np.sin(ang), 0.0], [np.sin(ang), np.cos(ang), 0.0], [0.0, 0.0, 1.0]])
+    X = rng.uniform(-1, 1, size=(60, 3)) + np.array([0.0, 0.0, 4.0])
+    x1 = X / X[:, 2:3]
+    y = X @ Rz.T
+    x2 = y / y[:, 2:3]
+    xs = []
+    for name, (a, b, R) in {"rot": (x1, x2, Rz),
+                            "gen": (x1, (X @ Rz.T + [0.4, -0.1, 0.2]) / (X @ Rz.T + [0.4, -0.1, 0.2])[:, 2:3],
+                                    Rz)}.items():
+        try:
+            t, msg = translation.reestimate_relative(a, b, R, cfg), ""
+        except translation.PairRejected as exc:
+            t, msg = np.zeros(3), str(exc)
+        xs.append((a, b, R, t, msg))
+    d.update(rrx_x1=np.stack([c[0] for c in xs]), rrx_x2=np.stack([c[1] for c in xs]),
+             rrx_R=np.stack([c[2] for c in xs]), rrx_t=np.stack([c[3] for c in xs]),
+             rrx_msg=np.array([c[4] for c in xs]))
+    print("synthetic sphere cases:", [c[4] or "ok" for c in xs])
     np.savez_compressed(os.path.join(HERE, "golden_pipeline.npz"), **d)
+    print(f"sphere search: {len(rr_calls)} calls, {int(d['rr_n_rejected'][0])} rejected, "
+          f"{1e3 * np.mean(rr_seconds):.2f} ms per call (reference, this host)")
     print(f"pipeline {total:.1f}s: translation {d['tr_seconds'][0]:.1f}s ({len(d['tr_ei'])} edges), "
           f"irls {d['ep_seconds'][0]:.1f}s ({int(d['ep_len'].sum())} point pairs, "
           f"{len(d['ep_len'])} image pairs); ATE {table['ATE']:.3e} RRA@1 {table['RRA@1']} "

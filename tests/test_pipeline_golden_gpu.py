@@ -74,3 +74,45 @@ def test_irls_refine_on_pipeline_inputs(golden_pipeline, precision):
     for key in ("RRA@1", "RRA@3", "RTA@1", "RTA@3"):
         assert ours[key] == ref[key], (key, ours, ref)
     assert abs(ours["ATE"] - ref["ATE"]) < 1e-4, (ours, ref)
+
+
+class _SphereCfg:
+    def __init__(self, g):
+        self.sphere_samples, self.sphere_refine_levels = (int(v) for v in g["rr_cfg"])
+
+
+def test_sphere_search_on_pipeline_inputs(golden_pipeline):
+    """reestimate_relative (ref/translation.py:58-95) on the first 80 calls
+    the reference pipeline made at ref/pipeline.py:209: the same refined
+    direction.  The candidate lattices are the reference's; the mean errors
+    are fp64 sums in a different order (x2^T (E x1) per point vs the
+    reference's (M, 9) @ (9, C) product), so candidates whose errors tie to
+    ~1e-16 may swap, which shifts the refined direction by far less than the
+    input noise: within 1e-6 rad (observed 2.6e-8), most pairs bitwise."""
+    g = golden_pipeline
+    cfg = _SphereCfg(g)
+    lengths = g["rr_len"].astype(np.int64)
+    x1s, x2s = split(g["rr_x1"], lengths), split(g["rr_x2"], lengths)
+    worst, exact = 0.0, 0
+    for k in range(len(lengths)):
+        t = T.reestimate_relative(x1s[k], x2s[k], g["rr_R"][k], cfg)
+        assert g["rr_msg"][k] == ""
+        exact += int(np.array_equal(t, g["rr_t"][k]))
+        worst = max(worst, float(np.linalg.norm(t - g["rr_t"][k])))
+    print(f"sphere search: {len(lengths)} pairs, {exact} bitwise, max |dt| {worst:.2e}")
+    assert worst < 1e-6 and exact >= len(lengths) // 2
+
+
+def test_sphere_search_rejections(golden_pipeline):
+    g = golden_pipeline
+    cfg = _SphereCfg(g)
+    for k in range(len(g["rrx_msg"])):
+        msg = str(g["rrx_msg"][k])
+        if msg:
+            with pytest.raises(T.PairRejected, match=msg.split(" (")[0]):
+                T.reestimate_relative(g["rrx_x1"][k], g["rrx_x2"][k], g["rrx_R"][k], cfg)
+        else:
+            t = T.reestimate_relative(g["rrx_x1"][k], g["rrx_x2"][k], g["rrx_R"][k], cfg)
+            assert np.abs(t - g["rrx_t"][k]).max() < 1e-9
+    with pytest.raises(T.PairRejected, match="no inlier point pairs"):
+        T.reestimate_relative(np.zeros((0, 3)), np.zeros((0, 3)), np.eye(3), cfg)
