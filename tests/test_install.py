@@ -1,0 +1,38 @@
+"""install() rebinds the reference package's hot-path names (CPU: no kernel
+runs).  Needs the reference source tree, so it is skipped where it is absent
+(the GPU box)."""
+
+import importlib
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference package not present")
+def test_install_swaps_the_pipeline_call_sites():
+    sys.path.insert(0, REF)
+    try:
+        fastmap = importlib.import_module("fastmap")
+        pipeline = importlib.import_module("fastmap.pipeline")
+        ref_tr = importlib.import_module("fastmap.translation")
+        ref_epi = importlib.import_module("fastmap.epipolar")
+    except ImportError as exc:  # reference dependencies missing
+        pytest.skip(str(exc))
+    finally:
+        sys.path.remove(REF)
+    import paper_2505_04612_b200 as b200
+    from paper_2505_04612_b200 import epipolar, translation
+    saved = b200.install(fastmap)
+    try:
+        assert pipeline.irls_refine is epipolar.irls_refine          # ref/pipeline.py:248
+        assert ref_tr.multi_init_align is translation.multi_init_align  # ref/pipeline.py:233
+        assert ref_tr.reestimate_relative is translation.reestimate_relative  # :209
+        assert translation.PairRejected is ref_tr.PairRejected       # caught at :210
+        assert ref_epi.quadratic_loss_and_grad is epipolar.quadratic_loss_and_grad
+    finally:
+        for (mod, name), obj in saved.items():
+            setattr(sys.modules[mod], name, obj)
+    assert translation.PairRejected is not ref_tr.PairRejected
