@@ -341,3 +341,43 @@ def test_l1_loss_with_nonfinite_active_point_is_nan(golden_small):
     pairs[0].x1[k, 0] = np.nan
     loss, Z = E.epipolar_loss(st, pairs, mode="l1")
     assert np.isnan(loss)
+
+
+@pytest.mark.parametrize("lanes", ["4", "8", "16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_hot_point_pass_ragged_and_empty_pairs(precision, lanes, monkeypatch):
+    """Pair lengths around the 16-slot block (0, 1, 2, 15, 16, 17, 33, ...),
+    an empty pair and an all-inactive pair through the hot kernel: counts,
+    masks and L1 bit-exact / 1e-12, W as in the main parity test."""
+    monkeypatch.setenv("FM_HOT_L", lanes)
+    poses, pairs = random_scene(seed=7, n_images=6, n_points=500)
+    cuts = [0, 1, 2, 15, 16, 17, 33, 64, 65, 250]
+    for p, m in zip(pairs, cuts):
+        p.x1, p.x2, p.active = p.x1[:m].copy(), p.x2[:m].copy(), p.active[:m].copy()
+    pairs[len(cuts)].active[:] = False
+    n = len(poses.rotations)
+    st = E.AdjustmentState.from_poses(poses, list(range(n)), 2, True)
+    dev = torch.device("cuda")
+    store = PointPairStore.from_pairs(pairs, device=dev, sanitize=True)
+    o = store.order
+    ii, jj, ci, cj = E._pair_indices(st, pairs)
+    graph = PairGraph(ii[o], jj[o], ci[o], cj[o], n, 2, True, device=dev)
+    eng = E.IrlsEngine(store, graph, torch.as_tensor(st.pack(), device=dev), Cfg(),
+                       precision=precision)
+    eng._ghat()
+    th = 0.01
+    eng.point_pass(N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS, th, 1, 0)
+    torch.cuda.synchronize()
+    sp = [pairs[q] for q in o]
+    flat = O.FlatPairs.from_pairs(sp)
+    gh = O.pair_forward(st.pack(), n, ii[o], jj[o], ci[o], cj[o], True)["ghat"]
+    ref = O.point_pass(flat, gh, threshold=th)
+    P = len(sp)
+    assert np.array_equal(eng.buf.n_active[1].cpu().numpy()[:P], ref["n_active"])
+    expect = np.concatenate([flat.split(flat.active)[store.rank[k]] for k in range(P)])
+    assert np.array_equal(store.caller_masks(), expect)
+    np.testing.assert_allclose(eng.buf.l1.cpu().numpy()[:P], ref["l1"], rtol=1e-12, atol=1e-300)
+    scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
+    mom = eng.buf.mom64 if precision == "fp64" else eng.buf.mom32
+    W = E.moments_to_weights(mom.cpu().numpy()[:, :P])
+    assert np.max(np.abs(W - ref["W"]) / scale) < (3e-7 if precision == "fp64" else 2e-5)
