@@ -327,6 +327,20 @@ int fm_sphere_errors(const double* x1, const double* x2, int64_t M, const double
 int fm_depth_counts(const double* R, const double* t, const double* x1,
                     const double* x2, int64_t M, int32_t* counts_out, void* stream);
 
+/*
+ * Batched forms over n_pairs image pairs (pair k owns points
+ * [pair_off[k], pair_off[k+1]) of x1 / x2, rotation R + 9k):
+ * errors_out [k][C] with candidates dirs + k * dir_stride (dir_stride 0: one
+ * lattice for all pairs); counts_out [k][2] over the first
+ * min(M_k, max_points) points with translation t + 3k.  n_pairs <= 65535.
+ */
+int fm_sphere_errors_batch(const double* x1, const double* x2, const int64_t* pair_off,
+                           int32_t n_pairs, const double* R, const double* dirs,
+                           int64_t dir_stride, int32_t C, double* errors_out, void* stream);
+int fm_depth_counts_batch(const double* R, const double* t, const double* x1,
+                          const double* x2, const int64_t* pair_off, int32_t n_pairs,
+                          int64_t max_points, int32_t* counts_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

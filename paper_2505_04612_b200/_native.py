@@ -109,6 +109,8 @@ SIGNATURES = {
     "fm_tr_merge": (ctypes.c_int, [ctypes.POINTER(DirGraph), _P, _I32, _P, _P, _P, _SZ, _P]),
     "fm_sphere_errors": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I32, _P, _P]),
     "fm_depth_counts": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P]),
+    "fm_sphere_errors_batch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _I64, _I32, _P, _P]),
+    "fm_depth_counts_batch": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I64, _P, _P]),
 }
 
 

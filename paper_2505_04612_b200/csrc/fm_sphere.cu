@@ -24,32 +24,39 @@ namespace {
 
 constexpr int kTile = 256;  // points staged per tile
 
+// blockIdx.y = pair k: points [off[k], off[k+1]), rotation R + 9k, candidates
+// dirs + k * dir_stride (dir_stride 0: one lattice shared by all pairs),
+// errors [k][C].
 __global__ void sphere_errors_kernel(const double* __restrict__ x1, const double* __restrict__ x2,
-                                     int64_t M, const double* __restrict__ R,
-                                     const double* __restrict__ dirs, int C,
+                                     const int64_t* __restrict__ off, const double* __restrict__ Rs,
+                                     const double* __restrict__ dirs, int64_t dir_stride, int C,
                                      double* __restrict__ errors) {
   __shared__ double sx1[kTile][3];
   __shared__ double sx2[kTile][3];
+  const int k = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* R = Rs + 9 * (int64_t)k;
+  const int64_t p0 = off[k], M = off[k + 1] - off[k];
   double E[9];
   {
     double d[3] = {0.0, 0.0, 1.0};
-    if (c < C) d[0] = dirs[3 * c], d[1] = dirs[3 * c + 1], d[2] = dirs[3 * c + 2];
+    const double* dk = dirs + k * dir_stride;
+    if (c < C) d[0] = dk[3 * c], d[1] = dk[3 * c + 1], d[2] = dk[3 * c + 2];
     // [d]_x = [[0, -d2, d1], [d2, 0, -d0], [-d1, d0, 0]];  E = [d]_x R
     const double S[9] = {0.0, -d[2], d[1], d[2], 0.0, -d[0], -d[1], d[0], 0.0};
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        E[r * 3 + k] = S[r * 3 + 0] * R[0 * 3 + k] + S[r * 3 + 1] * R[1 * 3 + k] + S[r * 3 + 2] * R[2 * 3 + k];
+      for (int q = 0; q < 3; ++q)
+        E[r * 3 + q] = S[r * 3 + 0] * R[0 * 3 + q] + S[r * 3 + 1] * R[1 * 3 + q] + S[r * 3 + 2] * R[2 * 3 + q];
   }
   double acc = 0.0;
   for (int64_t base = 0; base < M; base += kTile) {
     const int n = (int)(M - base < kTile ? M - base : kTile);
     __syncthreads();
-    for (int k = threadIdx.x; k < 3 * n; k += blockDim.x) {
-      sx1[k / 3][k % 3] = x1[3 * base + k];
-      sx2[k / 3][k % 3] = x2[3 * base + k];
+    for (int q = threadIdx.x; q < 3 * n; q += blockDim.x) {
+      sx1[q / 3][q % 3] = x1[3 * (p0 + base) + q];
+      sx2[q / 3][q % 3] = x2[3 * (p0 + base) + q];
     }
     __syncthreads();
     for (int m = 0; m < n; ++m) {
@@ -60,7 +67,7 @@ __global__ void sphere_errors_kernel(const double* __restrict__ x1, const double
       acc += fabs(fma(sx2[m][0], y0, fma(sx2[m][1], y1, sx2[m][2] * y2)));
     }
   }
-  if (c < C) errors[c] = acc / (double)M;
+  if (c < C) errors[(int64_t)k * C + c] = M > 0 ? acc / (double)M : 0.0;
 }
 
 // Right singular vector of the smallest singular value of a 4x4 matrix
@@ -139,31 +146,36 @@ __device__ bool in_front(const double* R, const double* t, const double* c2, con
   return z1 > 0 && z2 > 0;
 }
 
-__global__ void depth_counts_kernel(const double* __restrict__ R, const double* __restrict__ t,
+// blockIdx.y = pair k: the first min(M_k, cap) points, rotation Rs + 9k,
+// translation ts + 3k; counts [k][2] for (t, -t).
+__global__ void depth_counts_kernel(const double* __restrict__ Rs, const double* __restrict__ ts,
                                     const double* __restrict__ x1, const double* __restrict__ x2,
-                                    int64_t M, int32_t* __restrict__ counts) {
+                                    const int64_t* __restrict__ off, int64_t cap,
+                                    int32_t* __restrict__ counts) {
+  const int k = blockIdx.y;
+  const int64_t M = min(off[k + 1] - off[k], cap), p0 = off[k];
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double Rr[9], tp[3], tn[3], cp[3], cn[3];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Rr[k] = R[k];
+  for (int q = 0; q < 9; ++q) Rr[q] = Rs[9 * (int64_t)k + q];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) tp[k] = t[k], tn[k] = -t[k];
+  for (int q = 0; q < 3; ++q) tp[q] = ts[3 * (int64_t)k + q], tn[q] = -tp[q];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {  // c2 = -R^T t
-    cp[k] = -(Rr[0 * 3 + k] * tp[0] + Rr[1 * 3 + k] * tp[1] + Rr[2 * 3 + k] * tp[2]);
-    cn[k] = -cp[k];
+  for (int q = 0; q < 3; ++q) {  // c2 = -R^T t
+    cp[q] = -(Rr[0 * 3 + q] * tp[0] + Rr[1 * 3 + q] * tp[1] + Rr[2 * 3 + q] * tp[2]);
+    cn[q] = -cp[q];
   }
   bool fp = false, fn = false;
   if (m < M) {
-    const double a[3] = {x1[3 * m], x1[3 * m + 1], x1[3 * m + 2]};
-    const double b[3] = {x2[3 * m], x2[3 * m + 1], x2[3 * m + 2]};
+    const double a[3] = {x1[3 * (p0 + m)], x1[3 * (p0 + m) + 1], x1[3 * (p0 + m) + 2]};
+    const double b[3] = {x2[3 * (p0 + m)], x2[3 * (p0 + m) + 1], x2[3 * (p0 + m) + 2]};
     fp = in_front(Rr, tp, cp, a, b);
     fn = in_front(Rr, tn, cn, a, b);
   }
   const unsigned vp = __ballot_sync(0xffffffffu, fp), vn = __ballot_sync(0xffffffffu, fn);
   if ((threadIdx.x & 31) == 0) {
-    if (vp) atomicAdd(counts, __popc(vp));
-    if (vn) atomicAdd(counts + 1, __popc(vn));
+    if (vp) atomicAdd(counts + 2 * k, __popc(vp));
+    if (vn) atomicAdd(counts + 2 * k + 1, __popc(vn));
   }
 }
 
@@ -180,8 +192,29 @@ int fm_sphere_errors(const double* x1, const double* x2, int64_t M, const double
   FM_REQUIRE(M > 0 && C >= 0, "bad sphere-search sizes (M=%lld, C=%d)", (long long)M, C);
   FM_REQUIRE(x1 && x2 && R && (dirs || !C) && (errors_out || !C), "null sphere-search pointer");
   if (C == 0) return FM_OK;
-  sphere_errors_kernel<<<(unsigned)ceil_div(C, 128), 128, 0, as_stream(stream)>>>(x1, x2, M, R, dirs,
-                                                                                 C, errors_out);
+  // one pair: offsets {0, M} in a tiny device scratch of the stream
+  int64_t* off = nullptr;
+  cudaStream_t st = as_stream(stream);
+  FM_CUDA(cudaMallocAsync(&off, 2 * sizeof(int64_t), st));
+  const int64_t h[2] = {0, M};
+  FM_CUDA(cudaMemcpyAsync(off, h, sizeof(h), cudaMemcpyHostToDevice, st));
+  sphere_errors_kernel<<<dim3((unsigned)ceil_div(C, 128), 1), 128, 0, st>>>(x1, x2, off, R, dirs, 0, C,
+                                                                            errors_out);
+  const cudaError_t le = cudaGetLastError();
+  FM_CUDA(cudaFreeAsync(off, st));
+  if (le != cudaSuccess) return cuda_fail(le, "sphere_errors_kernel", __FILE__, __LINE__);
+  return FM_OK;
+}
+
+int fm_sphere_errors_batch(const double* x1, const double* x2, const int64_t* pair_off,
+                           int32_t n_pairs, const double* R, const double* dirs,
+                           int64_t dir_stride, int32_t C, double* errors_out, void* stream) {
+  FM_REQUIRE(n_pairs >= 0 && C >= 0 && dir_stride >= 0, "bad batched sphere-search sizes");
+  if (n_pairs == 0 || C == 0) return FM_OK;
+  FM_REQUIRE(x1 && x2 && pair_off && R && dirs && errors_out, "null sphere-search pointer");
+  FM_REQUIRE(n_pairs <= 65535, "at most 65535 pairs per batch");
+  sphere_errors_kernel<<<dim3((unsigned)ceil_div(C, 128), (unsigned)n_pairs), 128, 0, as_stream(stream)>>>(
+      x1, x2, pair_off, R, dirs, dir_stride, C, errors_out);
   FM_LAUNCHED(sphere_errors_kernel);
   return FM_OK;
 }
@@ -193,7 +226,29 @@ int fm_depth_counts(const double* R, const double* t, const double* x1, const do
   FM_CUDA(cudaMemsetAsync(counts_out, 0, 2 * sizeof(int32_t), st));
   if (M == 0) return FM_OK;
   FM_REQUIRE(x1 && x2, "null depth-count points");
-  depth_counts_kernel<<<(unsigned)ceil_div(M, 128), 128, 0, st>>>(R, t, x1, x2, M, counts_out);
+  int64_t* off = nullptr;
+  FM_CUDA(cudaMallocAsync(&off, 2 * sizeof(int64_t), st));
+  const int64_t h[2] = {0, M};
+  FM_CUDA(cudaMemcpyAsync(off, h, sizeof(h), cudaMemcpyHostToDevice, st));
+  depth_counts_kernel<<<dim3((unsigned)ceil_div(M, 128), 1), 128, 0, st>>>(R, t, x1, x2, off, M, counts_out);
+  const cudaError_t le = cudaGetLastError();
+  FM_CUDA(cudaFreeAsync(off, st));
+  if (le != cudaSuccess) return cuda_fail(le, "depth_counts_kernel", __FILE__, __LINE__);
+  return FM_OK;
+}
+
+int fm_depth_counts_batch(const double* R, const double* t, const double* x1, const double* x2,
+                          const int64_t* pair_off, int32_t n_pairs, int64_t max_points,
+                          int32_t* counts_out, void* stream) {
+  FM_REQUIRE(n_pairs >= 0 && max_points >= 0 && counts_out, "bad batched depth-count arguments");
+  cudaStream_t st = as_stream(stream);
+  if (n_pairs == 0) return FM_OK;
+  FM_REQUIRE(R && t && x1 && x2 && pair_off, "null depth-count pointer");
+  FM_REQUIRE(n_pairs <= 65535, "at most 65535 pairs per batch");
+  FM_CUDA(cudaMemsetAsync(counts_out, 0, 2 * sizeof(int32_t) * (size_t)n_pairs, st));
+  if (max_points == 0) return FM_OK;
+  depth_counts_kernel<<<dim3((unsigned)ceil_div(max_points, 128), (unsigned)n_pairs), 128, 0, st>>>(
+      R, t, x1, x2, pair_off, max_points, counts_out);
   FM_LAUNCHED(depth_counts_kernel);
   return FM_OK;
 }

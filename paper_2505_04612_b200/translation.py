@@ -69,44 +69,72 @@ def reestimate_relative(x1, x2, rel_rotation, cfg):
     times on shrinking caps around the best, sign by cheirality on the first
     200 points.  Raises PairRejected for empty, flat (near-zero baseline) or
     cheirality-tied pairs, with the reference's messages."""
-    x1 = np.asarray(x1, dtype=np.float64)
-    x2 = np.asarray(x2, dtype=np.float64)
-    if len(x1) == 0:
-        raise PairRejected("no inlier point pairs")
+    out = reestimate_relative_batch([x1], [x2], [rel_rotation], cfg)[0]
+    if isinstance(out, Exception):
+        raise out
+    return out
+
+
+def reestimate_relative_batch(x1s, x2s, rel_rotations, cfg):
+    """reestimate_relative for many image pairs at once: one device launch
+    per search level for all pairs (fm_sphere_errors_batch) and one for the
+    cheirality counts (fm_depth_counts_batch).  Returns, per pair, the unit
+    direction or the PairRejected instance the single call would raise; the
+    per-pair lattices and decisions are exactly those of the single call."""
+    P = len(x1s)
+    out = [None] * P
+    x1s = [np.asarray(a, dtype=np.float64).reshape(-1, 3) for a in x1s]
+    x2s = [np.asarray(b, dtype=np.float64).reshape(-1, 3) for b in x2s]
+    live = [k for k in range(P) if len(x1s[k])]
+    for k in range(P):
+        if not len(x1s[k]):
+            out[k] = PairRejected("no inlier point pairs")
+    if not live:
+        return out
     device = N.require_cuda()
     lib = N.lib()
-    X1 = torch.as_tensor(np.ascontiguousarray(x1.reshape(-1, 3)), device=device)
-    X2 = torch.as_tensor(np.ascontiguousarray(x2.reshape(-1, 3)), device=device)
-    R = torch.as_tensor(np.ascontiguousarray(rel_rotation, dtype=np.float64), device=device)
     n = int(cfg.sphere_samples)
+    for lo in range(0, len(live), 65535):
+        ks = live[lo:lo + 65535]
+        lens = np.array([len(x1s[k]) for k in ks], dtype=np.int64)
+        off = torch.as_tensor(np.concatenate([[0], np.cumsum(lens)]), device=device)
+        X1 = torch.as_tensor(np.concatenate([x1s[k] for k in ks]), device=device)
+        X2 = torch.as_tensor(np.concatenate([x2s[k] for k in ks]), device=device)
+        R = torch.as_tensor(np.ascontiguousarray(np.stack([rel_rotations[k] for k in ks]),
+                                                 dtype=np.float64), device=device)
+        B = len(ks)
 
-    def errors(cands):
-        d = torch.as_tensor(np.ascontiguousarray(cands), device=device)
-        e = torch.empty(len(cands), dtype=torch.float64, device=device)
-        N.check(lib.fm_sphere_errors(N.ptr(X1), N.ptr(X2), len(x1), N.ptr(R), N.ptr(d), len(cands),
-                                     N.ptr(e), N.stream_handle()))
-        return e.cpu().numpy()
+        def errors(cands, stride):
+            d = torch.as_tensor(np.ascontiguousarray(cands), device=device)
+            e = torch.empty((B, n), dtype=torch.float64, device=device)
+            N.check(lib.fm_sphere_errors_batch(N.ptr(X1), N.ptr(X2), N.ptr(off), B, N.ptr(R),
+                                               N.ptr(d), stride, n, N.ptr(e), N.stream_handle()))
+            return e.cpu().numpy()
 
-    cands = fibonacci_sphere(n)
-    err = errors(cands)
-    med = float(np.median(err))
-    if med < 1e-15 or np.min(err) > 0.9 * med:
-        raise PairRejected("flat epipolar landscape (near-zero baseline)")
-    best = cands[int(np.argmin(err))]
-    radius = 2.0 * np.sqrt(4.0 * np.pi / n)
-    for _ in range(int(cfg.sphere_refine_levels)):
-        cands = _cap_samples(best, radius, n)
-        best = cands[int(np.argmin(errors(cands)))]
-        radius *= 2.0 * np.sqrt(np.pi / n)
-    m = min(len(x1), 200)
-    t = torch.as_tensor(np.ascontiguousarray(best), device=device)
-    counts = torch.empty(2, dtype=torch.int32, device=device)
-    N.check(lib.fm_depth_counts(N.ptr(R), N.ptr(t), N.ptr(X1), N.ptr(X2), m, N.ptr(counts),
-                                N.stream_handle()))
-    pos, neg = (int(v) for v in counts.cpu().numpy())
-    if pos == neg:
-        raise PairRejected("cheirality tie")
-    return best if pos > neg else -best
+        lattice = fibonacci_sphere(n)
+        err = errors(lattice, 0)
+        med = np.median(err, axis=1)
+        flat = (med < 1e-15) | (np.min(err, axis=1) > 0.9 * med)
+        best = lattice[np.argmin(err, axis=1)]
+        radius = 2.0 * np.sqrt(4.0 * np.pi / n)
+        for _ in range(int(cfg.sphere_refine_levels)):
+            cands = np.stack([_cap_samples(best[q], radius, n) for q in range(B)])
+            e = errors(cands, 3 * n)
+            best = cands[np.arange(B), np.argmin(e, axis=1)]
+            radius *= 2.0 * np.sqrt(np.pi / n)
+        t = torch.as_tensor(np.ascontiguousarray(best), device=device)
+        counts = torch.empty((B, 2), dtype=torch.int32, device=device)
+        N.check(lib.fm_depth_counts_batch(N.ptr(R), N.ptr(t), N.ptr(X1), N.ptr(X2), N.ptr(off), B,
+                                          200, N.ptr(counts), N.stream_handle()))
+        counts = counts.cpu().numpy()
+        for q, k in enumerate(ks):
+            if flat[q]:
+                out[k] = PairRejected("flat epipolar landscape (near-zero baseline)")
+            elif counts[q, 0] == counts[q, 1]:
+                out[k] = PairRejected("cheirality tie")
+            else:
+                out[k] = best[q] if counts[q, 0] > counts[q, 1] else -best[q]
+    return out
 
 
 def world_direction(t_ij, R_j):
@@ -268,6 +296,7 @@ def multi_init_align(graph, cfg, seed=0, return_choice=False):
     return merge_and_finish(graph, cfg, runs, dg, return_choice)
 
 
-__all__ = ["PairRejected", "fibonacci_sphere", "reestimate_relative", "world_direction",
+__all__ = ["PairRejected", "fibonacci_sphere", "reestimate_relative", "reestimate_relative_batch",
+           "world_direction",
            "DirectionGraph", "translation_loss_and_grad", "canonicalize",
            "align_centers", "per_node_residuals", "multi_init_align", "TranslationL1Loss"]

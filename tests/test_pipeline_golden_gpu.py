@@ -116,3 +116,26 @@ def test_sphere_search_rejections(golden_pipeline):
             assert np.abs(t - g["rrx_t"][k]).max() < 1e-9
     with pytest.raises(T.PairRejected, match="no inlier point pairs"):
         T.reestimate_relative(np.zeros((0, 3)), np.zeros((0, 3)), np.eye(3), cfg)
+
+
+def test_sphere_search_batch_equals_single(golden_pipeline):
+    """The batched search (one launch per level for all pairs) returns exactly
+    the single-call results, rejections included."""
+    g = golden_pipeline
+    cfg = _SphereCfg(g)
+    lengths = g["rr_len"].astype(np.int64)
+    x1s = list(split(g["rr_x1"], lengths)) + [g["rrx_x1"][k] for k in range(len(g["rrx_msg"]))]
+    x2s = list(split(g["rr_x2"], lengths)) + [g["rrx_x2"][k] for k in range(len(g["rrx_msg"]))]
+    Rs = list(g["rr_R"]) + list(g["rrx_R"])
+    x1s.append(np.zeros((0, 3)))
+    x2s.append(np.zeros((0, 3)))
+    Rs.append(np.eye(3))
+    got = T.reestimate_relative_batch(x1s, x2s, Rs, cfg)
+    for k, r in enumerate(got):
+        try:
+            one = T.reestimate_relative(x1s[k], x2s[k], Rs[k], cfg)
+        except T.PairRejected as exc:
+            assert isinstance(r, T.PairRejected) and str(r) == str(exc)
+            continue
+        assert np.array_equal(r, one)
+    assert np.array_equal(np.stack(got[:len(lengths)]), g["rr_t"])
