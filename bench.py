@@ -246,8 +246,15 @@ def run_ours(args, spec, world, rank, local):
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    spec_r = scenes.SceneSpec(**{**spec.__dict__, "seed": spec.seed + rank})
-    scene = scenes.generate(spec_r, device)
+    if args.strong:
+        # strong scaling: the config's image pairs split into contiguous
+        # ranges over the ranks; each rank generates only its own range
+        lo, hi = spec.n_pairs * rank // world, spec.n_pairs * (rank + 1) // world
+        scene = scenes.generate(spec, device, pair_slice=slice(lo, hi))
+    else:
+        # weak scaling: one config-sized shard per rank (distinct seeds)
+        spec_r = scenes.SceneSpec(**{**spec.__dict__, "seed": spec.seed + rank})
+        scene = scenes.generate(spec_r, device)
     store = scenes.device_store(scene, device)
     graph, ids = scenes.device_graph(scene, device)
     params = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
@@ -311,7 +318,10 @@ def run_ours(args, spec, world, rank, local):
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_step = float(t_max.item())
-    value = world * Z / (ms_step * 1e-3)
+    Z_all = torch.tensor([Z], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(Z_all)
+    value = float(Z_all.item()) / (ms_step * 1e-3)
 
     # roofline of the dominant kernel (the pass) from the same events
     bytes_launch = BYTES_PER_POINT * Z + BYTES_PER_PAIR * P
@@ -398,14 +408,16 @@ def run_ours(args, spec, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
             "dtype": ("f64 (residual, W moments, prune decisions) on f32 coordinates"
                       if args.precision == "fp64" else
                       "f32 W moments (shifted model) + f64 residual on f32 coordinates"),
             "data": "synthetic (device-generated ring scene, random-perturbed poses)",
-            "config": {"workload": f"{args.config.upper()}: {spec.n_images} images, {P} image pairs, "
-                                   f"{Z} point pairs per GPU (band {spec.band}, {spec.points_per_pair}"
-                                   f" pts/pair)",
+            "config": {"workload": f"{args.config.upper()}: {spec.n_images} images, "
+                                   + (f"{spec.n_pairs} image pairs / {spec.n_pairs * spec.points_per_pair} "
+                                      f"point pairs split over {world} GPU(s)" if args.strong else
+                                      f"{P} image pairs, {Z} point pairs per GPU")
+                                   + f" (band {spec.band}, {spec.points_per_pair} pts/pair)",
                        "pass": "fused L1 + prune + IRLS W moments (irls_refine rounds 1-2 pass)",
                        "precision": args.precision,
                        "l2": "flushed between steps (256 MB write + 256 MB read, outside the events) and inputs > L2",
@@ -523,6 +535,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"])
+    ap.add_argument("--strong", action="store_true",
+                    help="split the config's image pairs over the ranks (strong scaling; "
+                         "default: one config-sized shard per rank)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-optimize", action="store_true")
     ap.add_argument("--precision", default="fp32", choices=["fp64", "fp32"],
