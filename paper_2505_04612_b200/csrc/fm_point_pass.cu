@@ -71,7 +71,6 @@ struct PartialBufs {
   double* s0;  // [n_items]
   double* l1;  // [n_items]
   int64_t cap; // items the buffers hold
-  unsigned int* ctr;  // [2] work counters of the persistent launch (zero at rest), or NULL
 };
 
 #ifdef FM_HOT_TRACE
@@ -601,34 +600,6 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
                            (int64_t)blockIdx.x * kGrpWarps + (threadIdx.x >> 5), 0);
 }
 
-// Persistent variant: one launch of resident blocks; every warp takes the
-// next item group from a global counter until none is left, so warps the
-// scheduler starves simply process fewer groups and the launch ends ~one
-// group after the queue drains.  counters[0] = next group, counters[1] =
-// finished warps; the last warp to finish re-zeroes both (zero at rest).
-template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
-point_pass_hot_dyn(const fm_point_store s, const double* __restrict__ ghat, const double thr,
-                   const int32_t* __restrict__ prev_active, const fm_pass_out out,
-                   const PartialBufs part, unsigned int* __restrict__ counters, const int64_t n_groups) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned int grp = 0;
-    if (lane == 0) grp = atomicAdd(counters, 1u);
-    grp = __shfl_sync(0xffffffffu, grp, 0);
-    if ((int64_t)grp >= n_groups) break;
-    hot_body<MODE, MOM64, L>(s, ghat, thr, prev_active, out, part, grp, 0);
-    __syncwarp();
-  }
-  if (lane == 0) {
-    const unsigned int total = gridDim.x * (blockDim.x >> 5);
-    if (atomicAdd(counters + 1, 1u) == total - 1) {
-      counters[0] = 0;
-      counters[1] = 0;
-    }
-  }
-}
-
 // Tail-shortened launch: items [0, n1) with L1 lanes per item (the most
 // efficient width, in whole waves), the rest with L2 > L1 lanes per item in
 // the blocks the scheduler dispatches last -- a tail item then takes
@@ -894,30 +865,6 @@ int launch_hot_mixed(const fm_point_store& s, double thr, const double* ghat,
   return FM_OK;
 }
 
-template <unsigned MODE, bool MOM64, int L>
-int launch_hot_dyn(const fm_point_store& s, double thr, const double* ghat,
-                   const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
-                   cudaStream_t stream, unsigned int* counters, int bps) {
-  const size_t smem = kGrpWarps * sizeof(LaneRing);
-  static bool attr = false;
-  if (!attr) {
-    FM_CUDA(cudaFuncSetAttribute(point_pass_hot_dyn<MODE, MOM64, L>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  const int64_t groups = ceil_div(s.n_items, 32 / L);
-  const int64_t grid = std::min<int64_t>((int64_t)bps * sm_count(), ceil_div(groups, kGrpWarps));
-  point_pass_hot_dyn<MODE, MOM64, L><<<(unsigned)grid, kGrpWarps * 32, smem, stream>>>(
-      s, ghat, thr, prev_active, out, part, counters, groups);
-  FM_LAUNCHED(point_pass_hot_dyn);
-  if (s.n_items > s.n_pairs) {
-    combine_kernel<MOM64, MODE><<<(unsigned)ceil_div(s.n_pairs, 128), 128, 0, stream>>>(s, out, part,
-                                                                                        !MOM64);
-    FM_LAUNCHED(combine_kernel);
-  }
-  return FM_OK;
-}
-
 // Lanes per item L in {4, 8, 16}: blocks are one-shot, so the last wave of
 // a launch is partially filled.  Score each L by the filled fraction of its
 // waves and a per-item reduction cost (log2(L) transpose-reduce levels plus a
@@ -959,18 +906,11 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     const bool mix = env_mix ? atoi(env_mix) != 0 : true;
     // (moment passes only: the light L1 pass runs faster with one width)
     constexpr bool kMomPass = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
-    if (kMomPass && mix && !getenv("FM_HOT_L") && !getenv("FM_HOT_DYN") && n1 > 0 &&
+    if (kMomPass && mix && !getenv("FM_HOT_L") && n1 > 0 &&
         s.n_items > n1 && mean_blk >= 8)
       return launch_hot_mixed<MODE, MOM64, 4, 16>(s, thr, ghat, prev_active, out, part, stream, n1);
   }
   if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
-  if (const char* env = getenv("FM_HOT_DYN")) {
-    if (atoi(env) && part.ctr) {
-      if (pick == 16) return launch_hot_dyn<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[2]);
-      if (pick == 8) return launch_hot_dyn<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[1]);
-      return launch_hot_dyn<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream, part.ctr, bps[0]);
-    }
-  }
   if (pick == 16) return launch_hot_l<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream);
   if (pick == 8) return launch_hot_l<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream);
   return launch_hot_l<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);
@@ -1107,14 +1047,11 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE(f64 ? out->mom64 != nullptr : out->mom32 != nullptr, "moment output missing");
     if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
   }
-  PartialBufs part{nullptr, nullptr, nullptr, 0, nullptr};
+  PartialBufs part{nullptr, nullptr, nullptr, 0};
   cudaStream_t st = as_stream(stream);
   fm_point_store s2 = s;  // with item descriptors
   {
     Scratch sc(scratch, scratch_bytes);
-    // first 256 bytes: the persistent launch's work counters (the caller
-    // zeroes the scratch once; every launch leaves them zero)
-    if (scratch) part.ctr = sc.take<unsigned int>(2);
     if (s.n_items > s.n_pairs) {
       part.red = sc.take<double>((size_t)s.n_items * kNumRed);
       part.s0 = sc.take<double>((size_t)s.n_items);

@@ -169,8 +169,7 @@ class PointPairStore:
 
     def scratch(self):
         nbytes = N.lib().fm_point_pass_scratch_bytes(ctypes.byref(self.struct()))
-        # zeroed once: the persistent pass keeps its work counters at zero between launches
-        return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------- masks
     def active_bits(self):
