@@ -50,7 +50,8 @@ typedef enum fm_status {
   FM_ERR_ROT6D_COLLINEAR = 6,   /* ref/optim.py:55-56         -> ValueError            */
   FM_ERR_NO_ACTIVE = 7,         /* ref/epipolar.py:147-148    -> ValueError            */
   FM_ERR_ALL_PRUNED = 8,        /* ref/epipolar.py:289-290    -> ValueError            */
-  FM_ERR_NONFINITE_TRANSLATION = 9 /* ref/translation.py:149-150 -> FloatingPointError */
+  FM_ERR_NONFINITE_TRANSLATION = 9, /* ref/translation.py:149-150 -> FloatingPointError */
+  FM_ERR_NONFINITE_ROTATION = 10 /* ref/rotation.py:218-219    -> FloatingPointError   */
 } fm_status;
 
 /* ------------------------------------------------------------------------ */
@@ -340,6 +341,47 @@ int fm_sphere_errors_batch(const double* x1, const double* x2, const int64_t* pa
 int fm_depth_counts_batch(const double* R, const double* t, const double* x1,
                           const double* x2, const int64_t* pair_off, int32_t n_pairs,
                           int64_t max_points, int32_t* counts_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* rotation refinement (SURVEY 8f "next" #3)                                 */
+/* ------------------------------------------------------------------------ */
+/*
+ * Relative-rotation graph over dense node indices: edge e maps frame
+ * edge_i[e] to frame edge_j[e] by rel[e] (row-major 3x3); node_inc lists
+ * (e << 1) | side per node (side 1: the node is the edge's j), CSR node_off.
+ */
+typedef struct fm_rot_graph {
+  int32_t n_nodes;
+  int64_t n_edges;
+  const int32_t* edge_i;
+  const int32_t* edge_j;
+  const double* rel;        /* [n_edges][9] */
+  const int32_t* node_off;  /* [n_nodes+1] */
+  const int32_t* node_inc;
+} fm_rot_graph;
+
+size_t fm_rot_scratch_bytes(int32_t n_nodes, int64_t n_edges);
+
+/* Mean geodesic loss over edges and its gradient w.r.t. the 6D parameters
+ * (ref/rotation.py:162-194).  params6 [n][6]; loss_out: one device double;
+ * grad_out [n][6]. */
+int fm_rot_loss_grad(const fm_rot_graph* g, const double* params6, double* loss_out,
+                     double* grad_out, int32_t* flag, void* scratch, size_t scratch_bytes,
+                     void* stream);
+
+/*
+ * Adam descent of the mean geodesic loss with the reference's best-iterate
+ * and early-stopping rules (ref/rotation.py:197-230): up to max_steps steps,
+ * stopping after a loss < 1e-12 or a relative change < 1e-9 over 100 steps.
+ * params6 [n][6]: in = initial, out = the best iterate; history_out
+ * [max_steps] losses; *steps_out (host int) = losses recorded.  Runs on the
+ * stream in CUDA-graph chunks and synchronises once per chunk to test the
+ * stop condition.
+ */
+int fm_rot_refine(const fm_rot_graph* g, double* params6, int32_t max_steps, double lr,
+                  double beta1, double beta2, double eps, double* history_out,
+                  int32_t* steps_out, int32_t* flag, void* scratch, size_t scratch_bytes,
+                  void* stream);
 
 #ifdef __cplusplus
 }

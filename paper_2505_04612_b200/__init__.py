@@ -50,6 +50,11 @@ def install(fastmap_module=None):
     for name in ("translation_loss_and_grad", "canonicalize", "align_centers",
                  "per_node_residuals", "multi_init_align", "reestimate_relative"):
         swap(ref_tr, name, getattr(translation, name))
+    # ref/pipeline.py:170 calls rotation.refine_rotations through the module
+    ref_rot = importlib.import_module(fm.__name__ + ".rotation")
+    from . import rotation
+    for name in ("rotation_loss_and_grad", "refine_rotations"):
+        swap(ref_rot, name, getattr(rotation, name))
     # raise the reference's PairRejected, which ref/pipeline.py:210 catches
     swap(translation, "PairRejected", ref_tr.PairRejected)
     for name in ("rot6d_to_matrix", "rot6d_jacobian"):

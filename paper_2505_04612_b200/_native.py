@@ -25,6 +25,7 @@ FM_ERR_ROT6D_COLLINEAR = 6
 FM_ERR_NO_ACTIVE = 7
 FM_ERR_ALL_PRUNED = 8
 FM_ERR_NONFINITE_TRANSLATION = 9
+FM_ERR_NONFINITE_ROTATION = 10
 
 FM_PASS_PRUNE = 1
 FM_PASS_L1 = 2
@@ -68,6 +69,11 @@ class PairGraph(ctypes.Structure):
                 ("cam_chunk_lo", _P), ("cam_chunk_cam", _P), ("cam_chunk_off", _P)]
 
 
+class RotGraph(ctypes.Structure):
+    _fields_ = [("n_nodes", _I32), ("n_edges", _I64), ("edge_i", _P), ("edge_j", _P), ("rel", _P),
+                ("node_off", _P), ("node_inc", _P)]
+
+
 class QuadModel(ctypes.Structure):
     _fields_ = [("kind", _I32), ("mom32", _P), ("vgrad", _P), ("s0", _P), ("ghat0", _P),
                 ("w81", _P), ("mom64", _P)]
@@ -108,6 +114,11 @@ SIGNATURES = {
     "fm_tr_node_residuals": (ctypes.c_int, [ctypes.POINTER(DirGraph), _P, _I32, _P, _P]),
     "fm_tr_merge": (ctypes.c_int, [ctypes.POINTER(DirGraph), _P, _I32, _P, _P, _P, _SZ, _P]),
     "fm_sphere_errors": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I32, _P, _P]),
+    "fm_rot_scratch_bytes": (_SZ, [_I32, _I64]),
+    "fm_rot_loss_grad": (ctypes.c_int, [ctypes.POINTER(RotGraph), _P, _P, _P, _P, _P, _SZ, _P]),
+    "fm_rot_refine": (ctypes.c_int, [ctypes.POINTER(RotGraph), _P, _I32, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, _P,
+                                     ctypes.POINTER(_I32), _P, _P, _SZ, _P]),
     "fm_depth_counts": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P]),
     "fm_sphere_errors_batch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _I64, _I32, _P, _P]),
     "fm_depth_counts_batch": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I64, _P, _P]),
@@ -181,6 +192,8 @@ def raise_flag(code, context="epipolar"):
         raise FloatingPointError("non-finite epipolar loss")
     if code == FM_ERR_NONFINITE_TRANSLATION:
         raise FloatingPointError("non-finite translation loss")
+    if code == FM_ERR_NONFINITE_ROTATION:
+        raise FloatingPointError("non-finite rotation loss")
     if code == FM_ERR_NONFINITE_GRAD:
         raise FloatingPointError("non-finite gradients")
     if code == FM_ERR_ROT6D_ZERO:

@@ -28,3 +28,8 @@ def golden_c1():
 @pytest.fixture(scope="session")
 def golden_pipeline():
     return dict(np.load(os.path.join(GOLDEN, "golden_pipeline.npz")))
+
+
+@pytest.fixture(scope="session")
+def golden_rotation():
+    return dict(np.load(os.path.join(GOLDEN, "golden_rotation.npz")))

@@ -19,12 +19,13 @@ def test_install_swaps_the_pipeline_call_sites():
         pipeline = importlib.import_module("fastmap.pipeline")
         ref_tr = importlib.import_module("fastmap.translation")
         ref_epi = importlib.import_module("fastmap.epipolar")
+        ref_rot = importlib.import_module("fastmap.rotation")
     except ImportError as exc:  # reference dependencies missing
         pytest.skip(str(exc))
     finally:
         sys.path.remove(REF)
     import paper_2505_04612_b200 as b200
-    from paper_2505_04612_b200 import epipolar, translation
+    from paper_2505_04612_b200 import epipolar, rotation, translation
     saved = b200.install(fastmap)
     try:
         assert pipeline.irls_refine is epipolar.irls_refine          # ref/pipeline.py:248
@@ -32,6 +33,7 @@ def test_install_swaps_the_pipeline_call_sites():
         assert ref_tr.reestimate_relative is translation.reestimate_relative  # :209
         assert translation.PairRejected is ref_tr.PairRejected       # caught at :210
         assert ref_epi.quadratic_loss_and_grad is epipolar.quadratic_loss_and_grad
+        assert ref_rot.refine_rotations is rotation.refine_rotations     # ref/pipeline.py:170
     finally:
         for (mod, name), obj in saved.items():
             setattr(sys.modules[mod], name, obj)
