@@ -210,6 +210,7 @@ struct HotAcc {
   float2 V0, V1, V2, V3;      // (v00,v01) (v10,v11) (v20,v21) (v02,v12)
   float v22, s0f;
   double l1;
+  float l1f;
   int cnt;
 
   __device__ __forceinline__ void zero() {
@@ -220,6 +221,7 @@ struct HotAcc {
     V0 = V1 = V2 = V3 = f2(0.f);
     v22 = s0f = 0.f;
     l1 = 0.0;
+    l1f = 0.f;
     cnt = 0;
   }
 
@@ -235,13 +237,16 @@ struct HotAcc {
     const double r = fma(C, y0, fma(D, y1, y2));
     const double ar = fabs(r);
     const bool keep = (kPrune && !FM_HOT_NOLOAD) ? (act & (ar <= thr)) : act;
-    if (kL1) l1 += act ? ar : 0.0;
+    // fp32 moment passes sum L1 in fp32 from the rounded residual (per-lane
+    // partials of ~10^2 terms, relative error ~1e-6; fp64 across lanes)
+    const float rf = (float)r;
+    if (kL1 && kMom && !MOM64) l1f += act ? fabsf(rf) : 0.f;
+    else if (kL1) l1 += act ? ar : 0.0;
     if (!kMom) return keep;
     // IRLS weight 1/max(|r|, 1e-6) (ref/epipolar.py:58); the opaque AND (not a
     // select) keeps the reciprocal out of a per-point branch.  Coordinates of
     // every slot are finite (store builders zero and deactivate non-finite
     // points), so w = +0 removes a dropped point exactly.
-    const float rf = (float)r;
     const float w = and_mask(rcp_approx(fmaxf(fabsf(rf), 1e-6f)), keep ? 0xffffffffu : 0u);
     if (MOM64) {
       const double wd = w;
@@ -424,22 +429,24 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
     // pruned, weights are +0 (its stale ring bytes are finite)
     const int pos = half0 + kBlkSlots * S * it;  // block's first bit, relative to word lo/32
     const uint32_t blk = (S * it + sg < nblk) ? (FM_HOT_NOLOAD ? 0xffffu : lds32(ring_m + st_read * kStageM) >> (pos & 31)) : 0u;
-    uint32_t cleared = 0;
+    // this lane's points: slots 2h, 2h+1 (chunk 0) and 2h+8, 2h+9 (chunk 1),
+    // i.e. bits 0, 1, 8, 9 of bh
+    const uint32_t bh = blk >> (2 * h);
+    uint32_t kept = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int c2 = 2 * h + 8 * j;  // first slot of the chunk within the block
-      const unsigned bits = (blk >> c2) & 3u;
       const float4 x1 = lds128(ring_c + st_read * kStageC + j * kChunkB);
       const float4 x2 = lds128(ring_c + st_read * kStageC + (2 + j) * kChunkB);
-      unsigned keep = (unsigned)acc.point(G, x1.x, x1.y, x2.x, x2.y, bits & 1u, thr);
-      keep |= (unsigned)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bits >> 1) & 1u, thr) << 1;
-      acc.cnt += __popc(keep);
-      if (kPrune) cleared |= (bits & ~keep) << c2;
+      kept |= (uint32_t)acc.point(G, x1.x, x1.y, x2.x, x2.y, (bh >> (8 * j)) & 1u, thr) << (8 * j);
+      kept |= (uint32_t)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bh >> (8 * j + 1)) & 1u, thr) << (8 * j + 1);
     }
+    acc.cnt += __popc(kept);
+    const uint32_t cleared = kPrune ? ((bh & 0x303u) & ~kept) << (2 * h) : 0u;
     if (kPrune && cleared) atomicAnd(mwb_w + (pos >> 5), ~(cleared << (pos & 31)));
     st_read = st_read + 1 == kRing ? 0 : st_read + 1;
   }
   cp_async_wait<0>();
+  if (kL1 && kMom && !MOM64) acc.l1 = acc.l1f;
 #ifdef FM_HOT_TRACE
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < 16384) {

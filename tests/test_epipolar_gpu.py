@@ -128,7 +128,9 @@ def test_hot_point_pass_matches_oracle(chunk, precision, lanes, monkeypatch):
     masks = store.caller_masks()
     expect = np.concatenate([flat.split(flat.active)[store.rank[k]] for k in range(P)])
     assert np.array_equal(masks, expect)
-    np.testing.assert_allclose(eng.buf.l1.cpu().numpy()[:P], ref["l1"], rtol=1e-12, atol=1e-300)
+    # fp32 mode sums L1 per lane in fp32 (HotAcc::point)
+    np.testing.assert_allclose(eng.buf.l1.cpu().numpy()[:P], ref["l1"],
+                               rtol=1e-12 if precision == "fp64" else 1e-5, atol=1e-300)
     scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
     if precision == "fp64":
         W = E.moments_to_weights(eng.buf.mom64.cpu().numpy()[:, :P])
@@ -376,7 +378,9 @@ def test_hot_point_pass_ragged_and_empty_pairs(precision, lanes, monkeypatch):
     assert np.array_equal(eng.buf.n_active[1].cpu().numpy()[:P], ref["n_active"])
     expect = np.concatenate([flat.split(flat.active)[store.rank[k]] for k in range(P)])
     assert np.array_equal(store.caller_masks(), expect)
-    np.testing.assert_allclose(eng.buf.l1.cpu().numpy()[:P], ref["l1"], rtol=1e-12, atol=1e-300)
+    # fp32 mode sums L1 per lane in fp32 (HotAcc::point)
+    np.testing.assert_allclose(eng.buf.l1.cpu().numpy()[:P], ref["l1"],
+                               rtol=1e-12 if precision == "fp64" else 1e-5, atol=1e-300)
     scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
     mom = eng.buf.mom64 if precision == "fp64" else eng.buf.mom32
     W = E.moments_to_weights(mom.cpu().numpy()[:, :P])
