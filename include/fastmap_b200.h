@@ -383,6 +383,24 @@ int fm_rot_refine(const fm_rot_graph* g, double* params6, int32_t max_steps, dou
                   int32_t* steps_out, int32_t* flag, void* scratch, size_t scratch_bytes,
                   void* stream);
 
+/*
+ * Distortion candidate scoring (ref/distortion.py:90-126): for every job =
+ * one (candidate alpha, image pair) with M >= 8 undistorted, scaled point
+ * pairs p1/p2 [n_points][2] fp64 (rows [job_off[k], job_off[k+1])), the
+ * robust fundamental-matrix fit of ref/twoview.py:58-104 (LMedS over the
+ * reference's 64 seeded 8-point samples when M >= 16: sample_idx +
+ * sample_off[k] holds them as [64][8] int32, sample_off[k] = -1 below 16)
+ * and _refit_on_inliers (:48-55), then err_sum[k] = sum |x2^T F x1| and
+ * n_err[k] = M -- or n_err[k] = 0 when a fit is degenerate (the reference
+ * raises DegenerateGeometryError and score_alpha skips the pair).
+ * Replaces the per-pair body of score_alpha (ref/distortion.py:107-124).
+ */
+size_t fm_fund_scratch_bytes(int64_t n_points);
+int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, const double* p2,
+                  const int32_t* sample_idx, const int64_t* sample_off, double* err_sum,
+                  int32_t* n_err, void* scratch, size_t scratch_bytes, int64_t n_points,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,4 +59,11 @@ def install(fastmap_module=None):
     swap(translation, "PairRejected", ref_tr.PairRejected)
     for name in ("rot6d_to_matrix", "rot6d_jacobian"):
         swap(ref_opt, name, getattr(optim, name))
+    # ref/pipeline.py:94 -> schedule_cameras -> search_alpha (module globals)
+    ref_dist = importlib.import_module(fm.__name__ + ".distortion")
+    ref_two = importlib.import_module(fm.__name__ + ".twoview")
+    from . import distortion
+    for name in ("score_alpha", "search_alpha"):
+        swap(ref_dist, name, getattr(distortion, name))
+    swap(distortion, "DegenerateGeometryError", ref_two.DegenerateGeometryError)
     return saved

@@ -1,0 +1,80 @@
+"""Golden vectors of the distortion candidate search (ref/distortion.py:90-193,
+SURVEY 8f "next" #4) from the REFERENCE implementation (read-only import):
+the synthetic match sets of the reference's own distortion tests
+(pkg/tests/test_distortion.py:43-80), the scores score_alpha gives every
+candidate of every search level, the search_alpha result, and the
+schedule_cameras result of the two-camera scene.  Also a subset-sized pair
+(M < 16, the non-LMedS branch) scored on its own.
+
+    python tests/golden/make_distortion_golden.py      (a minute; not run by pytest)
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from fastmap import distortion, synth  # noqa: E402
+from fastmap.config import PipelineConfig  # noqa: E402
+from fastmap.model import GeometryClass  # noqa: E402
+
+
+def pack(prefix, ms, out):
+    out[prefix + "img"] = np.array([[im.camera_id, im.width, im.height] for im in ms.images],
+                                   dtype=np.int64)
+    out[prefix + "kp_len"] = np.array([len(k) for k in ms.keypoints], dtype=np.int64)
+    out[prefix + "kp"] = np.concatenate(ms.keypoints)
+    out[prefix + "pair_ij"] = np.array([[p.i, p.j] for p in ms.pairs], dtype=np.int64)
+    out[prefix + "pair_len"] = np.array([len(p.correspondences) for p in ms.pairs], dtype=np.int64)
+    out[prefix + "corr"] = np.concatenate([p.correspondences for p in ms.pairs]).astype(np.int64)
+
+
+def main():
+    out = {}
+    cfg = PipelineConfig()
+    # scene A: single camera, alpha = -0.2 (test_recovers_alpha_on_synthetic_scene)
+    ms, _ = synth.generate(synth.SynthSpec(n_images=8, n_points=200, fov_deg=70.0, alpha=-0.2,
+                                           seed=0))
+    pack("a_", ms, out)
+    out["a_homography"] = np.array([p.geometry_class is GeometryClass.HOMOGRAPHY for p in ms.pairs])
+    pairs = distortion.ready_fundamental_pairs(ms)
+    ready = [ms.pairs.index(p) for p in pairs]
+    out["a_ready"] = np.array(ready, dtype=np.int64)
+    lo, hi, n = cfg.distortion_min, cfg.distortion_max, cfg.distortion_samples_per_level
+    cands, scores = [], []
+    t0 = time.perf_counter()
+    for _ in range(cfg.distortion_levels):
+        c = np.linspace(lo, hi, n)
+        s = np.array([distortion.score_alpha(a, ms, pairs) for a in c])
+        k = int(np.argmin(s))
+        cands.append(c)
+        scores.append(s)
+        lo, hi = c[max(k - 1, 0)], c[min(k + 1, n - 1)]
+    out["a_ref_seconds"] = np.array(time.perf_counter() - t0)
+    out["a_cands"] = np.stack(cands)
+    out["a_scores"] = np.stack(scores)
+    out["a_alpha"] = np.array(distortion.search_alpha(ms, pairs, cfg))
+    # small pairs: every ready pair cut to its first 12 correspondences (M < 16)
+    small = [type(p)(p.i, p.j, p.geometry_class, p.correspondences[:12]) for p in pairs]
+    out["a_small_scores"] = np.array([distortion.score_alpha(a, ms, small)
+                                      for a in (-0.3, 0.0, 0.25)])
+    # scene B: two cameras (test_multi_camera_scheduling)
+    ms_b, _ = synth.generate(synth.SynthSpec(n_images=10, n_points=250, seed=3, n_cameras=2,
+                                             alpha=(-0.15, 0.1)))
+    pack("b_", ms_b, out)
+    out["b_homography"] = np.array([p.geometry_class is GeometryClass.HOMOGRAPHY for p in ms_b.pairs])
+    alphas, unest = distortion.schedule_cameras(ms_b, cfg)
+    out["b_alphas"] = np.array([alphas[c] for c in sorted(alphas)])
+    out["b_unestimated"] = np.array(unest, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "golden_distortion.npz"), **out)
+    print({k: v.shape for k, v in out.items()})
+    print("scene A alpha", out["a_alpha"], "ref search seconds", out["a_ref_seconds"],
+          "scene B alphas", out["b_alphas"])
+
+
+if __name__ == "__main__":
+    main()

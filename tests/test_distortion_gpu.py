@@ -1,0 +1,94 @@
+"""Distortion candidate search (SURVEY 8f "next" #4) against the reference's
+own outputs recorded in tests/golden/golden_distortion.npz
+(make_distortion_golden.py): every candidate score of the three search
+levels, the searched alpha, the M < 16 (non-LMedS) branch, and the
+two-camera schedule of pkg/tests/test_distortion.py:70-80."""
+
+import os
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_distortion.npz")
+
+
+def _match_set(g, p):
+    img = g[p + "img"]
+    kp = np.split(g[p + "kp"], np.cumsum(g[p + "kp_len"])[:-1])
+    corr = np.split(g[p + "corr"], np.cumsum(g[p + "pair_len"])[:-1])
+    homog = g[p + "homography"]
+    images = [SimpleNamespace(camera_id=int(c), width=int(w), height=int(h)) for c, w, h in img]
+    pairs = [SimpleNamespace(i=int(i), j=int(j), correspondences=c,
+                             geometry_class=SimpleNamespace(name="HOMOGRAPHY" if h else "FUNDAMENTAL"))
+             for (i, j), c, h in zip(g[p + "pair_ij"], corr, homog)]
+    return SimpleNamespace(images=images, keypoints=kp, pairs=pairs)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+def _cfg():
+    from paper_2505_04612_b200.config import HotPathConfig
+    c = HotPathConfig()
+    for k, v in dict(distortion_levels=3, distortion_samples_per_level=10, distortion_min=-1.0,
+                     distortion_max=1.0, distortion_max_pairs=120).items():
+        setattr(c, k, v)
+    return c
+
+
+def test_candidate_scores_match_reference(golden):
+    """All 30 candidate scores of the reference's 3-level search (LMedS
+    branch, M = 200): the fit is the same algorithm with the same seeded
+    samples; only summation orders and the eigen-solver differ."""
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "a_")
+    pairs = [ms.pairs[k] for k in golden["a_ready"]]
+    assert [id(p) for p in D.ready_fundamental_pairs(ms)] == [id(p) for p in pairs]
+    for cands, ref in zip(golden["a_cands"], golden["a_scores"]):
+        got = D.score_alpha_batch(cands, ms, pairs)
+        np.testing.assert_allclose(got, ref, rtol=1e-8)
+        assert int(np.argmin(got)) == int(np.argmin(ref))
+
+
+def test_search_alpha_matches_reference(golden):
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "a_")
+    pairs = [ms.pairs[k] for k in golden["a_ready"]]
+    assert D.search_alpha(ms, pairs, _cfg()) == float(golden["a_alpha"])
+    assert D.score_alpha(float(golden["a_cands"][0, 3]), ms, pairs) == pytest.approx(
+        float(golden["a_scores"][0, 3]), rel=1e-8)
+
+
+def test_small_pairs_use_the_plain_fit(golden):
+    """12 correspondences per pair: no LMedS (M < 16), least squares + refit."""
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "a_")
+    small = [SimpleNamespace(i=p.i, j=p.j, correspondences=p.correspondences[:12],
+                             geometry_class=p.geometry_class)
+             for p in (ms.pairs[k] for k in golden["a_ready"])]
+    got = D.score_alpha_batch([-0.3, 0.0, 0.25], ms, small)
+    np.testing.assert_allclose(got, golden["a_small_scores"], rtol=1e-8)
+
+
+def test_two_camera_schedule_matches_reference(golden):
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "b_")
+    alphas, unest = D.schedule_cameras(ms, _cfg())
+    assert [alphas[c] for c in sorted(alphas)] == list(golden["b_alphas"])
+    assert unest == list(golden["b_unestimated"])
+
+
+def test_degenerate_inputs_raise_like_reference(golden):
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "a_")
+    with pytest.raises(D.DegenerateGeometryError):
+        D.score_alpha(0.0, ms, [])
+    tiny = [SimpleNamespace(i=p.i, j=p.j, correspondences=p.correspondences[:7],
+                            geometry_class=p.geometry_class) for p in ms.pairs[:3]]
+    with pytest.raises(D.DegenerateGeometryError):  # every pair below 8 points: none scored
+        D.score_alpha(0.0, ms, tiny)

@@ -20,12 +20,14 @@ def test_install_swaps_the_pipeline_call_sites():
         ref_tr = importlib.import_module("fastmap.translation")
         ref_epi = importlib.import_module("fastmap.epipolar")
         ref_rot = importlib.import_module("fastmap.rotation")
+        ref_dist = importlib.import_module("fastmap.distortion")
+        ref_two = importlib.import_module("fastmap.twoview")
     except ImportError as exc:  # reference dependencies missing
         pytest.skip(str(exc))
     finally:
         sys.path.remove(REF)
     import paper_2505_04612_b200 as b200
-    from paper_2505_04612_b200 import epipolar, rotation, translation
+    from paper_2505_04612_b200 import distortion, epipolar, rotation, translation
     saved = b200.install(fastmap)
     try:
         assert pipeline.irls_refine is epipolar.irls_refine          # ref/pipeline.py:248
@@ -34,7 +36,10 @@ def test_install_swaps_the_pipeline_call_sites():
         assert translation.PairRejected is ref_tr.PairRejected       # caught at :210
         assert ref_epi.quadratic_loss_and_grad is epipolar.quadratic_loss_and_grad
         assert ref_rot.refine_rotations is rotation.refine_rotations     # ref/pipeline.py:170
+        assert ref_dist.search_alpha is distortion.search_alpha          # via schedule_cameras
+        assert distortion.DegenerateGeometryError is ref_two.DegenerateGeometryError
     finally:
         for (mod, name), obj in saved.items():
             setattr(sys.modules[mod], name, obj)
     assert translation.PairRejected is not ref_tr.PairRejected
+    assert distortion.DegenerateGeometryError is not ref_two.DegenerateGeometryError
