@@ -392,14 +392,17 @@ int fm_rot_refine(const fm_rot_graph* g, double* params6, int32_t max_steps, dou
  * sample_off[k] holds them as [64][8] int32, sample_off[k] = -1 below 16)
  * and _refit_on_inliers (:48-55), then err_sum[k] = sum |x2^T F x1| and
  * n_err[k] = M -- or n_err[k] = 0 when a fit is degenerate (the reference
- * raises DegenerateGeometryError and score_alpha skips the pair).
- * Replaces the per-pair body of score_alpha (ref/distortion.py:107-124).
+ * raises DegenerateGeometryError and score_alpha skips the pair).  F_out
+ * (nullable) [n_jobs][9]: the fitted, Frobenius-normalised F row-major
+ * (NaN when degenerate).  Replaces the per-pair body of score_alpha
+ * (ref/distortion.py:107-124) and, with F_out, batches estimate_fundamental
+ * for undistorted_fundamentals (ref/focal.py:51-78).
  */
 size_t fm_fund_scratch_bytes(int64_t n_points);
 int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, const double* p2,
                   const int32_t* sample_idx, const int64_t* sample_off, double* err_sum,
-                  int32_t* n_err, void* scratch, size_t scratch_bytes, int64_t n_points,
-                  void* stream);
+                  int32_t* n_err, double* F_out, void* scratch, size_t scratch_bytes,
+                  int64_t n_points, void* stream);
 
 #ifdef __cplusplus
 }

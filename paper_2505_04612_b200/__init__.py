@@ -66,4 +66,8 @@ def install(fastmap_module=None):
     for name in ("score_alpha", "search_alpha"):
         swap(ref_dist, name, getattr(distortion, name))
     swap(distortion, "DegenerateGeometryError", ref_two.DegenerateGeometryError)
+    # ref/pipeline.py:105 calls focal.undistorted_fundamentals through the module
+    ref_focal = importlib.import_module(fm.__name__ + ".focal")
+    from . import focal
+    swap(ref_focal, "undistorted_fundamentals", focal.undistorted_fundamentals)
     return saved

@@ -12,8 +12,9 @@
 //     per sample (warp radix select), argmin, the 2.5-sigma consensus set,
 //     then the least-squares fit on it;
 //   M < 16: the least-squares fit on all points (ref/twoview.py:107-123);
-// then _refit_on_inliers (ref/twoview.py:48-55) and the error sum
-// (ref/distortion.py:119-122).  A fit whose Frobenius norm is < 1e-15
+// then _refit_on_inliers (ref/twoview.py:48-55), the error sum
+// (ref/distortion.py:119-122) and, optionally, the fitted F itself (the
+// batched estimate_fundamental of ref/focal.py:72).  A fit whose Frobenius norm is < 1e-15
 // reports n_err = 0 (the reference raises and score_alpha skips the pair).
 //
 // Reductions are block-level in a fixed order (deterministic); medians are
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kThreads)
 fund_score_kernel(const int64_t* __restrict__ job_off, const double2* __restrict__ p1all,
                   const double2* __restrict__ p2all, const int32_t* __restrict__ sample_idx,
                   const int64_t* __restrict__ sample_off, double* __restrict__ err_sum,
-                  int32_t* __restrict__ n_err, double* __restrict__ rbuf_all,
+                  int32_t* __restrict__ n_err, double* __restrict__ F_out, double* __restrict__ rbuf_all,
                   unsigned char* __restrict__ keep_all) {
   __shared__ Shared sh;
   const int64_t job = blockIdx.x;
@@ -331,7 +332,11 @@ fund_score_kernel(const int64_t* __restrict__ job_off, const double2* __restrict
   const int M = (int)(job_off[job + 1] - off);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (M < 8) {
-    if (threadIdx.x == 0) err_sum[job] = 0.0, n_err[job] = 0;
+    if (threadIdx.x == 0) {
+      err_sum[job] = 0.0, n_err[job] = 0;
+      if (F_out)
+        for (int i = 0; i < 9; ++i) F_out[9 * job + i] = NAN;
+    }
     return;
   }
   const double2* p1 = p1all + off;
@@ -473,9 +478,14 @@ fund_score_kernel(const int64_t* __restrict__ job_off, const double2* __restrict
 
   // ---------------- error sum (ref/distortion.py:121-122)
   if (!sh.status) {
-    if (threadIdx.x == 0) err_sum[job] = 0.0, n_err[job] = 0;
+    if (threadIdx.x == 0) {
+      err_sum[job] = 0.0, n_err[job] = 0;
+      if (F_out)
+        for (int i = 0; i < 9; ++i) F_out[9 * job + i] = NAN;
+    }
     return;
   }
+  if (F_out && threadIdx.x < 9) F_out[9 * job + threadIdx.x] = sh.F[threadIdx.x];
   double F[9];
   for (int i = 0; i < 9; ++i) F[i] = sh.F[i];
   double e[1] = {0.0};
@@ -498,8 +508,8 @@ size_t fm_fund_scratch_bytes(int64_t n_points) {
 
 int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, const double* p2,
                   const int32_t* sample_idx, const int64_t* sample_off, double* err_sum,
-                  int32_t* n_err, void* scratch, size_t scratch_bytes, int64_t n_points,
-                  void* stream) {
+                  int32_t* n_err, double* F_out, void* scratch, size_t scratch_bytes,
+                  int64_t n_points, void* stream) {
   FM_REQUIRE(n_jobs >= 0 && n_points >= 0, "bad fundamental-fit sizes");
   if (n_jobs == 0) return FM_OK;
   FM_REQUIRE(job_off && p1 && p2 && sample_off && err_sum && n_err && scratch,
@@ -510,7 +520,7 @@ int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, cons
   unsigned char* keep = reinterpret_cast<unsigned char*>(rbuf + kWarps * n_points);
   fund_score_kernel<<<(unsigned)n_jobs, kThreads, 0, as_stream(stream)>>>(
       job_off, reinterpret_cast<const double2*>(p1), reinterpret_cast<const double2*>(p2),
-      sample_idx, sample_off, err_sum, n_err, rbuf, keep);
+      sample_idx, sample_off, err_sum, n_err, F_out, rbuf, keep);
   FM_LAUNCHED(fund_score_kernel);
   return FM_OK;
 }

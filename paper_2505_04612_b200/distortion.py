@@ -105,6 +105,64 @@ def _jobs(alphas, match_set, pairs, camera_id, known_alphas):
             np.concatenate(p2s))
 
 
+def fit_jobs(lens, p1, p2, want_F=False):
+    """One fm_fund_score launch over concatenated jobs (lens[k] >= 8 point
+    pairs each, p1/p2 (sum lens, 2) fp64).  Returns (error sums, point counts
+    (0 = degenerate fit), F (n_jobs, 3, 3) or None)."""
+    device = N.require_cuda()
+    lib = N.lib()
+    lens = np.asarray(lens, dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    tables, s_off, at = [], [], 0
+    seen = {}
+    for M in lens:
+        if M < 16:
+            s_off.append(-1)
+            continue
+        if M not in seen:
+            seen[M] = at
+            tables.append(lmeds_samples(int(M)).ravel())
+            at += 8 * _LMEDS_ITERS
+        s_off.append(seen[M])
+    samples = np.concatenate(tables) if tables else np.zeros(1, dtype=np.int32)
+    n_pts = int(off[-1])
+    P1 = torch.as_tensor(np.ascontiguousarray(p1, dtype=np.float64), device=device)
+    P2 = torch.as_tensor(np.ascontiguousarray(p2, dtype=np.float64), device=device)
+    off_d = torch.as_tensor(off, device=device)
+    samp_d = torch.as_tensor(samples, device=device)
+    soff_d = torch.as_tensor(np.array(s_off, dtype=np.int64), device=device)
+    err = torch.empty(len(lens), dtype=torch.float64, device=device)
+    nerr = torch.empty(len(lens), dtype=torch.int32, device=device)
+    F = torch.empty((len(lens), 9), dtype=torch.float64, device=device) if want_F else None
+    nbytes = int(lib.fm_fund_scratch_bytes(n_pts))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    N.check(lib.fm_fund_score(len(lens), N.ptr(off_d), N.ptr(P1), N.ptr(P2), N.ptr(samp_d),
+                              N.ptr(soff_d), N.ptr(err), N.ptr(nerr),
+                              N.ptr(F) if want_F else None, N.ptr(scratch), nbytes, n_pts,
+                              N.stream_handle()))
+    return (err.cpu().numpy(), nerr.cpu().numpy(),
+            F.cpu().numpy().reshape(-1, 3, 3) if want_F else None)
+
+
+def estimate_fundamental_batch(p1s, p2s):
+    """estimate_fundamental (ref/twoview.py:58-76) for many point sets in one
+    launch: a list of F (Frobenius-normalised, rank 2) or None where the
+    reference raises DegenerateGeometryError (fewer than 8 points or a
+    degenerate fit)."""
+    out = [None] * len(p1s)
+    keep = [k for k in range(len(p1s)) if len(p1s[k]) >= 8]
+    if not keep:
+        return out
+    lens = [len(p1s[k]) for k in keep]
+    _, nerr, F = fit_jobs(lens, np.concatenate([np.asarray(p1s[k], np.float64) for k in keep]),
+                          np.concatenate([np.asarray(p2s[k], np.float64) for k in keep]),
+                          want_F=True)
+    for q, k in enumerate(keep):
+        if nerr[q]:
+            out[k] = F[q]
+    return out
+
+
 def score_alpha_batch(alphas, match_set, pairs, camera_id=None, known_alphas=None):
     """score_alpha (ref/distortion.py:90-126) for several candidates in one
     device launch.  Returns the scores in candidate order; raises like the
@@ -116,36 +174,7 @@ def score_alpha_batch(alphas, match_set, pairs, camera_id=None, known_alphas=Non
     total = np.zeros(len(alphas))
     count = np.zeros(len(alphas), dtype=np.int64)
     if len(lens):
-        device = N.require_cuda()
-        lib = N.lib()
-        off = np.concatenate([[0], np.cumsum(lens)])
-        tables, s_off, at = [], [], 0
-        seen = {}
-        for M in lens:
-            if M < 16:
-                s_off.append(-1)
-                continue
-            if M not in seen:
-                seen[M] = at
-                tables.append(lmeds_samples(int(M)).ravel())
-                at += 8 * _LMEDS_ITERS
-            s_off.append(seen[M])
-        samples = np.concatenate(tables) if tables else np.zeros(1, dtype=np.int32)
-        n_pts = int(off[-1])
-        P1 = torch.as_tensor(np.ascontiguousarray(p1), device=device)
-        P2 = torch.as_tensor(np.ascontiguousarray(p2), device=device)
-        off_d = torch.as_tensor(off, device=device)
-        samp_d = torch.as_tensor(samples, device=device)
-        soff_d = torch.as_tensor(np.array(s_off, dtype=np.int64), device=device)
-        err = torch.empty(len(lens), dtype=torch.float64, device=device)
-        nerr = torch.empty(len(lens), dtype=torch.int32, device=device)
-        nbytes = int(lib.fm_fund_scratch_bytes(n_pts))
-        scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        N.check(lib.fm_fund_score(len(lens), N.ptr(off_d), N.ptr(P1), N.ptr(P2), N.ptr(samp_d),
-                                  N.ptr(soff_d), N.ptr(err), N.ptr(nerr), N.ptr(scratch), nbytes,
-                                  n_pts, N.stream_handle()))
-        err = err.cpu().numpy()
-        nerr = nerr.cpu().numpy()
+        err, nerr, _ = fit_jobs(lens, p1, p2)
         for q, c in enumerate(job_cand):  # pair order within a candidate, as the reference
             if nerr[q]:
                 total[c] += float(err[q])
@@ -231,5 +260,6 @@ def schedule_cameras(match_set, cfg):
     return alphas, unestimated
 
 
-__all__ = ["DegenerateGeometryError", "undistort_normalized", "lmeds_samples", "score_alpha",
+__all__ = ["DegenerateGeometryError", "undistort_normalized", "lmeds_samples", "fit_jobs",
+           "estimate_fundamental_batch", "score_alpha",
            "score_alpha_batch", "search_alpha", "ready_fundamental_pairs", "schedule_cameras"]

@@ -3,8 +3,9 @@ SURVEY 8f "next" #4) from the REFERENCE implementation (read-only import):
 the synthetic match sets of the reference's own distortion tests
 (pkg/tests/test_distortion.py:43-80), the scores score_alpha gives every
 candidate of every search level, the search_alpha result, and the
-schedule_cameras result of the two-camera scene.  Also a subset-sized pair
-(M < 16, the non-LMedS branch) scored on its own.
+schedule_cameras result of the two-camera scene, a subset-sized pair set
+(M < 16, the non-LMedS branch), and undistorted_fundamentals + the focal
+vote (ref/focal.py:51-172) on both scenes.
 
     python tests/golden/make_distortion_golden.py      (a minute; not run by pytest)
 """
@@ -18,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from fastmap import distortion, synth  # noqa: E402
+from fastmap import distortion, focal, synth  # noqa: E402
 from fastmap.config import PipelineConfig  # noqa: E402
 from fastmap.model import GeometryClass  # noqa: E402
 
@@ -70,6 +71,15 @@ def main():
     alphas, unest = distortion.schedule_cameras(ms_b, cfg)
     out["b_alphas"] = np.array([alphas[c] for c in sorted(alphas)])
     out["b_unestimated"] = np.array(unest, dtype=np.int64)
+    # undistorted_fundamentals + the focal vote (ref/focal.py:51-172) on both scenes
+    for pre, m, al in (("a_", ms, {0: float(out["a_alpha"])}), ("b_", ms_b, alphas)):
+        t0 = time.perf_counter()
+        fund = focal.undistorted_fundamentals(m, al)
+        out[pre + "fund_seconds"] = np.array(time.perf_counter() - t0)
+        out[pre + "fund_idx"] = np.array([m.pairs.index(p) for p, _ in fund], dtype=np.int64)
+        out[pre + "fund_F"] = np.stack([F for _, F in fund])
+        foc, fb = focal.vote_focal_multi(m, fund, cfg)
+        out[pre + "focals"] = np.array([foc[c] for c in sorted(foc)])
     np.savez_compressed(os.path.join(HERE, "golden_distortion.npz"), **out)
     print({k: v.shape for k, v in out.items()})
     print("scene A alpha", out["a_alpha"], "ref search seconds", out["a_ref_seconds"],

@@ -92,3 +92,20 @@ def test_degenerate_inputs_raise_like_reference(golden):
                             geometry_class=p.geometry_class) for p in ms.pairs[:3]]
     with pytest.raises(D.DegenerateGeometryError):  # every pair below 8 points: none scored
         D.score_alpha(0.0, ms, tiny)
+
+
+@pytest.mark.parametrize("scene", ["a_", "b_"])
+def test_undistorted_fundamentals_match_reference(golden, scene):
+    """ref/focal.py:51-78 on both scenes with the searched alphas: the same
+    pairs survive, and every F equals the reference's up to its sign (the
+    eigenvector sign is solver-dependent; the focal vote uses singular
+    values only)."""
+    from paper_2505_04612_b200 import focal
+    ms = _match_set(golden, scene)
+    al = ({0: float(golden["a_alpha"])} if scene == "a_"
+          else {c: float(a) for c, a in enumerate(golden["b_alphas"])})
+    got = focal.undistorted_fundamentals(ms, al)
+    assert [ms.pairs.index(p) for p, _ in got] == list(golden[scene + "fund_idx"])
+    for (_, F), R in zip(got, golden[scene + "fund_F"]):
+        d = min(np.abs(F - R).max(), np.abs(F + R).max())
+        assert d < 1e-7, d

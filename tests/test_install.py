@@ -22,12 +22,13 @@ def test_install_swaps_the_pipeline_call_sites():
         ref_rot = importlib.import_module("fastmap.rotation")
         ref_dist = importlib.import_module("fastmap.distortion")
         ref_two = importlib.import_module("fastmap.twoview")
+        ref_focal = importlib.import_module("fastmap.focal")
     except ImportError as exc:  # reference dependencies missing
         pytest.skip(str(exc))
     finally:
         sys.path.remove(REF)
     import paper_2505_04612_b200 as b200
-    from paper_2505_04612_b200 import distortion, epipolar, rotation, translation
+    from paper_2505_04612_b200 import distortion, epipolar, focal, rotation, translation
     saved = b200.install(fastmap)
     try:
         assert pipeline.irls_refine is epipolar.irls_refine          # ref/pipeline.py:248
@@ -38,6 +39,7 @@ def test_install_swaps_the_pipeline_call_sites():
         assert ref_rot.refine_rotations is rotation.refine_rotations     # ref/pipeline.py:170
         assert ref_dist.search_alpha is distortion.search_alpha          # via schedule_cameras
         assert distortion.DegenerateGeometryError is ref_two.DegenerateGeometryError
+        assert ref_focal.undistorted_fundamentals is focal.undistorted_fundamentals  # :105
     finally:
         for (mod, name), obj in saved.items():
             setattr(sys.modules[mod], name, obj)

@@ -20,3 +20,10 @@ t0 = time.perf_counter(); D._jobs(list(cands), ms, pairs, None, None); host = ti
 st.record(); D.score_alpha_batch(cands, ms, pairs); en.record(); torch.cuda.synchronize()
 print({"alpha": a, "search_alpha_s": min(ts), "ref_search_alpha_s": float(g["a_ref_seconds"]),
        "level_launch_plus_host_ms": st.elapsed_time(en), "host_prep_ms": host * 1e3, "jobs": len(jobs[1])})
+from paper_2505_04612_b200 import focal
+for pre in ("a_", "b_"):
+    ms2 = _match_set(g, pre)
+    al = {0: float(g["a_alpha"])} if pre == "a_" else {c: float(a) for c, a in enumerate(g["b_alphas"])}
+    focal.undistorted_fundamentals(ms2, al)
+    t0 = time.perf_counter(); focal.undistorted_fundamentals(ms2, al); dt = time.perf_counter() - t0
+    print({"scene": pre, "undistorted_fundamentals_s": dt, "ref_s": float(g[pre + "fund_seconds"])})
