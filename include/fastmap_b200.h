@@ -404,6 +404,19 @@ int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, cons
                   int32_t* n_err, double* F_out, void* scratch, size_t scratch_bytes,
                   int64_t n_points, void* stream);
 
+/*
+ * Robust homography fit (ref/twoview.py:136-201) for every job (same layout
+ * as fm_fund_score, M >= 4 points; sample_off[k] = -1 below 12, else the
+ * offset of the reference's 64 sequential 4-point samples [64][4] int32).
+ * H_out [n_jobs][9]: Frobenius-normalised, positive-trace H row-major, NaN
+ * where the reference raises DegenerateGeometryError.  Scratch:
+ * fm_fund_scratch_bytes(n_points).  Batches the homography pairs of
+ * apply_calibration (ref/focal.py:195-200).
+ */
+int fm_homog_fit(int64_t n_jobs, const int64_t* job_off, const double* p1, const double* p2,
+                 const int32_t* sample_idx, const int64_t* sample_off, double* H_out,
+                 void* scratch, size_t scratch_bytes, int64_t n_points, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,5 +69,6 @@ def install(fastmap_module=None):
     # ref/pipeline.py:105 calls focal.undistorted_fundamentals through the module
     ref_focal = importlib.import_module(fm.__name__ + ".focal")
     from . import focal
-    swap(ref_focal, "undistorted_fundamentals", focal.undistorted_fundamentals)
+    for name in ("undistorted_fundamentals", "apply_calibration"):  # :105, :123
+        swap(ref_focal, name, getattr(focal, name))
     return saved

@@ -494,6 +494,245 @@ fund_score_kernel(const int64_t* __restrict__ job_off, const double2* __restrict
   if (threadIdx.x == 0) err_sum[job] = e[0], n_err[job] = M;
 }
 
+
+// ======================================================================
+// Robust homography fit (ref/twoview.py:136-201): the same job layout; the
+// LMedS samples are 64 sequential 4-point draws (table from the host),
+// a sample whose fit is degenerate is skipped, the score is the median
+// Euclidean transfer error (non-finite -> inf), and the fits keep the
+// reference's det / norm checks and positive-trace sign.
+// ======================================================================
+
+// transfer error ||proj(H x1) - x2|| (ref/twoview.py:126-134)
+__device__ __forceinline__ double transfer_err(const double (&H)[9], double2 a, double2 b) {
+  const double px = H[0] * a.x + H[1] * a.y + H[2];
+  const double py = H[3] * a.x + H[4] * a.y + H[5];
+  const double pz = H[6] * a.x + H[7] * a.y + H[8];
+  const double dx = px / pz - b.x, dy = py / pz - b.y;
+  if (!isfinite(dx) || !isfinite(dy)) return INFINITY;
+  return sqrt(dx * dx + dy * dy);
+}
+
+// A rows of the normalised DLT (ref/twoview.py:186-190), accumulated into
+// the 45 upper-triangle entries of A^T A
+__device__ __forceinline__ void homog_rows(const Hartley& T, double2 a, double2 b, double (&n45)[45]) {
+  const double x1[3] = {T.s1 * (a.x - T.cx1), T.s1 * (a.y - T.cy1), 1.0};
+  const double x2x = T.s2 * (b.x - T.cx2), x2y = T.s2 * (b.y - T.cy2);
+  double r0[9] = {0, 0, 0, -x1[0], -x1[1], -x1[2], x2y * x1[0], x2y * x1[1], x2y * x1[2]};
+  double r1[9] = {x1[0], x1[1], x1[2], 0, 0, 0, -x2x * x1[0], -x2x * x1[1], -x2x * x1[2]};
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j) n45[q++] += r0[i] * r0[j] + r1[i] * r1[j];
+}
+
+// H from the normal matrix: smallest eigenvector, H = inv(T2) H T1, the
+// degeneracy test on the unnormalised H, then Frobenius norm and trace sign.
+// Returns false when degenerate (ref/twoview.py:191-200).
+__device__ bool homog_from_normal(const double (&n45)[45], const Hartley& T, double (&H)[9]) {
+  double a[9][9];
+  int q = 0;
+  for (int i = 0; i < 9; ++i)
+    for (int j = i; j < 9; ++j) a[i][j] = a[j][i] = n45[q++];
+  double h[9];
+  smallest_eigvec9(a, h);
+  // inv(T2) = [[1/s2, 0, cx2], [0, 1/s2, cy2], [0, 0, 1]]
+  const double t1[9] = {T.s1, 0.0, -T.s1 * T.cx1, 0.0, T.s1, -T.s1 * T.cy1, 0.0, 0.0, 1.0};
+  const double i2[9] = {1.0 / T.s2, 0.0, T.cx2, 0.0, 1.0 / T.s2, T.cy2, 0.0, 0.0, 1.0};
+  double g[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += h[i * 3 + k] * t1[k * 3 + j];
+      g[i * 3 + j] = acc;
+    }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += i2[i * 3 + k] * g[k * 3 + j];
+      H[i * 3 + j] = acc;
+    }
+  double nrm = 0.0;
+  for (int i = 0; i < 9; ++i) nrm += H[i] * H[i];
+  nrm = sqrt(nrm);
+  const double det = H[0] * (H[4] * H[8] - H[5] * H[7]) - H[1] * (H[3] * H[8] - H[5] * H[6]) +
+                     H[2] * (H[3] * H[7] - H[4] * H[6]);
+  if (!(nrm >= 1e-15) || !(fabs(det) >= 1e-12)) return false;
+  const double sg = (H[0] + H[4] + H[8]) / nrm < 0 ? -1.0 : 1.0;
+  for (int i = 0; i < 9; ++i) H[i] = sg * (H[i] / nrm);
+  return true;
+}
+
+// block-level least-squares homography on the masked points -> sh.F / sh.status
+__device__ void fit_homography_block(const double2* p1, const double2* p2, const unsigned char* keep,
+                                     int M, Shared& sh) {
+  hartley(p1, p2, keep, M, sh);
+  const Hartley T = sh.T;
+  double n45[45];
+#pragma unroll
+  for (int i = 0; i < 45; ++i) n45[i] = 0.0;
+  for (int m = threadIdx.x; m < M; m += kThreads) {
+    if (keep && !keep[m]) continue;
+    homog_rows(T, p1[m], p2[m], n45);
+  }
+  block_sum<45>(n45, sh.red);
+  if (threadIdx.x == 0) {
+    double H[9];
+    if (homog_from_normal(n45, T, H))
+      for (int i = 0; i < 9; ++i) sh.F[i] = H[i];
+    else
+      sh.status = 0;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads)
+homog_fit_kernel(const int64_t* __restrict__ job_off, const double2* __restrict__ p1all,
+                 const double2* __restrict__ p2all, const int32_t* __restrict__ sample_idx,
+                 const int64_t* __restrict__ sample_off, double* __restrict__ H_out,
+                 double* __restrict__ rbuf_all, unsigned char* __restrict__ keep_all) {
+  __shared__ Shared sh;
+  const int64_t job = blockIdx.x;
+  const int64_t off = job_off[job];
+  const int M = (int)(job_off[job + 1] - off);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (M < 4) {
+    if (threadIdx.x < 9) H_out[9 * job + threadIdx.x] = NAN;
+    return;
+  }
+  const double2* p1 = p1all + off;
+  const double2* p2 = p2all + off;
+  double* rbuf = rbuf_all + kWarps * off;
+  unsigned char* keep = keep_all + off;
+  if (threadIdx.x == 0) sh.status = 1;
+  __syncthreads();
+
+  if (sample_off[job] >= 0) {
+    // ---------------- LMedS (ref/twoview.py:156-177)
+    if (threadIdx.x < kSamples) {
+      const int32_t* idx = sample_idx + sample_off[job] + 4 * threadIdx.x;
+      double2 a[4], b[4];
+      for (int r = 0; r < 4; ++r) a[r] = p1[idx[r]], b[r] = p2[idx[r]];
+      // Hartley normalisation of the 4 points (same expressions as hartley())
+      double sx1 = 0, sy1 = 0, sx2 = 0, sy2 = 0;
+      for (int r = 0; r < 4; ++r) sx1 += a[r].x, sy1 += a[r].y, sx2 += b[r].x, sy2 += b[r].y;
+      Hartley T;
+      T.cx1 = sx1 / 4.0, T.cy1 = sy1 / 4.0, T.cx2 = sx2 / 4.0, T.cy2 = sy2 / 4.0;
+      double d1 = 0, d2 = 0;
+      for (int r = 0; r < 4; ++r) {
+        d1 += sqrt((a[r].x - T.cx1) * (a[r].x - T.cx1) + (a[r].y - T.cy1) * (a[r].y - T.cy1));
+        d2 += sqrt((b[r].x - T.cx2) * (b[r].x - T.cx2) + (b[r].y - T.cy2) * (b[r].y - T.cy2));
+      }
+      T.s1 = sqrt(2.0) / fmax(d1 / 4.0, 1e-12);
+      T.s2 = sqrt(2.0) / fmax(d2 / 4.0, 1e-12);
+      double n45[45];
+      for (int i = 0; i < 45; ++i) n45[i] = 0.0;
+      for (int r = 0; r < 4; ++r) homog_rows(T, a[r], b[r], n45);
+      double H[9];
+      const bool ok = homog_from_normal(n45, T, H);
+      for (int i = 0; i < 9; ++i) sh.Fk[threadIdx.x][i] = ok ? H[i] : NAN;
+    }
+    __syncthreads();
+    double* mybuf = rbuf + (int64_t)w * M;
+    for (int k = w; k < kSamples; k += kWarps) {
+      double H[9];
+      for (int i = 0; i < 9; ++i) H[i] = sh.Fk[k][i];
+      if (isnan(H[0])) {  // degenerate sample: skipped (ref/twoview.py:162-165)
+        if (lane == 0) sh.med[k] = NAN;
+        continue;
+      }
+      for (int m = lane; m < M; m += 32) mybuf[m] = transfer_err(H, p1[m], p2[m]);
+      __syncwarp();
+      const double med = warp_median(mybuf, M, sh.hist[w]);
+      if (lane == 0) sh.med[k] = med;
+      __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int b = -1;
+      double bm = INFINITY;
+      for (int k = 0; k < kSamples; ++k)
+        if (sh.med[k] < bm) bm = sh.med[k], b = k;  // strict <, from +inf (ref :166-167)
+      sh.best = b;
+    }
+    __syncthreads();
+    if (sh.best < 0) {
+      fit_homography_block(p1, p2, nullptr, M, sh);
+    } else {
+      double H[9];
+      for (int i = 0; i < 9; ++i) H[i] = sh.Fk[sh.best][i];
+      for (int m = threadIdx.x; m < M; m += kThreads) rbuf[m] = transfer_err(H, p1[m], p2[m]);
+      __syncthreads();
+      if (w == 0) {
+        double m2;
+        if (M & 1) {
+          const double x = warp_kth(rbuf, M, (M - 1) / 2, sh.hist[0]);
+          m2 = x * x;
+        } else {
+          const double x = warp_kth(rbuf, M, M / 2 - 1, sh.hist[0]);
+          const double y = warp_kth(rbuf, M, M / 2, sh.hist[0]);
+          m2 = (x * x + y * y) / 2.0;
+        }
+        if (lane == 0) sh.thr = 2.5 * (1.4826 * (1.0 + 5.0 / max(M - 4, 1)) * sqrt(m2));
+      }
+      __syncthreads();
+      double cnt[1] = {0.0};
+      for (int m = threadIdx.x; m < M; m += kThreads) {
+        const bool k = rbuf[m] <= sh.thr;
+        keep[m] = k;
+        cnt[0] += k;
+      }
+      block_sum<1>(cnt, sh.red);
+      if (cnt[0] < 4.0) {
+        const int K = max(4, M / 2);
+        if (w == 0) {
+          const double v = warp_kth(rbuf, M, K - 1, sh.hist[0]);
+          if (lane == 0) sh.thr = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const double v = sh.thr;
+          int lt = 0;
+          for (int m = 0; m < M; ++m) lt += rbuf[m] < v;
+          int need = K - lt;
+          for (int m = 0; m < M; ++m) {
+            const bool tie = rbuf[m] == v && need > 0;
+            if (tie) --need;
+            keep[m] = rbuf[m] < v || tie;
+          }
+        }
+        __syncthreads();
+      }
+      fit_homography_block(p1, p2, keep, M, sh);
+    }
+  } else {
+    fit_homography_block(p1, p2, nullptr, M, sh);
+  }
+
+  // ---------------- _refit_on_inliers (ref/twoview.py:48-55), min support 4
+  if (sh.status) {
+    double H[9];
+    for (int i = 0; i < 9; ++i) H[i] = sh.F[i];
+    for (int m = threadIdx.x; m < M; m += kThreads) rbuf[m] = transfer_err(H, p1[m], p2[m]);
+    __syncthreads();
+    if (w == 0) {
+      const double med = warp_median(rbuf, M, sh.hist[0]);
+      if (lane == 0) sh.thr = fmax(10.0 * med, 1e-12);
+    }
+    __syncthreads();
+    double cnt[1] = {0.0};
+    for (int m = threadIdx.x; m < M; m += kThreads) {
+      const bool k = rbuf[m] <= sh.thr;
+      keep[m] = k;
+      cnt[0] += k;
+    }
+    block_sum<1>(cnt, sh.red);
+    if (cnt[0] >= 4.0 && cnt[0] < (double)M) fit_homography_block(p1, p2, keep, M, sh);
+  }
+  if (threadIdx.x < 9) H_out[9 * job + threadIdx.x] = sh.status ? sh.F[threadIdx.x] : NAN;
+}
+
 }  // namespace
 }  // namespace fm
 
@@ -522,6 +761,23 @@ int fm_fund_score(int64_t n_jobs, const int64_t* job_off, const double* p1, cons
       job_off, reinterpret_cast<const double2*>(p1), reinterpret_cast<const double2*>(p2),
       sample_idx, sample_off, err_sum, n_err, F_out, rbuf, keep);
   FM_LAUNCHED(fund_score_kernel);
+  return FM_OK;
+}
+
+int fm_homog_fit(int64_t n_jobs, const int64_t* job_off, const double* p1, const double* p2,
+                 const int32_t* sample_idx, const int64_t* sample_off, double* H_out,
+                 void* scratch, size_t scratch_bytes, int64_t n_points, void* stream) {
+  FM_REQUIRE(n_jobs >= 0 && n_points >= 0, "bad homography-fit sizes");
+  if (n_jobs == 0) return FM_OK;
+  FM_REQUIRE(job_off && p1 && p2 && sample_off && H_out && scratch, "null homography-fit pointer");
+  FM_REQUIRE(n_jobs <= 0x7fffffff, "too many homography-fit jobs");
+  FM_REQUIRE(scratch_bytes >= fm_fund_scratch_bytes(n_points), "homography-fit scratch too small");
+  double* rbuf = static_cast<double*>(scratch);
+  unsigned char* keep = reinterpret_cast<unsigned char*>(rbuf + kWarps * n_points);
+  homog_fit_kernel<<<(unsigned)n_jobs, kThreads, 0, as_stream(stream)>>>(
+      job_off, reinterpret_cast<const double2*>(p1), reinterpret_cast<const double2*>(p2),
+      sample_idx, sample_off, H_out, rbuf, keep);
+  FM_LAUNCHED(homog_fit_kernel);
   return FM_OK;
 }
 

@@ -163,6 +163,56 @@ def estimate_fundamental_batch(p1s, p2s):
     return out
 
 
+@functools.lru_cache(maxsize=4096)
+def lmeds_samples4(M):
+    """The reference's homography samples for M points (ref/twoview.py:157-161):
+    one rng(12345), 64 sequential choice(M, 4, replace=False) -> (64, 4) int32."""
+    rng = np.random.default_rng(_LMEDS_SEED)
+    return np.stack([rng.choice(M, 4, replace=False) for _ in range(_LMEDS_ITERS)]).astype(np.int32)
+
+
+def estimate_homography_batch(p1s, p2s):
+    """estimate_homography (ref/twoview.py:136-153) for many point sets in one
+    launch (fm_homog_fit): a list of H (Frobenius-normalised, positive trace)
+    or None where the reference raises DegenerateGeometryError."""
+    out = [None] * len(p1s)
+    keep = [k for k in range(len(p1s)) if len(p1s[k]) >= 4]
+    if not keep:
+        return out
+    device = N.require_cuda()
+    lib = N.lib()
+    lens = np.array([len(p1s[k]) for k in keep], dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    tables, s_off, at, seen = [], [], 0, {}
+    for M in lens:
+        if M < 12:
+            s_off.append(-1)
+            continue
+        if M not in seen:
+            seen[M] = at
+            tables.append(lmeds_samples4(int(M)).ravel())
+            at += 4 * _LMEDS_ITERS
+        s_off.append(seen[M])
+    samples = np.concatenate(tables) if tables else np.zeros(1, dtype=np.int32)
+    n_pts = int(off[-1])
+    P1 = torch.as_tensor(np.concatenate([np.asarray(p1s[k], np.float64) for k in keep]), device=device)
+    P2 = torch.as_tensor(np.concatenate([np.asarray(p2s[k], np.float64) for k in keep]), device=device)
+    off_d = torch.as_tensor(off, device=device)
+    samp_d = torch.as_tensor(samples, device=device)
+    soff_d = torch.as_tensor(np.array(s_off, dtype=np.int64), device=device)
+    H = torch.empty((len(keep), 9), dtype=torch.float64, device=device)
+    nbytes = int(lib.fm_fund_scratch_bytes(n_pts))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    N.check(lib.fm_homog_fit(len(keep), N.ptr(off_d), N.ptr(P1), N.ptr(P2), N.ptr(samp_d),
+                             N.ptr(soff_d), N.ptr(H), N.ptr(scratch), nbytes, n_pts,
+                             N.stream_handle()))
+    H = H.cpu().numpy().reshape(-1, 3, 3)
+    for q, k in enumerate(keep):
+        if np.all(np.isfinite(H[q])):
+            out[k] = H[q]
+    return out
+
+
 def score_alpha_batch(alphas, match_set, pairs, camera_id=None, known_alphas=None):
     """score_alpha (ref/distortion.py:90-126) for several candidates in one
     device launch.  Returns the scores in candidate order; raises like the
@@ -261,5 +311,5 @@ def schedule_cameras(match_set, cfg):
 
 
 __all__ = ["DegenerateGeometryError", "undistort_normalized", "lmeds_samples", "fit_jobs",
-           "estimate_fundamental_batch", "score_alpha",
+           "estimate_fundamental_batch", "lmeds_samples4", "estimate_homography_batch", "score_alpha",
            "score_alpha_batch", "search_alpha", "ready_fundamental_pairs", "schedule_cameras"]

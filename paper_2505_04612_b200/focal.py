@@ -1,5 +1,6 @@
-"""Drop-in for the per-pair fundamental refits of ``fastmap.focal``
-(ref/focal.py:51-78, reached from ref/pipeline.py:105; SURVEY 8f "next" #4).
+"""Drop-in for the per-pair geometry refits of ``fastmap.focal``
+(ref/focal.py:51-78 and :175-203, reached from ref/pipeline.py:105 and
+:123; SURVEY 8f "next" #2/#4).
 
 ``undistorted_fundamentals`` undistorts every fundamental pair's keypoints
 with its camera's alpha (the reference's numpy expressions) and fits all
@@ -11,7 +12,8 @@ reference's.
 
 import numpy as np
 
-from .distortion import _is_homography, estimate_fundamental_batch, undistort_normalized
+from .distortion import (_is_homography, estimate_fundamental_batch, estimate_homography_batch,
+                         undistort_normalized)
 
 
 def undistorted_fundamentals(match_set, alphas):
@@ -40,4 +42,35 @@ def undistorted_fundamentals(match_set, alphas):
     return [(pair, F) for pair, F in zip(cand, Fs) if F is not None]
 
 
-__all__ = ["undistorted_fundamentals"]
+def apply_calibration(match_set, cameras):
+    """ref/focal.py:175-203: normalised homogeneous keypoints per image
+    (undistort with the camera's alpha, subtract the principal point, divide
+    by the focal -- the reference's numpy expressions) and every pair's
+    geometry refit in normalised coordinates, all fundamental pairs in one
+    device launch and all homography pairs in another.  Returns
+    (norm_kps, [(pair, matrix or None)]) in pair order."""
+    norm_kps = []
+    for im in match_set.images:
+        cam = cameras[im.camera_id]
+        s = cam.half_diagonal
+        center = np.array([cam.cx, cam.cy])
+        xn = (np.asarray(match_set.keypoints[im.image_id], dtype=np.float64) - center) / s
+        und = undistort_normalized(xn, cam.alpha) * s + center
+        xy = (und - np.array([cam.cx, cam.cy])) / cam.focal
+        norm_kps.append(np.concatenate([xy, np.ones(xy.shape[:-1] + (1,))], axis=-1))
+    fund, homog = [], []
+    for q, pair in enumerate(match_set.pairs):
+        x1 = norm_kps[pair.i][pair.correspondences[:, 0]][:, :2]
+        x2 = norm_kps[pair.j][pair.correspondences[:, 1]][:, :2]
+        ok = np.all(np.isfinite(x1), axis=1) & np.all(np.isfinite(x2), axis=1)
+        (homog if _is_homography(pair) else fund).append((q, x1[ok], x2[ok]))
+    mats = [None] * len(match_set.pairs)
+    for group, fit in ((fund, estimate_fundamental_batch), (homog, estimate_homography_batch)):
+        if group:
+            res = fit([a for _, a, _ in group], [b for _, _, b in group])
+            for (q, _, _), m in zip(group, res):
+                mats[q] = m
+    return norm_kps, [(pair, m) for pair, m in zip(match_set.pairs, mats)]
+
+
+__all__ = ["undistorted_fundamentals", "apply_calibration"]

@@ -5,7 +5,8 @@ the synthetic match sets of the reference's own distortion tests
 candidate of every search level, the search_alpha result, and the
 schedule_cameras result of the two-camera scene, a subset-sized pair set
 (M < 16, the non-LMedS branch), and undistorted_fundamentals + the focal
-vote (ref/focal.py:51-172) on both scenes.
+vote (ref/focal.py:51-172) on both scenes, and apply_calibration
+(ref/focal.py:175-203) on those and on a planar scene (homography pairs).
 
     python tests/golden/make_distortion_golden.py      (a minute; not run by pytest)
 """
@@ -21,7 +22,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from fastmap import distortion, focal, synth  # noqa: E402
 from fastmap.config import PipelineConfig  # noqa: E402
-from fastmap.model import GeometryClass  # noqa: E402
+from fastmap.model import CameraModel, GeometryClass  # noqa: E402
 
 
 def pack(prefix, ms, out):
@@ -32,6 +33,10 @@ def pack(prefix, ms, out):
     out[prefix + "pair_ij"] = np.array([[p.i, p.j] for p in ms.pairs], dtype=np.int64)
     out[prefix + "pair_len"] = np.array([len(p.correspondences) for p in ms.pairs], dtype=np.int64)
     out[prefix + "corr"] = np.concatenate([p.correspondences for p in ms.pairs]).astype(np.int64)
+
+
+def m_cams(ms):
+    return max(im.camera_id for im in ms.images) + 1
 
 
 def main():
@@ -80,6 +85,25 @@ def main():
         out[pre + "fund_F"] = np.stack([F for _, F in fund])
         foc, fb = focal.vote_focal_multi(m, fund, cfg)
         out[pre + "focals"] = np.array([foc[c] for c in sorted(foc)])
+    # apply_calibration (ref/focal.py:175-203) on A, B and a planar
+    # scene C (homography pairs), with the cameras the pipeline would build
+    ms_c, _ = synth.generate(synth.SynthSpec(n_images=8, n_points=200, seed=2,
+                                             planar_fraction=1.0))
+    pack("c_", ms_c, out)
+    out["c_homography"] = np.array([p.geometry_class is GeometryClass.HOMOGRAPHY for p in ms_c.pairs])
+    for pre, m, foc, al in (("a_", ms, out["a_focals"], {0: float(out["a_alpha"])}),
+                            ("b_", ms_b, out["b_focals"], alphas),
+                            ("c_", ms_c, [500.0] * m_cams(ms_c), {})):
+        dims = {im.camera_id: (im.width, im.height) for im in m.images}
+        cams = {c: CameraModel(float(foc[c]), dims[c][0], dims[c][1], float(al.get(c, 0.0)))
+                for c in sorted(dims)}
+        t0 = time.perf_counter()
+        nk, geo = focal.apply_calibration(m, cams)
+        out[pre + "calib_seconds"] = np.array(time.perf_counter() - t0)
+        out[pre + "cam"] = np.array([[cams[c].focal, cams[c].alpha] for c in sorted(cams)])
+        out[pre + "norm_kps"] = np.concatenate(nk)
+        out[pre + "calib_mats"] = np.stack([np.full((3, 3), np.nan) if g is None else g
+                                            for _, g in geo])
     np.savez_compressed(os.path.join(HERE, "golden_distortion.npz"), **out)
     print({k: v.shape for k, v in out.items()})
     print("scene A alpha", out["a_alpha"], "ref search seconds", out["a_ref_seconds"],

@@ -20,7 +20,8 @@ def _match_set(g, p):
     kp = np.split(g[p + "kp"], np.cumsum(g[p + "kp_len"])[:-1])
     corr = np.split(g[p + "corr"], np.cumsum(g[p + "pair_len"])[:-1])
     homog = g[p + "homography"]
-    images = [SimpleNamespace(camera_id=int(c), width=int(w), height=int(h)) for c, w, h in img]
+    images = [SimpleNamespace(image_id=k, camera_id=int(c), width=int(w), height=int(h))
+              for k, (c, w, h) in enumerate(img)]
     pairs = [SimpleNamespace(i=int(i), j=int(j), correspondences=c,
                              geometry_class=SimpleNamespace(name="HOMOGRAPHY" if h else "FUNDAMENTAL"))
              for (i, j), c, h in zip(g[p + "pair_ij"], corr, homog)]
@@ -109,3 +110,30 @@ def test_undistorted_fundamentals_match_reference(golden, scene):
     for (_, F), R in zip(got, golden[scene + "fund_F"]):
         d = min(np.abs(F - R).max(), np.abs(F + R).max())
         assert d < 1e-7, d
+
+
+@pytest.mark.parametrize("scene", ["a_", "b_", "c_"])
+def test_apply_calibration_matches_reference(golden, scene):
+    """ref/focal.py:175-203 with the pipeline's cameras: normalised keypoints
+    bit-identical (same numpy expressions), every pair's refit essential
+    matrix (scenes a, b) or homography (scene c: all pairs planar) within
+    1e-7 -- E up to sign, H exactly signed (positive trace)."""
+    from paper_2505_04612_b200 import focal
+    ms = _match_set(golden, scene)
+    cams = {}
+    for c, (f, a) in enumerate(golden[scene + "cam"]):
+        im = next(i for i in ms.images if i.camera_id == c)
+        w, h = im.width, im.height
+        cams[c] = SimpleNamespace(focal=float(f), alpha=float(a), cx=w / 2.0, cy=h / 2.0,
+                                  half_diagonal=0.5 * float(np.hypot(w, h)))
+    nk, geo = focal.apply_calibration(ms, cams)
+    assert np.array_equal(np.concatenate(nk), golden[scene + "norm_kps"])
+    ref = golden[scene + "calib_mats"]
+    assert len(geo) == len(ref)
+    homog = golden[scene + "homography"]
+    for (pair, m), r, hg in zip(geo, ref, homog):
+        assert (m is None) == bool(np.isnan(r).any())
+        if m is None:
+            continue
+        d = np.abs(m - r).max() if hg else min(np.abs(m - r).max(), np.abs(m + r).max())
+        assert d < 1e-7, (pair.i, pair.j, d)

@@ -27,3 +27,14 @@ for pre in ("a_", "b_"):
     focal.undistorted_fundamentals(ms2, al)
     t0 = time.perf_counter(); focal.undistorted_fundamentals(ms2, al); dt = time.perf_counter() - t0
     print({"scene": pre, "undistorted_fundamentals_s": dt, "ref_s": float(g[pre + "fund_seconds"])})
+from types import SimpleNamespace
+for pre in ("a_", "b_", "c_"):
+    ms3 = _match_set(g, pre)
+    cams = {}
+    for c, (f, a) in enumerate(g[pre + "cam"]):
+        im = next(i for i in ms3.images if i.camera_id == c)
+        cams[c] = SimpleNamespace(focal=float(f), alpha=float(a), cx=im.width / 2.0, cy=im.height / 2.0,
+                                  half_diagonal=0.5 * float(np.hypot(im.width, im.height)))
+    focal.apply_calibration(ms3, cams)
+    t0 = time.perf_counter(); focal.apply_calibration(ms3, cams); dt = time.perf_counter() - t0
+    print({"scene": pre, "apply_calibration_s": dt, "ref_s": float(g[pre + "calib_seconds"])})
