@@ -417,6 +417,15 @@ int fm_homog_fit(int64_t n_jobs, const int64_t* job_off, const double* p1, const
                  const int32_t* sample_idx, const int64_t* sample_off, double* H_out,
                  void* scratch, size_t scratch_bytes, int64_t n_points, void* stream);
 
+/*
+ * Connected components of the keypoint match graph (build_tracks,
+ * ref/tracks.py:38-56): n_nodes (image, keypoint) ids, n_edges
+ * correspondences u[e] -- v[e].  labels_out[x] = the smallest node id of
+ * x's component.  Synchronises the stream once per hook round.
+ */
+int fm_cc_labels(int32_t n_nodes, int64_t n_edges, const int32_t* u, const int32_t* v,
+                 int32_t* labels_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,4 +71,10 @@ def install(fastmap_module=None):
     from . import focal
     for name in ("undistorted_fundamentals", "apply_calibration"):  # :105, :123
         swap(ref_focal, name, getattr(focal, name))
+    # ref/pipeline.py:178-181 calls tracks.build_tracks / complete_matches
+    ref_tracks = importlib.import_module(fm.__name__ + ".tracks")
+    from . import tracks
+    for name in ("build_tracks", "complete_matches"):
+        swap(ref_tracks, name, getattr(tracks, name))
+    swap(tracks, "TrackSet", ref_tracks.TrackSet)
     return saved

@@ -6,7 +6,8 @@ candidate of every search level, the search_alpha result, and the
 schedule_cameras result of the two-camera scene, a subset-sized pair set
 (M < 16, the non-LMedS branch), and undistorted_fundamentals + the focal
 vote (ref/focal.py:51-172) on both scenes, and apply_calibration
-(ref/focal.py:175-203) on those and on a planar scene (homography pairs).
+(ref/focal.py:175-203) on those and on a planar scene (homography pairs), and
+build_tracks + complete_matches (ref/tracks.py:38-106).
 
     python tests/golden/make_distortion_golden.py      (a minute; not run by pytest)
 """
@@ -20,7 +21,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from fastmap import distortion, focal, synth  # noqa: E402
+from fastmap import distortion, focal, synth, tracks  # noqa: E402
 from fastmap.config import PipelineConfig  # noqa: E402
 from fastmap.model import CameraModel, GeometryClass  # noqa: E402
 
@@ -104,6 +105,38 @@ def main():
         out[pre + "norm_kps"] = np.concatenate(nk)
         out[pre + "calib_mats"] = np.stack([np.full((3, 3), np.nan) if g is None else g
                                             for _, g in geo])
+    # build_tracks + complete_matches (ref/tracks.py:38-106) on A and B, and on
+    # B with a small completion cap (oversized tracks keep their edges)
+    # scene D: scene B thinned (60% of each pair's correspondences, every 4th
+    # pair dropped) plus cross links that merge tracks into same-image
+    # conflicts, so completion has pairs and correspondences to add
+    from fastmap.model import ImagePairMatches, MatchSet
+    rng = np.random.default_rng(7)
+    thin = []
+    for q, p in enumerate(ms_b.pairs):
+        if q % 4 == 3:
+            continue
+        c = p.correspondences[np.sort(rng.choice(len(p.correspondences),
+                                                 int(0.6 * len(p.correspondences)), replace=False))]
+        if q % 5 == 0 and len(c) > 2:
+            c = np.concatenate([c, [[c[0, 0], c[1, 1]]]])
+        thin.append(ImagePairMatches(p.i, p.j, p.geometry_class, c))
+    ms_d = MatchSet(images=ms_b.images, keypoints=ms_b.keypoints, pairs=thin)
+    pack("d_", ms_d, out)
+    out["d_homography"] = np.array([p.geometry_class is GeometryClass.HOMOGRAPHY for p in thin])
+    for pre, m, cap in (("a_", ms, 200), ("b_", ms_b, 200), ("d_", ms_d, 200), ("d3_", ms_d, 4)):
+        t0 = time.perf_counter()
+        ts = tracks.build_tracks(m)
+        done = tracks.complete_matches(ts, m, max_track_size=cap)
+        out[pre + "tracks_seconds"] = np.array(time.perf_counter() - t0)
+        out[pre + "track_len"] = np.array([len(t) for t in ts.tracks], dtype=np.int64)
+        out[pre + "track_nodes"] = np.array([x for t in ts.tracks for x in t], dtype=np.int64)
+        out[pre + "done_ij"] = np.array([[p.i, p.j] for p in done.pairs], dtype=np.int64)
+        out[pre + "done_len"] = np.array([len(p.correspondences) for p in done.pairs], dtype=np.int64)
+        out[pre + "done_corr"] = np.concatenate([p.correspondences for p in done.pairs]).astype(np.int64)
+        out[pre + "done_synth"] = np.array([p.synthetic_from_tracks for p in done.pairs])
+        out[pre + "done_homog"] = np.array([p.geometry_class is GeometryClass.HOMOGRAPHY
+                                            for p in done.pairs])
     np.savez_compressed(os.path.join(HERE, "golden_distortion.npz"), **out)
     print({k: v.shape for k, v in out.items()})
     print("scene A alpha", out["a_alpha"], "ref search seconds", out["a_ref_seconds"],

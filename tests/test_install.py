@@ -23,12 +23,13 @@ def test_install_swaps_the_pipeline_call_sites():
         ref_dist = importlib.import_module("fastmap.distortion")
         ref_two = importlib.import_module("fastmap.twoview")
         ref_focal = importlib.import_module("fastmap.focal")
+        ref_tracks = importlib.import_module("fastmap.tracks")
     except ImportError as exc:  # reference dependencies missing
         pytest.skip(str(exc))
     finally:
         sys.path.remove(REF)
     import paper_2505_04612_b200 as b200
-    from paper_2505_04612_b200 import distortion, epipolar, focal, rotation, translation
+    from paper_2505_04612_b200 import distortion, epipolar, focal, rotation, tracks, translation
     saved = b200.install(fastmap)
     try:
         assert pipeline.irls_refine is epipolar.irls_refine          # ref/pipeline.py:248
@@ -40,6 +41,9 @@ def test_install_swaps_the_pipeline_call_sites():
         assert ref_dist.search_alpha is distortion.search_alpha          # via schedule_cameras
         assert distortion.DegenerateGeometryError is ref_two.DegenerateGeometryError
         assert ref_focal.undistorted_fundamentals is focal.undistorted_fundamentals  # :105
+        assert ref_focal.apply_calibration is focal.apply_calibration  # :123
+        assert ref_tracks.complete_matches is tracks.complete_matches  # :179
+        assert tracks.TrackSet is ref_tracks.TrackSet
     finally:
         for (mod, name), obj in saved.items():
             setattr(sys.modules[mod], name, obj)
