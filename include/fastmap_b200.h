@@ -426,6 +426,16 @@ int fm_homog_fit(int64_t n_jobs, const int64_t* job_off, const double* p1, const
 int fm_cc_labels(int32_t n_nodes, int64_t n_edges, const int32_t* u, const int32_t* v,
                  int32_t* labels_out, void* stream);
 
+/*
+ * Focal voting (ref/focal.py:43-48, :81-120): votes_out[c] = sum over pairs
+ * p of exp((1 - s0/s1) / tau), s the singular values of E = K2^T F_p K1,
+ * K = [[f, 0, cx], [0, f, cy], [0, 0, 1]].  F [n_pairs][9] row-major;
+ * focal [n_cand][n_pairs][2] (image-i side, image-j side) -- the candidate
+ * focal or a known camera's; principal [n_pairs][4] (cx1, cy1, cx2, cy2).
+ */
+int fm_focal_votes(int32_t n_cand, int32_t n_pairs, const double* F, const double* focal,
+                   const double* principal, double tau, double* votes_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

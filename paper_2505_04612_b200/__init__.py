@@ -69,8 +69,10 @@ def install(fastmap_module=None):
     # ref/pipeline.py:105 calls focal.undistorted_fundamentals through the module
     ref_focal = importlib.import_module(fm.__name__ + ".focal")
     from . import focal
-    for name in ("undistorted_fundamentals", "apply_calibration"):  # :105, :123
+    # vote_focal_multi (ref/pipeline.py:106) finds vote_focal through the module
+    for name in ("undistorted_fundamentals", "apply_calibration", "vote_focal"):  # :105, :123
         swap(ref_focal, name, getattr(focal, name))
+    swap(focal, "FocalUnderdeterminedError", ref_focal.FocalUnderdeterminedError)
     # ref/pipeline.py:178-181 calls tracks.build_tracks / complete_matches
     ref_tracks = importlib.import_module(fm.__name__ + ".tracks")
     from . import tracks

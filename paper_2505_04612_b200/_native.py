@@ -124,6 +124,7 @@ SIGNATURES = {
     "fm_depth_counts_batch": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I64, _P, _P]),
     "fm_fund_scratch_bytes": (ctypes.c_size_t, [_I64]),
     "fm_cc_labels": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
+    "fm_focal_votes": (ctypes.c_int, [_I32, _I32, _P, _P, _P, ctypes.c_double, _P, _P]),
     "fm_homog_fit": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _I64, _P]),
     "fm_fund_score": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t,
                                      _I64, _P]),

@@ -782,3 +782,99 @@ int fm_homog_fit(int64_t n_jobs, const int64_t* job_off, const double* p1, const
 }
 
 }  // extern "C"
+
+// ======================================================================
+// Focal voting (ref/focal.py:43-48, :81-120): votes[c] = sum over pairs p of
+// exp((1 - s0/s1) / tau), s the singular values of E = K2^T F_p K1 with the
+// candidate's K on the unknown side(s).  Block per candidate, thread per
+// pair, fixed-order block sum; singular values by one-sided Jacobi (the
+// column norms of E V).
+// ======================================================================
+namespace fm {
+namespace {
+
+__global__ void focal_votes_kernel(int32_t P, const double* __restrict__ F,
+                                   const double* __restrict__ focal /* [C][P][2] */,
+                                   const double* __restrict__ pp /* [P][4] cx1 cy1 cx2 cy2 */,
+                                   double tau, double* __restrict__ votes) {
+  __shared__ double red[kWarps];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int p = threadIdx.x; p < P; p += kThreads) {
+    const double f1 = focal[(2 * (int64_t)c * P) + 2 * p], f2 = focal[(2 * (int64_t)c * P) + 2 * p + 1];
+    const double K1[9] = {f1, 0.0, pp[4 * p], 0.0, f1, pp[4 * p + 1], 0.0, 0.0, 1.0};
+    const double K2[9] = {f2, 0.0, pp[4 * p + 2], 0.0, f2, pp[4 * p + 3], 0.0, 0.0, 1.0};
+    const double* Fp = F + 9 * (int64_t)p;
+    double G[9], W[3][3];
+    for (int i = 0; i < 3; ++i)  // G = F K1
+      for (int l = 0; l < 3; ++l) {
+        double s = 0.0;
+        for (int k = 0; k < 3; ++k) s += Fp[i * 3 + k] * K1[k * 3 + l];
+        G[i * 3 + l] = s;
+      }
+    for (int i = 0; i < 3; ++i)  // E = K2^T G
+      for (int l = 0; l < 3; ++l) {
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j) s += K2[j * 3 + i] * G[j * 3 + l];
+        W[i][l] = s;
+      }
+    bool finite = true;
+    for (int i = 0; i < 3; ++i)
+      for (int l = 0; l < 3; ++l) finite &= isfinite(W[i][l]);
+    double sv[3] = {NAN, NAN, NAN};
+    if (finite) {
+      for (int sweep = 0; sweep < 30; ++sweep) {
+        bool rotated = false;
+        for (int a = 0; a < 2; ++a)
+          for (int b = a + 1; b < 3; ++b) {
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int k = 0; k < 3; ++k) {
+              al += W[k][a] * W[k][a];
+              be += W[k][b] * W[k][b];
+              ga += W[k][a] * W[k][b];
+            }
+            if (ga == 0.0 || fabs(ga) <= 1e-17 * sqrt(al * be)) continue;
+            rotated = true;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            for (int k = 0; k < 3; ++k) {
+              const double wa = W[k][a], wb = W[k][b];
+              W[k][a] = cs * wa - sn * wb;
+              W[k][b] = sn * wa + cs * wb;
+            }
+          }
+        if (!rotated) break;
+      }
+      for (int j = 0; j < 3; ++j) sv[j] = sqrt(W[0][j] * W[0][j] + W[1][j] * W[1][j] + W[2][j] * W[2][j]);
+    }
+    // s0 >= s1 >= s2
+    double s0 = fmax(sv[0], fmax(sv[1], sv[2])), s2 = fmin(sv[0], fmin(sv[1], sv[2]));
+    double s1 = sv[0] + sv[1] + sv[2] - s0 - s2;
+    const double ratio = s0 / fmax(s1, 1e-300);
+    acc += exp((1.0 - ratio) / tau);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int k = 0; k < kWarps; ++k) v += red[k];
+    votes[c] = v;
+  }
+}
+
+}  // namespace
+}  // namespace fm
+
+extern "C" int fm_focal_votes(int32_t n_cand, int32_t n_pairs, const double* F,
+                              const double* focal, const double* principal, double tau,
+                              double* votes_out, void* stream) {
+  FM_REQUIRE(n_cand >= 0 && n_pairs >= 0 && tau > 0, "bad focal-vote arguments");
+  if (n_cand == 0) return FM_OK;
+  FM_REQUIRE(votes_out && (n_pairs == 0 || (F && focal && principal)), "null focal-vote pointer");
+  fm::focal_votes_kernel<<<(unsigned)n_cand, fm::kThreads, 0, fm::as_stream(stream)>>>(
+      n_pairs, F, focal, principal, tau, votes_out);
+  FM_LAUNCHED(focal_votes_kernel);
+  return FM_OK;
+}

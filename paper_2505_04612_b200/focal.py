@@ -5,13 +5,63 @@
 ``undistorted_fundamentals`` undistorts every fundamental pair's keypoints
 with its camera's alpha (the reference's numpy expressions) and fits all
 pairs' robust fundamental matrices in one device launch
-(``distortion.estimate_fundamental_batch`` -> ``fm_fund_score``).  The
-focal vote itself (``vote_focal``, a few 3x3 SVDs per candidate) stays the
-reference's.
+(``distortion.estimate_fundamental_batch`` -> ``fm_fund_score``).
+``vote_focal`` scores every FoV candidate against every fundamental matrix
+in one launch (``fm_focal_votes``); the candidate focals are computed with
+the reference's numpy expressions.  ``apply_calibration`` refits all pairs
+in two launches (F and H).
 """
 
-import numpy as np
 
+class FocalUnderdeterminedError(ValueError):
+    """ref/focal.py:16-17 (install() rebinds it to the reference class)."""
+
+
+def fov_to_focal(fov_deg, width):
+    """ref/focal.py:20-21."""
+    return (width / 2.0) / np.tan(np.radians(fov_deg) / 2.0)
+
+
+def vote_focal(fundamentals, width, height, cfg, known=None, images=None, camera_id=None):
+    """ref/focal.py:81-120: (focal_px, fov_deg, votes) -- the FoV candidate
+    whose K makes the fundamentals most essential-like, summed validity
+    exp((1 - s0/s1) / tau) per candidate."""
+    if not fundamentals:
+        raise FocalUnderdeterminedError("focal underdetermined: no fundamental matrices")
+    fovs = np.linspace(cfg.fov_min_deg, cfg.fov_max_deg, cfg.focal_samples)
+    known = known or {}
+    C, P = len(fovs), len(fundamentals)
+    focal = np.empty((C, P, 2))
+    principal = np.empty((P, 4))
+    for q, (pair, _) in enumerate(fundamentals):
+        if images is None or camera_id is None:
+            focal[:, q, 0] = focal[:, q, 1] = fov_to_focal(fovs, width)
+            principal[q] = (width / 2.0, height / 2.0, width / 2.0, height / 2.0)
+            continue
+        for side, img_id in enumerate((pair.i, pair.j)):
+            im = images[img_id]
+            if im.camera_id == camera_id:
+                focal[:, q, side] = fov_to_focal(fovs, im.width)
+            else:
+                focal[:, q, side] = known[im.camera_id]
+            principal[q, 2 * side:2 * side + 2] = (im.width / 2.0, im.height / 2.0)
+    device = N.require_cuda()
+    F = torch.as_tensor(np.ascontiguousarray(np.stack([F for _, F in fundamentals]), dtype=np.float64),
+                        device=device)
+    foc = torch.as_tensor(focal, device=device)
+    pp = torch.as_tensor(principal, device=device)
+    votes = torch.empty(C, dtype=torch.float64, device=device)
+    N.check(N.lib().fm_focal_votes(C, P, N.ptr(F), N.ptr(foc), N.ptr(pp), float(cfg.tau),
+                                   N.ptr(votes), N.stream_handle()))
+    votes = votes.cpu().numpy()
+    best = int(np.argmax(votes))
+    return float(fov_to_focal(fovs[best], width)), float(fovs[best]), votes
+
+
+import numpy as np
+import torch
+
+from . import _native as N
 from .distortion import (_is_homography, estimate_fundamental_batch, estimate_homography_batch,
                          undistort_normalized)
 
@@ -73,4 +123,5 @@ def apply_calibration(match_set, cameras):
     return norm_kps, [(pair, m) for pair, m in zip(match_set.pairs, mats)]
 
 
-__all__ = ["undistorted_fundamentals", "apply_calibration"]
+__all__ = ["FocalUnderdeterminedError", "fov_to_focal", "vote_focal", "undistorted_fundamentals",
+           "apply_calibration"]

@@ -86,6 +86,12 @@ def main():
         out[pre + "fund_F"] = np.stack([F for _, F in fund])
         foc, fb = focal.vote_focal_multi(m, fund, cfg)
         out[pre + "focals"] = np.array([foc[c] for c in sorted(foc)])
+        im0 = m.images[0]
+        out[pre + "votes"] = focal.vote_focal(fund, im0.width, im0.height, cfg)[2]
+        if pre == "b_":  # the cross-camera form: camera 1 against camera 0's focal
+            out[pre + "votes_cam1"] = focal.vote_focal(
+                focal._pairs_for_camera(fund, m.images, 1, {0: foc[0]}), m.images[0].width,
+                m.images[0].height, cfg, known={0: foc[0]}, images=m.images, camera_id=1)[2]
     # apply_calibration (ref/focal.py:175-203) on A, B and a planar
     # scene C (homography pairs), with the cameras the pipeline would build
     ms_c, _ = synth.generate(synth.SynthSpec(n_images=8, n_points=200, seed=2,

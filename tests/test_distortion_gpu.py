@@ -137,3 +137,30 @@ def test_apply_calibration_matches_reference(golden, scene):
             continue
         d = np.abs(m - r).max() if hg else min(np.abs(m - r).max(), np.abs(m + r).max())
         assert d < 1e-7, (pair.i, pair.j, d)
+
+
+def test_focal_votes_match_reference(golden):
+    """ref/focal.py:81-120: all 100 FoV candidate votes within 1e-9 and the
+    same winner -- one camera (scene a) and the cross-camera form (scene b,
+    camera 1 voted against camera 0's known focal)."""
+    from paper_2505_04612_b200 import focal
+    cfg = SimpleNamespace(fov_min_deg=20.0, fov_max_deg=160.0, focal_samples=100, tau=0.01)
+    ms = _match_set(golden, "a_")
+    fund = focal.undistorted_fundamentals(ms, {0: float(golden["a_alpha"])})
+    im0 = ms.images[0]
+    f, fov, votes = focal.vote_focal(fund, im0.width, im0.height, cfg)
+    np.testing.assert_allclose(votes, golden["a_votes"], rtol=1e-9, atol=1e-300)
+    assert f == pytest.approx(float(golden["a_focals"][0]), rel=1e-15)
+    ms = _match_set(golden, "b_")
+    al = {c: float(a) for c, a in enumerate(golden["b_alphas"])}
+    fund = focal.undistorted_fundamentals(ms, al)
+    f0 = float(golden["b_focals"][0])
+    mine = [(p, F) for p, F in fund
+            if {ms.images[p.i].camera_id, ms.images[p.j].camera_id} <= {0, 1}
+            and 1 in (ms.images[p.i].camera_id, ms.images[p.j].camera_id)]
+    _, _, votes = focal.vote_focal(mine, ms.images[0].width, ms.images[0].height, cfg,
+                                   known={0: f0}, images=ms.images, camera_id=1)
+    np.testing.assert_allclose(votes, golden["b_votes_cam1"], rtol=1e-9, atol=1e-300)
+    assert int(np.argmax(votes)) == int(np.argmax(golden["b_votes_cam1"]))
+    with pytest.raises(focal.FocalUnderdeterminedError):
+        focal.vote_focal([], 640, 480, cfg)

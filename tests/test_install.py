@@ -42,6 +42,7 @@ def test_install_swaps_the_pipeline_call_sites():
         assert distortion.DegenerateGeometryError is ref_two.DegenerateGeometryError
         assert ref_focal.undistorted_fundamentals is focal.undistorted_fundamentals  # :105
         assert ref_focal.apply_calibration is focal.apply_calibration  # :123
+        assert ref_focal.vote_focal is focal.vote_focal  # via vote_focal_multi, :106
         assert ref_tracks.complete_matches is tracks.complete_matches  # :179
         assert tracks.TrackSet is ref_tracks.TrackSet
     finally:
