@@ -72,7 +72,7 @@ def _jobs(alphas, match_set, pairs, camera_id, known_alphas):
     kp_i = np.asarray(kp_i, dtype=np.float64)
     kp_j = np.asarray(kp_j, dtype=np.float64)
     lens = np.array([len(p.correspondences) for p in pairs], dtype=np.int64)
-    start = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    seg = np.repeat(np.arange(len(pairs)), lens)  # pair of every point
     geo_i = [_geom(match_set, p.i) for p in pairs]
     geo_j = [_geom(match_set, p.j) for p in pairs]
     c_i = np.repeat(np.stack([g[0] for g in geo_i]), lens, axis=0)
@@ -95,7 +95,7 @@ def _jobs(alphas, match_set, pairs, camera_id, known_alphas):
         u_i = undistort_normalized(xn_i, a_i) * s_i + c_i
         u_j = undistort_normalized(xn_j, a_j) * s_j + c_j
         ok = np.all(np.isfinite(u_i), axis=1) & np.all(np.isfinite(u_j), axis=1)
-        n_ok = np.add.reduceat(ok.astype(np.int64), start) if len(ok) else np.zeros(0, np.int64)
+        n_ok = np.bincount(seg, weights=ok, minlength=len(pairs)).astype(np.int64)
         use = np.repeat(n_ok >= 8, lens) & ok
         job_cand.append(np.full(int((n_ok >= 8).sum()), c, dtype=np.int64))
         job_len.append(n_ok[n_ok >= 8])

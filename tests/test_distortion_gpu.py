@@ -164,3 +164,18 @@ def test_focal_votes_match_reference(golden):
     assert int(np.argmax(votes)) == int(np.argmax(golden["b_votes_cam1"]))
     with pytest.raises(focal.FocalUnderdeterminedError):
         focal.vote_focal([], 640, 480, cfg)
+
+
+def test_empty_and_short_pairs_are_skipped(golden):
+    """Pairs with 0 or < 8 valid correspondences contribute nothing (as the
+    reference's `ok.sum() < 8: continue`), wherever they sit in the list."""
+    from paper_2505_04612_b200 import distortion as D
+    ms = _match_set(golden, "a_")
+    pairs = [ms.pairs[k] for k in golden["a_ready"]]
+    empty = SimpleNamespace(i=pairs[0].i, j=pairs[0].j, geometry_class=pairs[0].geometry_class,
+                            correspondences=np.zeros((0, 2), dtype=np.int64))
+    short = SimpleNamespace(i=pairs[1].i, j=pairs[1].j, geometry_class=pairs[1].geometry_class,
+                            correspondences=pairs[1].correspondences[:5])
+    cands = golden["a_cands"][0]
+    got = D.score_alpha_batch(cands, ms, [empty] + pairs + [short, empty])
+    np.testing.assert_allclose(got, golden["a_scores"][0], rtol=1e-8)
