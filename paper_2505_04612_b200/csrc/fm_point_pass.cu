@@ -131,7 +131,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #endif
 constexpr int kRing = FM_HOT_RING;  // stages per lane
 constexpr int kUnroll = FM_HOT_UNROLL;  // main-loop unroll (points in flight per lane = 4 x kUnroll)
-constexpr int kGrpWarps = 4;  // warps per block (8 or 16: slower, measured)
+#ifndef FM_GRP_WARPS
+#define FM_GRP_WARPS 4
+#endif
+constexpr int kGrpWarps = FM_GRP_WARPS;  // warps per block (2, 8 or 16: slower, measured)
 constexpr int kBlkSlots = 16;       // slots per group iteration (= slot alignment)
 
 __device__ __forceinline__ float and_mask(float x, unsigned m) {
