@@ -61,7 +61,8 @@ def main():
         ix, isrc = h.index("Instructions Executed"), h.index("Source")
         ops = collections.Counter()
         for r in src[2:]:
-            if len(r) > ix and r[isrc].split():
+            # multi-kernel reports repeat the header row per kernel: skip it
+            if len(r) > ix and r[isrc].split() and (r[ix] or "0").isdigit():
                 t = r[isrc].split()
                 op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
                 ops[op] += int(r[ix] or 0)
