@@ -99,3 +99,20 @@ def test_tracks_and_completion_match_reference(scene, src, cap):
                           g[scene + "done_corr"])
     assert [p.synthetic_from_tracks for p in done.pairs] == g[scene + "done_synth"].tolist()
     assert [p.geometry_class is GC.HOMOGRAPHY for p in done.pairs] == g[scene + "done_homog"].tolist()
+
+
+def test_integration_stub_components():
+    """The fm_cc_labels ctypes stub in INTEGRATION.md works as written."""
+    import re
+    from paper_2505_04612_b200 import _native
+    from tests.conftest import ROOT
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"could replace its union-find.*?```python\n(.*?)```", text, re.S).group(1)
+    os.environ["FASTMAP_B200_LIB"] = _native.lib_path()
+    ns = {}
+    try:
+        exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    finally:
+        os.environ.pop("FASTMAP_B200_LIB", None)
+    lab = ns["component_labels_gpu"](7, [0, 1, 4, 6], [1, 2, 5, 4])
+    assert lab.tolist() == [0, 0, 0, 3, 4, 4, 4]
