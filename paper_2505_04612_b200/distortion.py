@@ -83,26 +83,27 @@ def _jobs(alphas, match_set, pairs, camera_id, known_alphas):
     cam_j = np.array([match_set.images[p.j].camera_id for p in pairs])
     xn_i = (kp_i - c_i) / s_i
     xn_j = (kp_j - c_j) / s_j
-    job_cand, job_len, p1s, p2s = [], [], [], []
-    for c, alpha in enumerate(alphas):
-        def alpha_for(cam):
-            if camera_id is None or cam == camera_id:
-                return alpha
-            return known_alphas[cam]
+    # all candidates at once: (C, n, 2); every element sees the same operations
+    def alpha_for(alpha, cam):
+        if camera_id is None or cam == camera_id:
+            return alpha
+        return known_alphas[cam]
 
-        a_i = np.repeat(np.array([alpha_for(k) for k in cam_i], dtype=np.float64), lens)[:, None]
-        a_j = np.repeat(np.array([alpha_for(k) for k in cam_j], dtype=np.float64), lens)[:, None]
-        u_i = undistort_normalized(xn_i, a_i) * s_i + c_i
-        u_j = undistort_normalized(xn_j, a_j) * s_j + c_j
-        ok = np.all(np.isfinite(u_i), axis=1) & np.all(np.isfinite(u_j), axis=1)
-        n_ok = np.bincount(seg, weights=ok, minlength=len(pairs)).astype(np.int64)
-        use = np.repeat(n_ok >= 8, lens) & ok
-        job_cand.append(np.full(int((n_ok >= 8).sum()), c, dtype=np.int64))
-        job_len.append(n_ok[n_ok >= 8])
-        p1s.append(u_i[use] / s_i[use])
-        p2s.append(u_j[use] / s_i[use])
-    return (np.concatenate(job_cand), np.concatenate(job_len), np.concatenate(p1s),
-            np.concatenate(p2s))
+    a_i = np.array([[alpha_for(a, k) for k in cam_i] for a in alphas], dtype=np.float64)
+    a_j = np.array([[alpha_for(a, k) for k in cam_j] for a in alphas], dtype=np.float64)
+    a_i = np.repeat(a_i, lens, axis=1)[:, :, None]
+    a_j = np.repeat(a_j, lens, axis=1)[:, :, None]
+    u_i = undistort_normalized(xn_i[None], a_i) * s_i[None] + c_i[None]
+    u_j = undistort_normalized(xn_j[None], a_j) * s_j[None] + c_j[None]
+    ok = np.all(np.isfinite(u_i), axis=2) & np.all(np.isfinite(u_j), axis=2)  # (C, n)
+    C, P = len(alphas), len(pairs)
+    n_ok = np.bincount((np.arange(C)[:, None] * P + seg[None, :]).ravel(), weights=ok.ravel(),
+                       minlength=C * P).astype(np.int64).reshape(C, P)
+    good = n_ok >= 8
+    use = ok & np.repeat(good, lens, axis=1)
+    s_full = np.broadcast_to(s_i[None], (C,) + s_i.shape)
+    return (np.nonzero(good)[0].astype(np.int64), n_ok[good], u_i[use] / s_full[use],
+            u_j[use] / s_full[use])
 
 
 def fit_jobs(lens, p1, p2, want_F=False):
