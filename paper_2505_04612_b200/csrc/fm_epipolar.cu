@@ -28,7 +28,7 @@ constexpr int kPG = 24;          // per-pair gradient record: gRi 9, gRj 9, gdc 
 constexpr int kMaxSteps = 4096;  // steps per fm_epi_adam_steps call (bias-correction table)
 
 struct EpiScratch {
-  double* R;      // [N][9]
+  double* R;      // [N][9] rotations, then [n_cameras] focal scales exp(-log_focal)
   double* pg;     // [kPG][P]
   double* cpart;  // [n_cam_chunks]
   double* lpart;  // [loss blocks]
@@ -40,7 +40,7 @@ int loss_blocks(int64_t P) { return (int)std::min<int64_t>(std::max<int64_t>(cei
 
 size_t scratch_need(const fm_pair_graph& g) {
   size_t b = 0;
-  b += scratch_round((size_t)g.n_images * 9 * sizeof(double));
+  b += scratch_round(((size_t)g.n_images * 9 + std::max(g.n_cameras, 1)) * sizeof(double));
   b += scratch_round((size_t)g.n_pairs * kPG * sizeof(double));
   b += scratch_round((size_t)std::max(g.n_cam_chunks, 1) * sizeof(double));
   b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
@@ -51,7 +51,7 @@ size_t scratch_need(const fm_pair_graph& g) {
 
 bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
   Scratch sc(p, n);
-  s.R = sc.take<double>((size_t)g.n_images * 9);
+  s.R = sc.take<double>((size_t)g.n_images * 9 + std::max(g.n_cameras, 1));
   s.pg = sc.take<double>((size_t)g.n_pairs * kPG);
   s.cpart = sc.take<double>((size_t)std::max(g.n_cam_chunks, 1));
   s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
@@ -61,15 +61,29 @@ bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
 }
 
 // ------------------------------------------------------------------ kernels
+// Per image: R from the 6D parameters; per camera (n_cam > 0 when focals
+// are refined): the focal scale exp(-log_focal) after the rotations, so the
+// pair kernels read it instead of evaluating two fp64 exps per pair.
 __global__ void image_rot_kernel(const double* __restrict__ params, int n, double* __restrict__ R,
-                                 int32_t* flag) {
+                                 int32_t* flag, int n_cam) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n_cam) R[9 * n + k] = exp(-params[9 * n + k]);
   if (k >= n) return;
   double Rk[9];
   const int code = rot6d_to_R(params + 6 * k, Rk);
   if (code) raise_flag(flag, code);
 #pragma unroll
   for (int q = 0; q < 9; ++q) R[9 * k + q] = Rk[q];
+}
+
+int launch_image_rot(const fm_pair_graph& g, const double* params, double* R, int32_t* flag,
+                     cudaStream_t st) {
+  const int n_cam = g.refine_focal ? g.n_cameras : 0;
+  const int n = std::max(g.n_images, n_cam);
+  if (n == 0) return FM_OK;
+  image_rot_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(params, g.n_images, R, flag, n_cam);
+  FM_LAUNCHED(image_rot_kernel);
+  return FM_OK;
 }
 
 // Forward geometry of one image pair (ref/epipolar.py:109-138).
@@ -95,8 +109,8 @@ __device__ __forceinline__ void pair_forward(const fm_pair_graph& g, const doubl
   const double* cj = params + 6 * N + 3 * j;
   essential(f.Ri, f.Rj, ci, cj, f.dc, f.t, f.Rrel, f.E);
   if (g.refine_focal) {
-    f.di = exp(-params[9 * N + g.pair_ci[n]]);
-    f.dj = exp(-params[9 * N + g.pair_cj[n]]);
+    f.di = R[9 * N + g.pair_ci[n]];  // exp(-log_focal), image_rot_kernel / cam_finalise
+    f.dj = R[9 * N + g.pair_cj[n]];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -299,7 +313,7 @@ struct AdamArgs {
 constexpr int kReduceBlock = 64;  // 2 warps: spreads small image counts over all SMs
 
 template <bool ADAM>
-__device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params,
+__device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params, double* R,
                              const double* __restrict__ cpart, double* __restrict__ grad,
                              const AdamArgs& ad, int32_t* flag) {
   // Executed by the last camera-chunk block: warp per camera, fixed-order
@@ -322,6 +336,7 @@ __device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params
     const double lr = ad.sched[0];
     const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
     adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+    R[9 * g.n_images + c] = exp(-params[idx]);  // the focal scale the next step's pairs read
   }
 }
 
@@ -365,7 +380,7 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     __syncthreads();
     if (!last) return;
     __threadfence();
-    cam_finalise<ADAM>(g, params, cpart, grad, ad, flag);
+    cam_finalise<ADAM>(g, params, R, cpart, grad, ad, flag);
     if (threadIdx.x == 0) *ticket = 0u;  // ready for the next step
     return;
   }
@@ -586,10 +601,7 @@ int fm_epi_pair_ghat(const fm_pair_graph* g, const double* params, double* ghat,
   EpiScratch s;
   FM_REQUIRE(carve(*g, scratch, scratch_bytes, s), "epipolar scratch too small");
   cudaStream_t st = as_stream(stream);
-  if (g->n_images > 0) {
-    image_rot_kernel<<<(unsigned)ceil_div(g->n_images, 128), 128, 0, st>>>(params, g->n_images, s.R, flag);
-    FM_LAUNCHED(image_rot_kernel);
-  }
+  if (int rc = launch_image_rot(*g, params, s.R, flag, st)) return rc;
   if (g->n_pairs > 0) {
     pair_ghat_kernel<<<(unsigned)ceil_div(g->n_pairs, 128), 128, 0, st>>>(*g, params, s.R, ghat);
     FM_LAUNCHED(pair_ghat_kernel);
@@ -610,10 +622,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   const size_t n_grad = (size_t)9 * N + (g->refine_focal ? g->n_cameras : 0);
   set_sched_kernel<<<1, 1, 0, st>>>(s.sched, 0.0, scale, s.ticket);
   FM_LAUNCHED(set_sched_kernel);
-  if (N > 0) {
-    image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
-    FM_LAUNCHED(image_rot_kernel);
-  }
+  if (int rc = launch_image_rot(*g, params, s.R, flag, st)) return rc;
   if (P == 0) {
     FM_CUDA(cudaMemsetAsync(grad_out, 0, n_grad * sizeof(double), st));
     FM_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(double), st));
@@ -652,12 +661,8 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
   FM_REQUIRE(carve(*g, scratch, scratch_bytes, s), "epipolar scratch too small");
   cudaStream_t st = as_stream(stream);
   if (n_steps == 0) return FM_OK;
-  const int N = g->n_images;
   FM_CUDA(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned int), st));
-  if (N > 0) {
-    image_rot_kernel<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(params, N, s.R, flag);
-    FM_LAUNCHED(image_rot_kernel);
-  }
+  if (int rc = launch_image_rot(*g, params, s.R, flag, st)) return rc;
   for (int32_t done = 0; done < n_steps;) {
     const int chunk = std::min<int32_t>(n_steps - done, kMaxSteps);
     // schedule: lr, 2/Z, and the bias corrections 1 - beta^t computed with the
