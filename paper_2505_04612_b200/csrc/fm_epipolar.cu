@@ -362,6 +362,9 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     if (ADAM && *flag) return;
     double acc = 0;
     const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
+    // unrolled: the two dependent loads of several incidences in flight
+    // together (same per-thread accumulation order)
+#pragma unroll 8
     for (int e = lo + threadIdx.x; e < hi; e += kReduceBlock) {
       const int inc = g.cam_inc[e];
       acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
