@@ -481,26 +481,10 @@ def translation_bench(device, stream, sharded=False):
     import torch
     from paper_2505_04612_b200 import parallel as P_
     from paper_2505_04612_b200 import translation as T
-    rng = np.random.default_rng(0)
+    from paper_2505_04612_b200.scenes import translation_graph_c3
     n, m = 2000, 200_000
-    c = rng.normal(size=(n, 3))
-    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], axis=1)
-    extra = set()
-    while len(extra) < m - n:
-        a = rng.integers(0, n, size=(m, 2))
-        for i, j in a:
-            if i != j:
-                extra.add((min(i, j), max(i, j)))
-            if len(extra) >= m - n:
-                break
-    e = np.concatenate([np.sort(ring, axis=1), np.array(sorted(extra))])
-    d = c[e[:, 1]] - c[e[:, 0]]
-    d /= np.linalg.norm(d, axis=1, keepdims=True)
-    d += rng.normal(scale=np.radians(1.0), size=d.shape)
-    bad = rng.random(m) < 0.05
-    d[bad] = rng.normal(size=(bad.sum(), 3))
-    d /= np.linalg.norm(d, axis=1, keepdims=True)
-    g = T.DirectionGraph(n=n, edges_i=e[:, 0], edges_j=e[:, 1], directions=d)
+    ei, ej, d, _ = translation_graph_c3(n, m)
+    g = T.DirectionGraph(n=n, edges_i=ei, edges_j=ej, directions=d)
 
     class C:
         translation_lr, translation_steps, translation_inits = 1e-3, 6000, 16

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 2
+#define FM_ABI_VERSION 3
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -99,6 +99,13 @@ typedef struct fm_point_store {
    * NULL = derived into scratch on every pass. */
   int32_t* item_desc;
   int64_t slot_align;           /* alignment of pair_off (slots): 4 or a multiple of 16 */
+  /* [n_slots][3] fp64 (x, y, z) columns or NULL.  When set, every pass reads
+   * the caller's fp64 coordinates (the API functions precompute_weights,
+   * current_residuals and epipolar_loss take fp64 arrays,
+   * ref/epipolar.py:46-59, :141-160, :251-255) through the generic kernel;
+   * x1/x2/x1z/x2z may then be NULL.  Moment passes need FM_PASS_F64. */
+  const double* x1d;
+  const double* x2d;
 } fm_point_store;
 
 /* Fill store->item_desc from the pair / item arrays (one small kernel). */
@@ -257,8 +264,13 @@ int fm_adam_step(double* params, double* adam_m, double* adam_v,
 /*
  * DirectionGraph (ref/translation.py:104-109) plus a node incidence list
  * node_inc[node_off[v] .. node_off[v+1]) of (edge << 1) | side, side 0 = v is
- * the edge's i, sorted by edge.  Centres of B independent runs are stored
- * node-major [n][B][3] fp64 so one gather serves all runs.
+ * the edge's i.  Per node the list holds the edges where v is j (side 1) by
+ * ascending edge id, then the edges where v is i (side 0) by ascending edge
+ * id: the order of the reference's np.add.at scatter
+ * (ref/translation.py:123-124).  The kernels fold in this order, which makes
+ * every loss, gradient and trajectory bitwise the reference's.  Centres of B
+ * independent runs are stored node-major [n][B][3] fp64 so one gather serves
+ * all runs.
  */
 typedef struct fm_dir_graph {
   int32_t n_nodes;

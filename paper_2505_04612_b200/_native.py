@@ -44,7 +44,7 @@ FM_QUAD_MOM64 = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
-ABI_VERSION = 2
+ABI_VERSION = 3
 _F64 = ctypes.c_double
 _SZ = ctypes.c_size_t
 
@@ -53,7 +53,7 @@ class PointStore(ctypes.Structure):
     _fields_ = [("n_pairs", _I64), ("n_slots", _I64), ("n_items", _I64), ("chunk", _I64),
                 ("pair_off", _P), ("pair_len", _P), ("pair_item_off", _P), ("item_pair", _P),
                 ("x1", _P), ("x2", _P), ("x1z", _P), ("x2z", _P), ("active", _P),
-                ("item_desc", _P), ("slot_align", _I64)]
+                ("item_desc", _P), ("slot_align", _I64), ("x1d", _P), ("x2d", _P)]
 
 
 class PassOut(ctypes.Structure):

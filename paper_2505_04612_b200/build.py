@@ -38,18 +38,32 @@ def _stale():
 
 
 def build(force=False, verbose=False, extra=(), out=None):
-    """Compile every CUDA source into LIB_PATH (skipped when up to date)."""
+    """Compile every CUDA source into LIB_PATH (skipped when up to date).
+    The translation units compile in parallel (one nvcc per source), then
+    link into one shared library."""
     if out is None and not force and not _stale():
         return LIB_PATH
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     target = out or LIB_PATH
     tmp = target + ".tmp"
-    cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-           "-Xcompiler", "-fPIC", "-cudart", "static",
-           "-I", os.path.join(REPO_DIR, "include"),
-           *extra, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-I", os.path.join(REPO_DIR, "include"), *extra]
+    with tempfile.TemporaryDirectory() as td:
+        objs = [os.path.join(td, s.replace(".cu", ".o")) for s in SOURCES]
+        cmds = [[nvcc_path(), *flags, "-c", os.path.join(CSRC, s), "-o", o]
+                for s, o in zip(SOURCES, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), file=sys.stderr)
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+            procs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+        for c, p in zip(cmds, procs):
+            sys.stderr.write(p.stderr)
+            if p.returncode:
+                raise subprocess.CalledProcessError(p.returncode, c)
+        subprocess.run([nvcc_path(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs],
+                       check=True)
     os.replace(tmp, target)
     return target
 

@@ -630,7 +630,11 @@ point_pass_hot_mixed(const fm_point_store s, const double* __restrict__ ghat, co
 // -------------------------------------------------------------- generic kernel
 // API modes: optional z columns, fp64 moments, caller-given residual weights,
 // residual output, mask-free sweeps.  Plain scalar code; not on the hot loop.
-template <bool HOMOG, bool F64, unsigned MODE>
+// COORD: kXY32 = fp32 (x, y), z = 1; kXYZ32 = fp32 (x, y) + z columns;
+// kXYZ64 = the caller's fp64 (x, y, z) (x1d / x2d).
+enum Coord { kXY32 = 0, kXYZ32 = 1, kXYZ64 = 2 };
+
+template <int COORD, bool F64, unsigned MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 point_pass_generic(const fm_point_store s, const double* __restrict__ ghat,
                    const double* __restrict__ res_in, const double thr,
@@ -683,10 +687,16 @@ point_pass_generic(const fm_point_store s, const double* __restrict__ ghat,
         const bool valid = sl < hi;
         const bool act = valid && ((bits >> k) & 1u);
         if (!valid) continue;
-        const double a = s.x1[2 * sl], bb = s.x1[2 * sl + 1];
-        const double c = s.x2[2 * sl], d = s.x2[2 * sl + 1];
-        const double e = HOMOG ? (double)s.x1z[sl] : 1.0;
-        const double f = HOMOG ? (double)s.x2z[sl] : 1.0;
+        double a, bb, c, d, e, f;
+        if (COORD == kXYZ64) {
+          a = s.x1d[3 * sl], bb = s.x1d[3 * sl + 1], e = s.x1d[3 * sl + 2];
+          c = s.x2d[3 * sl], d = s.x2d[3 * sl + 1], f = s.x2d[3 * sl + 2];
+        } else {
+          a = s.x1[2 * sl], bb = s.x1[2 * sl + 1];
+          c = s.x2[2 * sl], d = s.x2[2 * sl + 1];
+          e = COORD == kXYZ32 ? (double)s.x1z[sl] : 1.0;
+          f = COORD == kXYZ32 ? (double)s.x2z[sl] : 1.0;
+        }
         double r = 0.0;
         if (kNeedR) {
           const double y0 = fma(G[0], a, fma(G[1], bb, G[2] * e));
@@ -926,12 +936,12 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
   return launch_hot_l<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);
 }
 
-template <bool HOMOG, bool F64, unsigned MODE>
+template <int COORD, bool F64, unsigned MODE>
 int launch_generic(const fm_point_store& s, double thr, const double* ghat, const double* res_in,
                    const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
                    cudaStream_t stream) {
   const int64_t blocks = ceil_div(s.n_items, kWarpsPerBlock);
-  point_pass_generic<HOMOG, F64, MODE><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, stream>>>(
+  point_pass_generic<COORD, F64, MODE><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, stream>>>(
       s, ghat, res_in, thr, prev_active, out, part);
   FM_LAUNCHED(point_pass_generic);
   if (s.n_items > s.n_pairs) {
@@ -969,12 +979,12 @@ constexpr unsigned kIrlsM = FM_PASS_MOMENTS | FM_PASS_IRLS;
   X(FM_PASS_MOMENTS | FM_PASS_RES_IN)                                \
   X(FM_PASS_MOMENTS | FM_PASS_L1)
 
-template <bool HOMOG, bool F64>
+template <int COORD, bool F64>
 int dispatch_generic(unsigned mode, const fm_point_store& s, double thr, const double* ghat,
                      const double* res_in, const int32_t* prev_active, const fm_pass_out& out,
                      const PartialBufs& part, cudaStream_t stream) {
 #define FM_CASE(M) \
-  if (mode == (M)) return launch_generic<HOMOG, F64, (M)>(s, thr, ghat, res_in, prev_active, out, part, stream);
+  if (mode == (M)) return launch_generic<COORD, F64, (M)>(s, thr, ghat, res_in, prev_active, out, part, stream);
   FM_GENERIC_MODES(FM_CASE)
 #undef FM_CASE
   return set_error(FM_ERR_INVALID, "unsupported point-pass mode 0x%x", mode);
@@ -1040,14 +1050,18 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
              (long long)s.n_items, (long long)s.chunk);
   FM_REQUIRE(s.n_slots % 128 == 0, "n_slots must be a multiple of 128");
   if (s.n_pairs == 0) return FM_OK;
-  FM_REQUIRE(s.x1 && s.x2 && s.active && s.pair_off && s.pair_len && s.pair_item_off && s.item_pair,
+  const bool d64 = s.x1d != nullptr;
+  FM_REQUIRE(d64 == (s.x2d != nullptr), "x1d and x2d must both be set or both NULL");
+  FM_REQUIRE((d64 || (s.x1 && s.x2)) && s.active && s.pair_off && s.pair_len && s.pair_item_off &&
+                 s.item_pair,
              "incomplete point store");
-  FM_REQUIRE(((uintptr_t)s.x1 % 16) == 0 && ((uintptr_t)s.x2 % 16) == 0,
+  FM_REQUIRE(d64 || (((uintptr_t)s.x1 % 16) == 0 && ((uintptr_t)s.x2 % 16) == 0),
              "coordinate columns must be 16-byte aligned");
   const bool homog = s.x1z != nullptr;
   FM_REQUIRE(homog == (s.x2z != nullptr), "x1z and x2z must both be set or both NULL");
   const bool f64 = (mode & FM_PASS_F64) != 0;
   const unsigned m = mode & ~FM_PASS_F64;
+  FM_REQUIRE(!d64 || f64 || !(m & FM_PASS_MOMENTS), "fp64-coordinate stores need FM_PASS_F64 moments");
   const bool need_r = m & (FM_PASS_PRUNE | FM_PASS_L1 | FM_PASS_IRLS | FM_PASS_RES_OUT);
   FM_REQUIRE(!need_r || ghat, "mode 0x%x needs ghat", mode);
   FM_REQUIRE(!(m & FM_PASS_RES_IN) || res_in, "FM_PASS_RES_IN needs res_in");
@@ -1075,6 +1089,7 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE((sc.used == 0 || scratch) && sc.ok(), "point-pass scratch too small (%zu < %zu)",
                scratch_bytes, sc.used);
   }
+  if (d64) return dispatch_generic<kXYZ64, true>(m, s2, threshold, ghat, res_in, prev_active, *out, part, st);
   if (!homog && s.slot_align >= kBlkSlots && s.slot_align % kBlkSlots == 0) {
     // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
     const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
@@ -1085,11 +1100,11 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     }
   }
   if (homog) {
-    return f64 ? dispatch_generic<true, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
-               : dispatch_generic<true, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+    return f64 ? dispatch_generic<kXYZ32, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
+               : dispatch_generic<kXYZ32, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
   }
-  return f64 ? dispatch_generic<false, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
-             : dispatch_generic<false, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+  return f64 ? dispatch_generic<kXY32, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
+             : dispatch_generic<kXY32, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
 }
 
 }  // extern "C"

@@ -2,14 +2,34 @@
 // and Adam, for B independent random initialisations in lock-step, plus the
 // multi-init merge (ref/translation.py:112-186).
 //
+// Bitwise the reference.  Every floating-point operation is the one numpy
+// performs, in numpy's order (explicit _rn intrinsics, so nvcc cannot
+// contract a product into an FMA):
+//   * per edge, with the reference's orientation delta = c_j - c_i:
+//     |delta| = sqrt((d0^2 + d1^2) + d2^2) (np.linalg.norm along axis 1),
+//     u = delta / max(|delta|, 1e-8), r = u - d, g_u = sign(r) / m,
+//     s = (u0 g0 + u1 g1) + u2 g2, g_delta = (g_u - u s) / |delta|
+//     (ref/translation.py:114-121);
+//   * per node, the np.add.at scatter order (ref/translation.py:123-124): a
+//     left fold starting at 0.0 over the edges where the node is j (ascending
+//     edge id, +g_delta), then over the edges where it is i (-g_delta).  The
+//     node incidence list is sorted that way (j-side block, then i-side block,
+//     each by edge), so the fold is the incidence order;
+//   * the loss, np.abs(r).sum() / m, is numpy's pairwise summation over the
+//     flattened (m, 3) array (tr_loss_* kernels; the leaf list comes from the
+//     host), evaluated once at the state the reference returns it for;
+//   * Adam in the numpy expression order with the host's pow() bias
+//     corrections (ref/optim.py:30-34).
+// So a run's trajectory depends on nothing but its start: identical to the
+// reference's for the same seed, in any batch.
+//
 // Node-centric and deterministic: a warp owns (node v, group of <= 4 runs) and
-// gathers the node's incident edges (fixed lane-strided order + fixed warp
-// butterfly), evaluating each edge once per endpoint instead of scattering with
-// atomics.  One read of an edge's direction serves all runs of the group; the
-// centres of all runs of a node are contiguous ([n][B][3]) so the gather of
-// the other endpoint is one 96-byte segment.  The new centres go to a
-// ping-pong buffer, so one launch is one full optimizer step (the fused
-// loss + grad + Adam of ref/translation.py:146-151).
+// gathers the node's incident edges, evaluating each edge once per endpoint
+// instead of scattering with atomics.  One read of an edge's direction serves
+// all runs of the group; the centres of all runs of a node are contiguous
+// ([n][B][3]) so the gather of the other endpoint is one 24R-byte segment.  The
+// new centres go to a ping-pong buffer, so one launch is one full optimizer
+// step (the fused loss + grad + Adam of ref/translation.py:146-151).
 #include <map>
 #include <mutex>
 #include <vector>
@@ -24,27 +44,35 @@ namespace fm {
 namespace {
 
 constexpr int kGraphSteps = 200;  // steps per captured CUDA graph (even: keeps ping-pong parity)
+constexpr int kPwBlock = 128;     // numpy PW_BLOCKSIZE (pairwise-summation leaf size)
 
 struct TrScratch {
-  double4* rec;   // [2m] incidence records {direction, (other node) | side << 31}
-  double* buf;    // [n][B][3] ping-pong partner of the caller's centres
-  double* m;      // [n][B][3]
-  double* v;      // [n][B][3]
-  double* lpart;  // [n][B] per-node loss partials (edges where the node is i)
-  double* bc;     // [2][kGraphSteps] bias corrections
-  double* res;    // [n][B] node residuals (merge)
+  double4* rec;    // [2m] incidence records {direction, (other node) | side << 31}
+  double* buf;     // [n][B][3] ping-pong partner of the caller's centres
+  double* m;       // [n][B][3]
+  double* v;       // [n][B][3]
+  double* lpart;   // [n][B] per-node loss partials (finiteness check)
+  double* bc;      // [2][kGraphSteps] bias corrections
+  double* res;     // [n][B] node residuals (merge)
+  int64_t* leaf;   // [n_leaves + 1] pairwise-summation leaf offsets over 3m
+  double* lsum;    // [B][n_leaves] leaf sums
 };
+
+int64_t max_leaves(int64_t m) { return 3 * m / 32 + 16; }
 
 size_t tr_need(int32_t n, int64_t m, int32_t B) {
   const size_t nb3 = (size_t)n * B * 3;
+  const size_t L = (size_t)max_leaves(m);
   return scratch_round((size_t)2 * m * sizeof(double4)) +
          3 * scratch_round(nb3 * sizeof(double)) + 2 * scratch_round((size_t)n * B * sizeof(double)) +
-         scratch_round(2 * kGraphSteps * sizeof(double)) + 256;
+         scratch_round(2 * kGraphSteps * sizeof(double)) + scratch_round((L + 1) * sizeof(int64_t)) +
+         scratch_round(L * B * sizeof(double)) + 256;
 }
 
 bool tr_carve(int32_t n, int64_t m, int32_t B, void* p, size_t bytes, TrScratch& s) {
   Scratch sc(p, bytes);
   const size_t nb3 = (size_t)n * B * 3;
+  const size_t L = (size_t)max_leaves(m);
   s.rec = sc.take<double4>((size_t)2 * m);
   s.buf = sc.take<double>(nb3);
   s.m = sc.take<double>(nb3);
@@ -52,33 +80,139 @@ bool tr_carve(int32_t n, int64_t m, int32_t B, void* p, size_t bytes, TrScratch&
   s.lpart = sc.take<double>((size_t)n * B);
   s.bc = sc.take<double>(2 * kGraphSteps);
   s.res = sc.take<double>((size_t)n * B);
+  s.leaf = sc.take<int64_t>(L + 1);
+  s.lsum = sc.take<double>(L * B);
   return p != nullptr && sc.ok();
 }
 
-template <typename T>
-__device__ __forceinline__ T warp_sum(T x) {
+// numpy's pairwise-summation tree over n elements (pairwise_sum in
+// numpy/_core/src/umath/loops_utils.h): leaves of <= 128 elements, a node of
+// n > 128 splits at n2 = n/2 rounded down to a multiple of 8.  Host side:
+// the leaf offsets, left to right.
+void pw_leaves(int64_t lo, int64_t n, std::vector<int64_t>& off) {
+  if (n <= kPwBlock) {
+    off.push_back(lo + n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_leaves(lo, n2, off);
+  pw_leaves(lo + n2, n - n2, off);
+}
+
+// numpy's leaf sum: < 8 elements a plain left fold from 0.0; otherwise eight
+// interleaved accumulators, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// then the remainder folded in.
+template <typename F>
+__device__ double pw_leaf_sum(int64_t lo, int64_t n, F x) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, x(lo + i));
+    return res;
+  }
+  double r[8];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-  return x;
+  for (int j = 0; j < 8; ++j) r[j] = x(lo + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], x(lo + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, x(lo + i));
+  return res;
 }
 
-// 1/sqrt(q) for normal q > 0: hardware approximation + two Newton steps
-// (~1 ulp; no slow-path call)
-__device__ __forceinline__ double rsqrt_nr(double q) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
-  const double h = 0.5 * q;
-  y = fma(y, fma(-h * y, y, 0.5), y);
-  y = fma(y, fma(-h * y, y, 0.5), y);
-  return y;
+// The tree above evaluated without recursion (no device stack growth):
+// post-order walk with an explicit stack; leaf(lo, n) gives a leaf's sum,
+// children are added left + right as numpy does.
+template <typename Leaf>
+__device__ double pw_tree(int64_t n, Leaf leaf) {
+  int64_t lo_s[64], n_s[64];
+  int stage[64];
+  double left[64];
+  int sp = 0;
+  lo_s[0] = 0, n_s[0] = n, stage[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    const int64_t lo = lo_s[sp], cn = n_s[sp];
+    if (cn <= kPwBlock) {
+      ret = leaf(lo, cn);
+      --sp;
+      continue;
+    }
+    int64_t n2 = cn / 2;
+    n2 -= n2 % 8;
+    if (stage[sp] == 0) {
+      stage[sp] = 1;
+      ++sp;
+      lo_s[sp] = lo, n_s[sp] = n2, stage[sp] = 0;
+    } else if (stage[sp] == 1) {
+      left[sp] = ret;
+      stage[sp] = 2;
+      ++sp;
+      lo_s[sp] = lo + n2, n_s[sp] = cn - n2, stage[sp] = 0;
+    } else {
+      ret = __dadd_rn(left[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
 }
 
-// np.sign for finite x on the integer pipe: +-1 with x's sign bit, 0 for +-0
-// (a NaN residual yields +-1 here; the NaN loss it comes with raises anyway)
-__device__ __forceinline__ double sign_or_zero(double x) {
-  const int hi = __double2hiint(x);
-  const int one = 0x3FF00000 | (hi & (int)0x80000000);
-  return __hiloint2double(x != 0.0 ? one : 0, 0);
+// Combine from precomputed leaf sums (leaves are visited left to right).
+__device__ double pw_combine(int64_t n, const double* leaf_sum) {
+  int64_t k = 0;
+  return pw_tree(n, [&](int64_t, int64_t) { return leaf_sum[k++]; });
+}
+
+// Whole pairwise sum by one thread (small n: the canonicalize norms).
+template <typename F>
+__device__ double pw_sum(int64_t n, F x) {
+  return pw_tree(n, [&](int64_t lo, int64_t cn) { return pw_leaf_sum(lo, cn, x); });
+}
+
+// np.linalg.norm of a 3-vector along axis 1: sqrt((x0^2 + x1^2) + x2^2)
+__device__ __forceinline__ double norm3(const double d[3]) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                              __dmul_rn(d[2], d[2])));
+}
+
+// np.maximum(x, 1e-8): NaN propagates
+__device__ __forceinline__ double clamp_len(double x) { return x < 1e-8 ? 1e-8 : x; }
+
+// np.sign: -1, 0, +1, NaN for NaN
+__device__ __forceinline__ double np_sign(double x) {
+  return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
+}
+
+// One edge in the reference's arithmetic: u = delta / len, r = u - d and
+// g_delta (ref/translation.py:114-121); delta = c_j - c_i.
+struct EdgeTerm {
+  double r[3];
+  double gd[3];
+};
+
+__device__ __forceinline__ EdgeTerm edge_term(const double ci[3], const double cj[3],
+                                              const double dir[3], double inv_m) {
+  double delta[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) delta[k] = __dsub_rn(cj[k], ci[k]);
+  const double len = clamp_len(norm3(delta));
+  double u[3], gu[3];
+  EdgeTerm t;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    u[k] = __ddiv_rn(delta[k], len);
+    t.r[k] = __dsub_rn(u[k], dir[k]);
+    gu[k] = __dmul_rn(np_sign(t.r[k]), inv_m);  // sign(r) / m: +-(1/m) rounded once
+  }
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(u[0], gu[0]), __dmul_rn(u[1], gu[1])),
+                             __dmul_rn(u[2], gu[2]));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t.gd[k] = __ddiv_rn(__dsub_rn(gu[k], __dmul_rn(u[k], s)), len);
+  return t;
 }
 
 enum TrMode { kTrAdam = 0, kTrGrad = 1 };
@@ -98,19 +232,14 @@ __global__ void tr_incidence_kernel(const fm_dir_graph g, double4* __restrict__ 
 }
 
 // One warp per (node, group of R runs); lane = R * slot + run: the warp
-// walks the node's incidences 32/R at a time, every lane evaluates one
-// (incidence, run) term, so the R lanes of an incidence read the record once
-// (broadcast) and the R runs' centres of the other endpoint as one contiguous
-// 24R-byte segment.  Two incidences per lane are in flight (the step is a
-// chain of dependent L2 gathers).  Fixed-order butterflies over the slots.
+// walks the node's incidences 32/R slots x kIF at a time, every lane
+// evaluating one (incidence, run) edge term, so the R lanes of an incidence
+// read the record once (broadcast) and the R runs' centres of the other
+// endpoint as one contiguous 24R-byte segment.  The node's gradient is then
+// the left fold of the terms in incidence order, done by every lane of the
+// run from shuffled terms (the fold is the reference's np.add.at order, see
+// the file comment).
 // kTrAdam: Adam step cur -> nxt.  kTrGrad: write the gradient (API).
-//
-// Per term, with e = c_o - c_v, s = +1 if v is the edge's i else -1 and the
-// reference's u = s e / |e|, r = u - d, g_u = sign(r) / m
-// (ref/translation.py:112-125): writing w = e / |e| and d' = s d,
-// r = s (w - d'), so |r| = |w - d'|, sign(r) = s sign(w - d') and the node's
-// gradient term -s g_delta = -(sign(w - d') - w (w . sign(w - d'))) / (m |e|)
-// carries no sign of its own -- one formula for both endpoints, 1/m once.
 template <int MODE, int R>
 __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
                                const double* __restrict__ cur,
@@ -119,6 +248,7 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
                                double lr, double b1, double b2, double eps,
                                const double* __restrict__ bc, int step, int32_t* flag) {
   constexpr int kSlots = 32 / R;
+  constexpr int kIF = 2;  // incidences in flight per lane
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int groups = (B + R - 1) / R;
@@ -129,40 +259,20 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
   const int b = (int)(w % groups) * R + rb;  // this lane's run
   const bool run_ok = b < B;
   const int bl = run_ok ? b : B - 1;          // idle lanes mirror a valid run
-  const double inv_m = 1.0 / (double)g.n_edges;
+  const double inv_m = __ddiv_rn(1.0, (double)g.n_edges);
 
   double cv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) cv[k] = cur[((int64_t)v * B + bl) * 3 + k];
   double acc[3] = {0.0, 0.0, 0.0}, lacc = 0.0;
-  auto term = [&](const double4 r, const double co[3]) {
-    const bool vj = (__double_as_longlong(r.w) >> 31) & 1;  // v is the edge's j
-    const double dp[3] = {vj ? -r.x : r.x, vj ? -r.y : r.y, vj ? -r.z : r.z};
-    double e[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) e[k] = co[k] - cv[k];
-    const double q = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
-    // 1 / max(|e|, 1e-8) as one fp64 reciprocal square root (the reference
-    // divides each component by the clamped norm, ref/translation.py:115-121;
-    // same value to within an ulp)
-    const double inv = q > 1e-16 ? rsqrt_nr(q) : 1e8;
-    double wv[3], sg[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      wv[k] = e[k] * inv;
-      sg[k] = sign_or_zero(wv[k] - dp[k]);
-    }
-    const double wg = wv[0] * sg[0] + wv[1] * sg[1] + wv[2] * sg[2];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] -= (sg[k] - wv[k] * wg) * inv;
-    if (!vj) lacc += fabs(wv[0] - dp[0]) + fabs(wv[1] - dp[1]) + fabs(wv[2] - dp[2]);
-  };
   const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
-  constexpr int kIF = 2;  // incidences in flight per lane (4: more registers, half the warps)
-  for (int e = e0 + slot; e < e1; e += kIF * kSlots) {
+  for (int base = e0; base < e1; base += kIF * kSlots) {
     double4 r[kIF];
 #pragma unroll
-    for (int f = 0; f < kIF; ++f) r[f] = rec[e + f * kSlots < e1 ? e + f * kSlots : e];
+    for (int f = 0; f < kIF; ++f) {
+      const int e = base + f * kSlots + slot;
+      r[f] = rec[e < e1 ? e : e0];
+    }
     double c[kIF][3];
 #pragma unroll
     for (int f = 0; f < kIF; ++f) {
@@ -170,19 +280,34 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
 #pragma unroll
       for (int k = 0; k < 3; ++k) c[f][k] = __ldg(p + k);
     }
+    double term[kIF][3];
 #pragma unroll
-    for (int f = 0; f < kIF; ++f)
-      if (e + f * kSlots < e1) term(r[f], c[f]);
+    for (int f = 0; f < kIF; ++f) {
+      const bool vj = (__double_as_longlong(r[f].w) >> 31) & 1;  // v is the edge's j
+      const double dir[3] = {r[f].x, r[f].y, r[f].z};
+      const EdgeTerm t = vj ? edge_term(c[f], cv, dir, inv_m) : edge_term(cv, c[f], dir, inv_m);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) term[f][k] = vj ? t.gd[k] : -t.gd[k];  // np.add.at(j, +) / (i, -)
+      if (!vj && base + f * kSlots + slot < e1)
+        lacc += fabs(t.r[0]) + fabs(t.r[1]) + fabs(t.r[2]);
+    }
+    // left fold in incidence order: incidence base + f * kSlots + s
+#pragma unroll
+    for (int f = 0; f < kIF; ++f) {
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const bool live = base + f * kSlots + s < e1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double x = __shfl_sync(0xffffffffu, term[f][k], s * R + rb);
+          if (live) acc[k] = __dadd_rn(acc[k], x);
+        }
+      }
+    }
   }
 #pragma unroll
-  for (int off = R; off < 32; off <<= 1) {
-    lacc += __shfl_xor_sync(0xffffffffu, lacc, off);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-  }
+  for (int off = R; off < 32; off <<= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, off);
   if (slot != 0 || !run_ok) return;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) acc[k] *= inv_m;
   const int64_t base = ((int64_t)v * B + b) * 3;
   lpart[(int64_t)v * B + b] = lacc;
   if (MODE == kTrGrad) {
@@ -207,67 +332,83 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
     am[base + k] = mk;
     av[base + k] = vk;
     nxt[base + k] = __dsub_rn(cv[k], __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
-                                               __dadd_rn(sqrt(__ddiv_rn(vk, c2)), eps)));
+                                               __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, c2)), eps)));
   }
 }
 
-// loss[b] = sum_v lpart[v][b] / m  (fixed-order block reduction, block per run)
-__global__ void tr_loss_kernel(const double* __restrict__ lpart, int n, int B, int64_t m,
-                               double* __restrict__ loss) {
-  __shared__ double red[256];
+// |r| of flattened element q of the (m, 3) residual array of run b
+__device__ __forceinline__ double abs_residual(const fm_dir_graph& g, const double* __restrict__ c,
+                                               int B, int b, int64_t q) {
+  const int64_t e = q / 3;
+  const int k = (int)(q - 3 * e);
+  const int i = g.edge_i[e], j = g.edge_j[e];
+  double ci[3], cj[3], delta[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ci[a] = c[((int64_t)i * B + b) * 3 + a];
+    cj[a] = c[((int64_t)j * B + b) * 3 + a];
+    delta[a] = __dsub_rn(cj[a], ci[a]);
+  }
+  const double len = clamp_len(norm3(delta));
+  return fabs(__dsub_rn(__ddiv_rn(delta[k], len), g.dirs[3 * e + k]));
+}
+
+// loss = np.abs(r).sum() / m (ref/translation.py:119): pairwise leaves
+// (thread per (leaf, run)), then the combine (thread per run).
+__global__ void tr_loss_leaf_kernel(const fm_dir_graph g, const double* __restrict__ c, int B,
+                                    const int64_t* __restrict__ leaf, int64_t n_leaves,
+                                    double* __restrict__ lsum) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (l >= n_leaves) return;
+  const int64_t lo = l ? leaf[l - 1] : 0;
+  lsum[(int64_t)b * n_leaves + l] =
+      pw_leaf_sum(lo, leaf[l] - lo, [&](int64_t q) { return abs_residual(g, c, B, b, q); });
+}
+
+__global__ void tr_loss_combine_kernel(int64_t n_elem, const double* __restrict__ lsum,
+                                       int64_t n_leaves, int64_t m, double* __restrict__ loss) {
   const int b = blockIdx.x;
-  double acc = 0;
-  for (int v = threadIdx.x; v < n; v += 256) acc += lpart[(int64_t)v * B + b];
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) loss[b] = red[0] / (double)m;
+  loss[b] = __ddiv_rn(pw_combine(n_elem, lsum + (int64_t)b * n_leaves), (double)m);
 }
 
-// canonicalize (ref/translation.py:128-134), block per run, in place
+// canonicalize (ref/translation.py:128-134), block per run, in place:
+// mean over axis 0 is numpy's sequential row accumulation, the mean norm a
+// pairwise sum.
 __global__ void tr_canon_kernel(double* __restrict__ c, int n, int B) {
-  __shared__ double red[256][3];
+  __shared__ double mean[3];
+  __shared__ double scale;
   const int b = blockIdx.x;
-  double s[3] = {0, 0, 0};
-  for (int v = threadIdx.x; v < n; v += 256)
-    for (int k = 0; k < 3; ++k) s[k] += c[((int64_t)v * B + b) * 3 + k];
-  for (int k = 0; k < 3; ++k) red[threadIdx.x][k] = s[k];
-  __syncthreads();
-  for (int st = 128; st > 0; st >>= 1) {
-    if (threadIdx.x < st)
-      for (int k = 0; k < 3; ++k) red[threadIdx.x][k] += red[threadIdx.x + st][k];
-    __syncthreads();
+  if (threadIdx.x < 3) {
+    const int k = threadIdx.x;
+    double s = c[(int64_t)b * 3 + k];
+    for (int v = 1; v < n; ++v) s = __dadd_rn(s, c[((int64_t)v * B + b) * 3 + k]);
+    mean[k] = __ddiv_rn(s, (double)n);
   }
-  const double mean[3] = {red[0][0] / n, red[0][1] / n, red[0][2] / n};
   __syncthreads();
-  double ns = 0;
-  for (int v = threadIdx.x; v < n; v += 256) {
-    double q = 0;
+  if (threadIdx.x == 0) {
+    const double mu[3] = {mean[0], mean[1], mean[2]};
+    const double tot = pw_sum(n, [&](int64_t v) {
+      double o[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o[k] = __dsub_rn(c[(v * B + b) * 3 + k], mu[k]);
+      return norm3(o);
+    });
+    scale = __ddiv_rn(tot, (double)n);
+  }
+  __syncthreads();
+  const double sc = scale;
+  for (int v = threadIdx.x; v < n; v += blockDim.x)
     for (int k = 0; k < 3; ++k) {
-      const double x = c[((int64_t)v * B + b) * 3 + k] - mean[k];
-      q += x * x;
-    }
-    ns += sqrt(q);
-  }
-  red[threadIdx.x][0] = ns;
-  __syncthreads();
-  for (int st = 128; st > 0; st >>= 1) {
-    if (threadIdx.x < st) red[threadIdx.x][0] += red[threadIdx.x + st][0];
-    __syncthreads();
-  }
-  const double scale = red[0][0] / n;
-  for (int v = threadIdx.x; v < n; v += 256)
-    for (int k = 0; k < 3; ++k) {
-      double x = c[((int64_t)v * B + b) * 3 + k] - mean[k];
-      if (scale > 1e-8) x = x / scale;
+      double x = __dsub_rn(c[((int64_t)v * B + b) * 3 + k], mean[k]);
+      if (sc > 1e-8) x = __ddiv_rn(x, sc);
       c[((int64_t)v * B + b) * 3 + k] = x;
     }
 }
 
-// per_node_residuals (ref/translation.py:155-166), warp per (node, run)
+// per_node_residuals (ref/translation.py:155-166), warp per (node, run):
+// the np.add.at order is the edges where the node is i (the second block of
+// its incidence list), then those where it is j (the first block).
 __global__ void tr_node_res_kernel(const fm_dir_graph g, const double* __restrict__ c, int B,
                                    double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -275,17 +416,37 @@ __global__ void tr_node_res_kernel(const fm_dir_graph g, const double* __restric
   if (w >= (int64_t)g.n_nodes * B) return;
   const int v = (int)(w / B), b = (int)(w % B);
   const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
-  double acc = 0;
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const int64_t edge = g.node_inc[e] >> 1;
-    const int i = g.edge_i[edge], j = g.edge_j[edge];
-    double delta[3];
-    for (int k = 0; k < 3; ++k) delta[k] = c[((int64_t)j * B + b) * 3 + k] - c[((int64_t)i * B + b) * 3 + k];
-    const double len = fmax(sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]), 1e-8);
-    for (int k = 0; k < 3; ++k) acc += fabs(delta[k] / len - g.dirs[3 * edge + k]);
+  // first i-side incidence (side bit 0)
+  int mid = e1;
+  for (int e = e0; e < e1; e += 32) {
+    const bool is_i = e + lane < e1 && !(g.node_inc[e + lane] & 1);
+    const unsigned m = __ballot_sync(0xffffffffu, is_i);
+    if (m) {
+      mid = e + __ffs(m) - 1;
+      break;
+    }
   }
-  acc = warp_sum(acc);
-  if (lane == 0) out[(int64_t)v * B + b] = acc / fmax((double)(e1 - e0), 1.0);
+  double acc = 0.0;
+  for (int part = 0; part < 2; ++part) {
+    const int lo = part ? e0 : mid, hi = part ? mid : e1;
+    for (int e = lo; e < hi; e += 32) {
+      double r = 0.0;
+      if (e + lane < hi) {
+        const int64_t edge = g.node_inc[e + lane] >> 1;
+        const int i = g.edge_i[edge], j = g.edge_j[edge];
+        double delta[3];
+        for (int k = 0; k < 3; ++k)
+          delta[k] = __dsub_rn(c[((int64_t)j * B + b) * 3 + k], c[((int64_t)i * B + b) * 3 + k]);
+        const double len = clamp_len(norm3(delta));
+        double a[3];
+        for (int k = 0; k < 3; ++k) a[k] = fabs(__dsub_rn(__ddiv_rn(delta[k], len), g.dirs[3 * edge + k]));
+        r = __dadd_rn(__dadd_rn(a[0], a[1]), a[2]);
+      }
+      const int cnt = min(32, hi - e);
+      for (int s = 0; s < cnt; ++s) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, r, s));
+    }
+  }
+  if (lane == 0) out[(int64_t)v * B + b] = __ddiv_rn(acc, fmax((double)(e1 - e0), 1.0));
 }
 
 // per-node argmin over runs (first minimum, as np.argmin) + gather
@@ -317,9 +478,8 @@ int check_dir_graph(const fm_dir_graph* g, int32_t B) {
 unsigned warp_blocks(int64_t warps) { return (unsigned)ceil_div(warps * 32, 256); }
 
 // runs per warp: 4 for every batch (idle lanes when B % 4 != 0), 1 for a
-// single run.  A run's summation order depends only on R, so a run's
-// trajectory is the same in any batch of >= 2 runs -- the multi-init runs
-// sharded over ranks reproduce the single-GPU batch bit for bit.
+// single run.  The arithmetic of a run does not depend on R (the fold is in
+// incidence order), so the grouping is a pure throughput choice.
 int run_group(int B) {
   if (const char* env = getenv("FM_TR_R")) return B >= 2 ? atoi(env) : 1;  // tuning override
   return B >= 2 ? 4 : 1;
@@ -354,6 +514,25 @@ int enqueue_tr_steps(const fm_dir_graph& g, double* c0, double* c1, const TrScra
                                                          b1, b2, eps, s.bc, k, flag);
     FM_LAUNCHED(tr_step_kernel);
   }
+  return FM_OK;
+}
+
+// loss_out[b] = np.abs(r).sum() / m at centres c (ref/translation.py:119),
+// numpy's pairwise summation over the flattened (m, 3) residuals
+int enqueue_exact_loss(const fm_dir_graph& g, const double* c, int B, const TrScratch& s,
+                       double* loss_out, cudaStream_t st) {
+  const int64_t n_elem = 3 * g.n_edges;
+  std::vector<int64_t> off;
+  pw_leaves(0, n_elem, off);
+  const int64_t L = (int64_t)off.size();
+  FM_REQUIRE(L <= max_leaves(g.n_edges), "pairwise leaf bound");
+  FM_CUDA(cudaMemcpyAsync(s.leaf, off.data(), L * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // the host vector must outlive the copy: pageable memcpy is staged synchronously
+  tr_loss_leaf_kernel<<<dim3((unsigned)ceil_div(L, 128), (unsigned)B), 128, 0, st>>>(g, c, B, s.leaf, L,
+                                                                                    s.lsum);
+  FM_LAUNCHED(tr_loss_leaf_kernel);
+  tr_loss_combine_kernel<<<B, 1, 0, st>>>(n_elem, s.lsum, L, g.n_edges, loss_out);
+  FM_LAUNCHED(tr_loss_combine_kernel);
   return FM_OK;
 }
 
@@ -394,9 +573,7 @@ int fm_tr_loss_grad(const fm_dir_graph* g, const double* centers, int32_t B, dou
     tr_step_kernel<kTrGrad, 4><<<blocks, 256, 0, st>>>(*g, s.rec, centers, grad_out, nullptr, nullptr,
                                                        s.lpart, B, 0, 0, 0, 0, nullptr, 0, nullptr);
   FM_LAUNCHED(tr_step_kernel);
-  tr_loss_kernel<<<B, 256, 0, st>>>(s.lpart, g->n_nodes, B, g->n_edges, loss_out);
-  FM_LAUNCHED(tr_loss_kernel);
-  return FM_OK;
+  return enqueue_exact_loss(*g, centers, B, s, loss_out, st);
 }
 
 int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps, double lr,
@@ -473,13 +650,18 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
     } else {
       if (int rc = enqueue_tr_steps(*g, centers, s.buf, s, B, chunk, lr, beta1, beta2, eps, flag, st))
         return rc;
-      if (chunk & 1) FM_CUDA(cudaMemcpyAsync(centers, s.buf, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (chunk & 1) {
+        // odd tail: the last step read `centers`; its loss before the copy-back
+        if (int rc = enqueue_exact_loss(*g, centers, B, s, loss_out, st)) return rc;
+        FM_CUDA(cudaMemcpyAsync(centers, s.buf, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return FM_OK;
+      }
     }
     done += chunk;
   }
-  tr_loss_kernel<<<B, 256, 0, st>>>(s.lpart, n, B, g->n_edges, loss_out);
-  FM_LAUNCHED(tr_loss_kernel);
-  return FM_OK;
+  // even step count per chunk: the last step read the ping-pong buffer; the
+  // loss the reference returns is the one evaluated there (before the update)
+  return enqueue_exact_loss(*g, s.buf, B, s, loss_out, st);
 }
 
 int fm_tr_canonicalize(double* centers, int32_t n_nodes, int32_t B, void* scratch,

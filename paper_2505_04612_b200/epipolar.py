@@ -100,7 +100,7 @@ def precompute_weights(x1, x2, residuals=None):
     if len(x1) == 0:
         return np.zeros((9, 9))
     device = N.require_cuda()
-    store = PointPairStore(x1, x2, [len(x1)], [0], [0], device=device)
+    store = PointPairStore(x1, x2, [len(x1)], [0], [0], device=device, fp64=True)
     P = 1
     mom = torch.zeros((36, P), dtype=torch.float64, device=device)
     mode = N.FM_PASS_MOMENTS | N.FM_PASS_ALL_POINTS | N.FM_PASS_F64
@@ -194,7 +194,7 @@ class _Problem:
         idx_i, idx_j, cam_i, cam_j = _pair_indices(state, pairs)
         n_cams = len(state.log_focal)
         if need_points:
-            self.store = PointPairStore.from_pairs(pairs, device=self.device)
+            self.store = PointPairStore.from_pairs(pairs, device=self.device, fp64=True)
             order = self.store.order
         else:
             self.store = None

@@ -172,3 +172,30 @@ def initial_params(scene, ids, refine_focal=True):
 
 __all__ = ["SceneSpec", "CONFIGS", "generate", "device_store", "device_graph", "initial_params",
            "slot_layout", "pair_list"]
+
+
+def translation_graph_c3(n=2000, m=200_000, seed=0):
+    """BASELINE configs[2] direction graph (SURVEY 8d "C3"): n GT centres
+    from default_rng(seed).normal, a ring backbone plus uniform random pairs
+    up to m edges (i < j, sorted), directions = unit GT differences + 1 degree
+    noise, 5% replaced by random unit vectors.  Host numpy (deterministic on
+    every machine).  Returns (edges_i, edges_j, directions, gt_centers)."""
+    rng = np.random.default_rng(seed)
+    c = rng.normal(size=(n, 3))
+    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], axis=1)
+    extra = set()
+    while len(extra) < m - n:
+        a = rng.integers(0, n, size=(m, 2))
+        for i, j in a:
+            if i != j:
+                extra.add((min(i, j), max(i, j)))
+            if len(extra) >= m - n:
+                break
+    e = np.concatenate([np.sort(ring, axis=1), np.array(sorted(extra))])
+    d = c[e[:, 1]] - c[e[:, 0]]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d += rng.normal(scale=np.radians(1.0), size=d.shape)
+    bad = rng.random(m) < 0.05
+    d[bad] = rng.normal(size=(bad.sum(), 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return e[:, 0].astype(np.int64), e[:, 1].astype(np.int64), d, c

@@ -32,6 +32,10 @@ def _i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
 
 
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
 def _dev(a, device):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device, non_blocking=False)
 
@@ -74,7 +78,7 @@ class PointPairStore:
     """
 
     def __init__(self, x1, x2, lengths, pair_i, pair_j, active=None, device=None,
-                 chunk=CHUNK, order=None, sanitize=False):
+                 chunk=CHUNK, order=None, sanitize=False, fp64=False):
         """x1, x2: (Z, 2) or (Z, 3) float arrays of all points, pairs in caller
         order; lengths: points per pair (caller order).
 
@@ -82,7 +86,13 @@ class PointPairStore:
         their active bit.  The IRLS moment passes need finite coordinates on
         every slot; for irls_refine this is exactly the reference's behaviour
         (a non-finite residual fails ``res <= th`` in the first prune,
-        ref/epipolar.py:283).  API stores (current_residuals) keep NaNs."""
+        ref/epipolar.py:283).  API stores (current_residuals) keep NaNs.
+
+        fp64=True keeps the caller's fp64 (x, y, z) coordinates ([n_slots][3],
+        48 B per point pair) instead of the fp32 hot-store columns: the API
+        functions (precompute_weights, current_residuals, epipolar_loss) then
+        compute on exactly the reference's inputs.  irls_refine uses the fp32
+        hot store (north star: fp32 storage, 1e-4 tolerance)."""
         device = device or N.require_cuda()
         lengths = np.asarray(lengths, dtype=np.int64)
         P = len(lengths)
@@ -122,8 +132,34 @@ class PointPairStore:
                     x2[bad, 2] = 1.0
                 act = np.ones(len(x1), dtype=bool) if active is None else np.asarray(active, dtype=bool)
                 active = act & ~bad
-        homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
+        self.fp64 = bool(fp64)
+        self.x1d = self.x2d = None
+        if fp64:
+            d1 = np.zeros((n_slots, 3), dtype=np.float64)
+            d2 = np.zeros((n_slots, 3), dtype=np.float64)
+            d1[:, 2] = d2[:, 2] = 1.0
+            k = min(x1.shape[1], 3) if x1.ndim == 2 else 3
+            d1[self.point_slot, :k] = x1[:, :k]
+            d2[self.point_slot, :k] = x2[:, :k]
+            self.x1d = _dev(d1, device)
+            self.x2d = _dev(d2, device)
+            homog = False
+            self.x1 = self.x2 = self.x1z = self.x2z = None
+        else:
+            homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
         self.homogeneous = bool(homog)
+        if not fp64:
+            self._fp32_columns(x1, x2, n_slots, homog, device)
+        bits = np.zeros(n_slots, dtype=bool)
+        bits[self.point_slot] = True if active is None else np.asarray(active, dtype=bool)
+        self.active = _dev(np.packbits(bits, bitorder="little").view(np.int32), device)
+        self.pair_off_d = _dev(pair_off, device)
+        self.pair_len_d = _dev(_i32(s_len), device)
+        self.pair_item_off_d = _dev(pair_item_off, device)
+        self.item_pair_d = _dev(item_pair, device)
+        self._struct = None
+
+    def _fp32_columns(self, x1, x2, n_slots, homog, device):
         c1 = np.zeros((n_slots, 2), dtype=np.float32)
         c2 = np.zeros((n_slots, 2), dtype=np.float32)
         c1[self.point_slot] = x1[:, :2]
@@ -139,14 +175,6 @@ class PointPairStore:
             self.x2z = _dev(z2, device)
         else:
             self.x1z = self.x2z = None
-        bits = np.zeros(n_slots, dtype=bool)
-        bits[self.point_slot] = True if active is None else np.asarray(active, dtype=bool)
-        self.active = _dev(np.packbits(bits, bitorder="little").view(np.int32), device)
-        self.pair_off_d = _dev(pair_off, device)
-        self.pair_len_d = _dev(_i32(s_len), device)
-        self.pair_item_off_d = _dev(pair_item_off, device)
-        self.item_pair_d = _dev(item_pair, device)
-        self._struct = None
 
     # ---------------------------------------------------------------- ctypes
     def struct(self):
@@ -157,10 +185,9 @@ class PointPairStore:
                 pair_off=self.pair_off_d.data_ptr(), pair_len=self.pair_len_d.data_ptr(),
                 pair_item_off=self.pair_item_off_d.data_ptr(),
                 item_pair=self.item_pair_d.data_ptr(),
-                x1=self.x1.data_ptr(), x2=self.x2.data_ptr(),
-                x1z=self.x1z.data_ptr() if self.x1z is not None else None,
-                x2z=self.x2z.data_ptr() if self.x2z is not None else None,
-                active=self.active.data_ptr(), item_desc=None, slot_align=SLOT_ALIGN)
+                x1=_ptr(self.x1), x2=_ptr(self.x2), x1z=_ptr(self.x1z), x2z=_ptr(self.x2z),
+                active=self.active.data_ptr(), item_desc=None, slot_align=SLOT_ALIGN,
+                x1d=_ptr(getattr(self, "x1d", None)), x2d=_ptr(getattr(self, "x2d", None)))
             self.item_desc_d = torch.empty((max(self.n_items, 1), 4), dtype=torch.int32,
                                            device=self.device)
             self._struct.item_desc = self.item_desc_d.data_ptr()
@@ -258,7 +285,8 @@ class PointPairStore:
         return torch.from_numpy(self.point_slot).to(self.device)
 
     @classmethod
-    def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False, sanitize=False):
+    def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False, sanitize=False,
+                   fp64=False):
         """Build from EpipolarPair-like objects (reference or ours)."""
         lengths = np.array([len(p.x1) for p in pairs], dtype=np.int64)
         if len(pairs):
@@ -272,7 +300,8 @@ class PointPairStore:
             act = None
         i = np.array([p.i for p in pairs], dtype=np.int64)
         j = np.array([p.j for p in pairs], dtype=np.int64)
-        return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk, sanitize=sanitize)
+        return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk, sanitize=sanitize,
+                   fp64=fp64)
 
 
 def csr(keys, n_keys, payload):
@@ -365,8 +394,16 @@ class DirGraphDevice:
         self.m = m
         if m and (min(ei.min(), ej.min()) < 0 or max(ei.max(), ej.max()) >= self.n):
             raise IndexError("edge endpoint out of range")
-        inc = np.concatenate([np.arange(m) * 2, np.arange(m) * 2 + 1])
-        self.node_off, self.node_inc = csr(np.concatenate([ei, ej]), self.n, inc)
+        # per node: the edges where it is j (by edge id), then those where it
+        # is i -- the order of the reference's np.add.at scatter
+        # (ref/translation.py:123-124), which the kernels fold in
+        edge = np.concatenate([np.arange(m), np.arange(m)])
+        side = np.concatenate([np.zeros(m, np.int64), np.ones(m, np.int64)])
+        node = np.concatenate([ei, ej])
+        order = np.lexsort((edge, 1 - side, node))
+        self.node_off = np.zeros(self.n + 1, dtype=np.int32)
+        np.cumsum(np.bincount(node, minlength=self.n), out=self.node_off[1:])
+        self.node_inc = _i32((edge * 2 + side)[order])
         self.ei = _dev(_i32(ei), device)
         self.ej = _dev(_i32(ej), device)
         self.dirs = _dev(np.asarray(graph.directions, dtype=np.float64).reshape(m, 3), device)

@@ -155,16 +155,27 @@ class DirectionGraph:
 _GRAPH_CACHE = {}
 
 
+def _graph_digest(graph):
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.int64(graph.n).tobytes())
+    for a, dt in ((graph.edges_i, np.int64), (graph.edges_j, np.int64), (graph.directions, np.float64)):
+        h.update(np.ascontiguousarray(np.asarray(a, dtype=dt)).tobytes())
+    return h.digest()
+
+
 def device_graph(graph):
-    """Upload (and memoise per graph object) the direction graph."""
+    """Upload the direction graph, memoised per graph object AND content (an
+    in-place edit of the arrays re-uploads)."""
     key = id(graph)
+    digest = _graph_digest(graph)
     hit = _GRAPH_CACHE.get(key)
-    if hit is not None and hit[0] is graph:
-        return hit[1]
+    if hit is not None and hit[0] is graph and hit[1] == digest:
+        return hit[2]
     dg = DirGraphDevice(graph)
     if len(_GRAPH_CACHE) > 8:
         _GRAPH_CACHE.clear()
-    _GRAPH_CACHE[key] = (graph, dg)
+    _GRAPH_CACHE[key] = (graph, digest, dg)
     return dg
 
 
