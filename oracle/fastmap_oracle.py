@@ -15,7 +15,9 @@ Formulation differences from the reference (same mathematics):
 * point pairs live in one flat array with a per-point pair index instead of
   per-pair Python objects; per-pair sums are segment sums (np.add.reduceat);
 * the Jacobian of the 6D map is applied as a vector-Jacobian product;
-* scatters use np.bincount instead of np.add.at.
+* epipolar scatters use np.bincount instead of np.add.at; the translation
+  functions keep the reference's np.add.at calls in the reference's order, so
+  they are bitwise the reference (the CUDA translation path is held to that).
 """
 
 import numpy as np
@@ -345,8 +347,9 @@ def translation_loss_grad(centers, ei, ej, dirs):
     m = len(dirs)
     gu = np.sign(r) / m
     gd = (gu - u * np.sum(u * gu, axis=1, keepdims=True)) / length
-    n = len(centers)
-    grad = segment_sum(gd, ej, n) - segment_sum(gd, ei, n)
+    grad = np.zeros_like(centers)
+    np.add.at(grad, ej, gd)       # ref/translation.py:123-124 order
+    np.add.at(grad, ei, -gd)
     return float(np.abs(r).sum() / m), grad
 
 
@@ -379,8 +382,12 @@ def per_node_residuals(c, ei, ej, dirs):
     length = np.maximum(np.linalg.norm(delta, axis=1, keepdims=True), NORM_EPS)
     r = np.abs(delta / length - dirs).sum(axis=1)
     n = len(c)
-    tot = np.bincount(ei, weights=r, minlength=n) + np.bincount(ej, weights=r, minlength=n)
-    cnt = np.bincount(ei, minlength=n) + np.bincount(ej, minlength=n)
+    tot = np.zeros(n)
+    cnt = np.zeros(n)
+    np.add.at(tot, ei, r)         # ref/translation.py:161-164 order
+    np.add.at(tot, ej, r)
+    np.add.at(cnt, ei, 1.0)
+    np.add.at(cnt, ej, 1.0)
     return tot / np.maximum(cnt, 1.0)
 
 

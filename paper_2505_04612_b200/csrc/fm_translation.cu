@@ -52,7 +52,8 @@ struct TrScratch {
   double* m;       // [n][B][3]
   double* v;       // [n][B][3]
   double* lpart;   // [n][B] per-node loss partials (finiteness check)
-  double* bc;      // [2][kGraphSteps] bias corrections
+  const double** ctrl;  // [2] bias-correction tables (1 - b1^t, 1 - b2^t) of the current chunk
+  double* cA;      // [n][B][3] ping buffer (the caller's centres are copied in and out)
   double* res;     // [n][B] node residuals (merge)
   int64_t* leaf;   // [n_leaves + 1] pairwise-summation leaf offsets over 3m
   double* lsum;    // [B][n_leaves] leaf sums
@@ -65,7 +66,8 @@ size_t tr_need(int32_t n, int64_t m, int32_t B) {
   const size_t L = (size_t)max_leaves(m);
   return scratch_round((size_t)2 * m * sizeof(double4)) +
          3 * scratch_round(nb3 * sizeof(double)) + 2 * scratch_round((size_t)n * B * sizeof(double)) +
-         scratch_round(2 * kGraphSteps * sizeof(double)) + scratch_round((L + 1) * sizeof(int64_t)) +
+         scratch_round(2 * sizeof(double*)) + scratch_round(nb3 * sizeof(double)) +
+         scratch_round((L + 1) * sizeof(int64_t)) +
          scratch_round(L * B * sizeof(double)) + 256;
 }
 
@@ -78,7 +80,8 @@ bool tr_carve(int32_t n, int64_t m, int32_t B, void* p, size_t bytes, TrScratch&
   s.m = sc.take<double>(nb3);
   s.v = sc.take<double>(nb3);
   s.lpart = sc.take<double>((size_t)n * B);
-  s.bc = sc.take<double>(2 * kGraphSteps);
+  s.ctrl = sc.take<const double*>(2);
+  s.cA = sc.take<double>(nb3);
   s.res = sc.take<double>((size_t)n * B);
   s.leaf = sc.take<int64_t>(L + 1);
   s.lsum = sc.take<double>(L * B);
@@ -187,6 +190,33 @@ __device__ __forceinline__ double np_sign(double x) {
   return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
 }
 
+// a / b correctly rounded (bitwise __ddiv_rn) from y = RN(1/b), for the six
+// divisions by the same edge length: q0 = RN(a y) is within 1.5 ulp, one
+// FMA-residual correction brings it within 1 ulp, and the second is exact
+// by Markstein's theorem (y correctly rounded, q within 1 ulp; the residual
+// a - b q is exact in an FMA).  The theorem assumes no underflow and finite
+// operands: edge_term checks its six quotients once and redoes them with
+// __ddiv_rn otherwise (never on real data; kept off the fast path).
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double q1 = __fma_rn(__fma_rn(-q0, b, a), y, q0);
+  return __fma_rn(__fma_rn(-q1, b, a), y, q1);
+}
+
+__device__ __forceinline__ bool rcp_div_safe(double q) { return fabs(q) >= 0x1p-960 || q == 0.0; }
+
+// sign(r) / m for the reference's np.sign(r) / m: +-(1/m) (rounded once, as
+// the reference's division of +-1 by m), 0 for +-0, NaN for NaN
+// (kNaN = false: NaN residuals need not propagate -- the descent's loss
+// check raises for them before the gradient is used)
+template <bool kNaN>
+__device__ __forceinline__ double sign_over_m(double r, double inv_m) {
+  const long long bits = __double_as_longlong(r);
+  const double sg = __longlong_as_double(__double_as_longlong(inv_m) | (bits & (1ll << 63)));
+  if (!kNaN) return r == 0.0 ? 0.0 : sg;
+  return r == 0.0 ? 0.0 : (r != r ? r : sg);
+}
+
 // One edge in the reference's arithmetic: u = delta / len, r = u - d and
 // g_delta (ref/translation.py:114-121); delta = c_j - c_i.
 struct EdgeTerm {
@@ -194,24 +224,43 @@ struct EdgeTerm {
   double gd[3];
 };
 
-__device__ __forceinline__ EdgeTerm edge_term(const double ci[3], const double cj[3],
-                                              const double dir[3], double inv_m) {
-  double delta[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) delta[k] = __dsub_rn(cj[k], ci[k]);
+template <bool kNaN>
+__device__ __forceinline__ EdgeTerm edge_term(const double delta[3], const double dir[3],
+                                              double inv_m) {
   const double len = clamp_len(norm3(delta));
-  double u[3], gu[3];
+  const double y = __drcp_rn(len);
+  double u[3], gu[3], num[3];
   EdgeTerm t;
 #pragma unroll
+  for (int k = 0; k < 3; ++k) u[k] = div_rcp(delta[k], len, y);
+  bool ok = rcp_div_safe(u[0]) && rcp_div_safe(u[1]) && rcp_div_safe(u[2]);
+#pragma unroll
   for (int k = 0; k < 3; ++k) {
-    u[k] = __ddiv_rn(delta[k], len);
     t.r[k] = __dsub_rn(u[k], dir[k]);
-    gu[k] = __dmul_rn(np_sign(t.r[k]), inv_m);  // sign(r) / m: +-(1/m) rounded once
+    gu[k] = sign_over_m<kNaN>(t.r[k], inv_m);
   }
   const double s = __dadd_rn(__dadd_rn(__dmul_rn(u[0], gu[0]), __dmul_rn(u[1], gu[1])),
                              __dmul_rn(u[2], gu[2]));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) t.gd[k] = __ddiv_rn(__dsub_rn(gu[k], __dmul_rn(u[k], s)), len);
+  for (int k = 0; k < 3; ++k) {
+    num[k] = __dsub_rn(gu[k], __dmul_rn(u[k], s));
+    t.gd[k] = div_rcp(num[k], len, y);
+    ok = ok && rcp_div_safe(t.gd[k]);
+  }
+  if (__builtin_expect(!ok, 0)) {
+    // exact division everywhere (u first: r and gu depend on it)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) u[k] = __ddiv_rn(delta[k], len);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      t.r[k] = __dsub_rn(u[k], dir[k]);
+      gu[k] = sign_over_m<kNaN>(t.r[k], inv_m);
+    }
+    const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(u[0], gu[0]), __dmul_rn(u[1], gu[1])),
+                                __dmul_rn(u[2], gu[2]));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t.gd[k] = __ddiv_rn(__dsub_rn(gu[k], __dmul_rn(u[k], s2)), len);
+  }
   return t;
 }
 
@@ -231,25 +280,36 @@ __global__ void tr_incidence_kernel(const fm_dir_graph g, double4* __restrict__ 
                         __longlong_as_double((long long)(uint32_t)o | ((long long)side << 31)));
 }
 
+__device__ __forceinline__ double flip(double x, long long sign_mask) {
+  return __longlong_as_double(__double_as_longlong(x) ^ sign_mask);
+}
+
 // One warp per (node, group of R runs); lane = R * slot + run: the warp
-// walks the node's incidences 32/R slots x kIF at a time, every lane
-// evaluating one (incidence, run) edge term, so the R lanes of an incidence
-// read the record once (broadcast) and the R runs' centres of the other
-// endpoint as one contiguous 24R-byte segment.  The node's gradient is then
-// the left fold of the terms in incidence order, done by every lane of the
-// run from shuffled terms (the fold is the reference's np.add.at order, see
-// the file comment).
+// walks the node's incidences kIF x 32/R at a time, every lane evaluating
+// one (incidence, run) edge term, so the R lanes of an incidence read the
+// record once (broadcast) and the R runs' centres of the other endpoint as one
+// contiguous 24R-byte segment.  The terms go to a per-warp shared-memory
+// tile; then lane 3 rb + k folds component k of run rb over the tile in
+// incidence order (the reference's np.add.at order, see the file comment):
+// 3R sequential chains per warp, no redundant shuffled folds.
 // kTrAdam: Adam step cur -> nxt.  kTrGrad: write the gradient (API).
+#ifndef FM_TR_MINB
+#define FM_TR_MINB 2  // resident 256-thread blocks per SM (3: register cap 80, spills, no faster)
+#endif
+
 template <int MODE, int R>
-__global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
+__global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
                                const double* __restrict__ cur,
                                double* __restrict__ nxt, double* __restrict__ am,
                                double* __restrict__ av, double* __restrict__ lpart, int B,
                                double lr, double b1, double b2, double eps,
-                               const double* __restrict__ bc, int step, int32_t* flag) {
+                               const double* const* __restrict__ bc, int step, int32_t* flag) {
   constexpr int kSlots = 32 / R;
-  constexpr int kIF = 2;  // incidences in flight per lane
+  constexpr int kIF = 2;               // incidences in flight per lane
+  constexpr int kTile = kIF * 32 * 3;  // doubles per warp: [kIF * kSlots][R][3]
+  __shared__ double tile_all[8][kTile];
   const int lane = threadIdx.x & 31;
+  double* tile = tile_all[threadIdx.x >> 5];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int groups = (B + R - 1) / R;
   if (w >= (int64_t)g.n_nodes * groups) return;
@@ -257,14 +317,17 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
   const int v = (int)(w / groups);
   const int rb = lane % R, slot = lane / R;
   const int b = (int)(w % groups) * R + rb;  // this lane's run
-  const bool run_ok = b < B;
-  const int bl = run_ok ? b : B - 1;          // idle lanes mirror a valid run
+  const int bl = b < B ? b : B - 1;           // idle lanes mirror a valid run
   const double inv_m = __ddiv_rn(1.0, (double)g.n_edges);
+  // folding role: lane 3 fr + fk folds component fk of run fr of the group
+  const int fr = lane / 3, fk = lane - 3 * (lane / 3);
+  const bool folder = lane < 3 * R;
+  const int fb = (int)(w % groups) * R + fr;
 
   double cv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) cv[k] = cur[((int64_t)v * B + bl) * 3 + k];
-  double acc[3] = {0.0, 0.0, 0.0}, lacc = 0.0;
+  double acc = 0.0, lacc = 0.0;
   const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
   for (int base = e0; base < e1; base += kIF * kSlots) {
     double4 r[kIF];
@@ -280,60 +343,58 @@ __global__ void __launch_bounds__(256) tr_step_kernel(const fm_dir_graph g, cons
 #pragma unroll
       for (int k = 0; k < 3; ++k) c[f][k] = __ldg(p + k);
     }
-    double term[kIF][3];
 #pragma unroll
     for (int f = 0; f < kIF; ++f) {
-      const bool vj = (__double_as_longlong(r[f].w) >> 31) & 1;  // v is the edge's j
+      // v is the edge's j -> delta = c_v - c_o = -(c_o - c_v) (exact), term +g_delta;
+      // v is the edge's i -> delta = c_o - c_v, term -g_delta (np.add.at(i, -))
+      const long long vj = (__double_as_longlong(r[f].w) >> 31) & 1;
+      const long long to_delta = vj << 63, to_term = (vj ^ 1) << 63;
+      double delta[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) delta[k] = flip(__dsub_rn(c[f][k], cv[k]), to_delta);
       const double dir[3] = {r[f].x, r[f].y, r[f].z};
-      const EdgeTerm t = vj ? edge_term(c[f], cv, dir, inv_m) : edge_term(cv, c[f], dir, inv_m);
+      const EdgeTerm t = edge_term<MODE == kTrGrad>(delta, dir, inv_m);
+      const bool live = base + f * kSlots + slot < e1;
+      // past the node's last incidence: -0.0, the exact identity of the fold
 #pragma unroll
-      for (int k = 0; k < 3; ++k) term[f][k] = vj ? t.gd[k] : -t.gd[k];  // np.add.at(j, +) / (i, -)
-      if (!vj && base + f * kSlots + slot < e1)
-        lacc += fabs(t.r[0]) + fabs(t.r[1]) + fabs(t.r[2]);
+      for (int k = 0; k < 3; ++k) tile[(f * 32 + lane) * 3 + k] = live ? flip(t.gd[k], to_term) : -0.0;
+      if (!vj && live) lacc += fabs(t.r[0]) + fabs(t.r[1]) + fabs(t.r[2]);
     }
-    // left fold in incidence order: incidence base + f * kSlots + s
+    __syncwarp();
+    if (folder) {
+      // incidence base + q (q = f kSlots + s) of run fr sits at
+      // [(f 32 + s R + fr) 3 + fk] = [q 3R + lane]
 #pragma unroll
-    for (int f = 0; f < kIF; ++f) {
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        const bool live = base + f * kSlots + s < e1;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const double x = __shfl_sync(0xffffffffu, term[f][k], s * R + rb);
-          if (live) acc[k] = __dadd_rn(acc[k], x);
-        }
-      }
+      for (int q = 0; q < kIF * kSlots; ++q) acc = __dadd_rn(acc, tile[q * 3 * R + lane]);
     }
+    __syncwarp();
   }
 #pragma unroll
   for (int off = R; off < 32; off <<= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, off);
-  if (slot != 0 || !run_ok) return;
-  const int64_t base = ((int64_t)v * B + b) * 3;
-  lpart[(int64_t)v * B + b] = lacc;
+  lacc = __shfl_sync(0xffffffffu, lacc, fr < R ? fr : 0);  // run fr's loss partial
+  if (!folder || fb >= B) return;
+  const int64_t base = ((int64_t)v * B + fb) * 3;
+  if (fk == 0) lpart[(int64_t)v * B + fb] = lacc;
   if (MODE == kTrGrad) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) nxt[base + k] = acc[k];
+    nxt[base + fk] = acc;
     return;
   }
   if (!isfinite(lacc)) {
     atomicMax(flag, FM_ERR_NONFINITE_TRANSLATION);
     return;
   }
-  if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
+  if (!isfinite(acc)) {
     atomicMax(flag, FM_ERR_NONFINITE_GRAD);
     return;
   }
-  const double c1 = bc[step], c2 = bc[kGraphSteps + step];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const double gk = acc[k];
-    const double mk = __dadd_rn(__dmul_rn(b1, am[base + k]), __dmul_rn(1.0 - b1, gk));
-    const double vk = __dadd_rn(__dmul_rn(b2, av[base + k]), __dmul_rn(1.0 - b2, __dmul_rn(gk, gk)));
-    am[base + k] = mk;
-    av[base + k] = vk;
-    nxt[base + k] = __dsub_rn(cv[k], __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
-                                               __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, c2)), eps)));
-  }
+  const double c1 = bc[0][step], c2 = bc[1][step];
+  const double ck = cur[base + fk];
+  const double mk = __dadd_rn(__dmul_rn(b1, am[base + fk]), __dmul_rn(1.0 - b1, acc));
+  const double vk = __dadd_rn(__dmul_rn(b2, av[base + fk]), __dmul_rn(1.0 - b2, __dmul_rn(acc, acc)));
+  am[base + fk] = mk;
+  av[base + fk] = vk;
+  nxt[base + fk] = __dsub_rn(ck, __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
+                                           __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, c2)), eps)));
 }
 
 // |r| of flattened element q of the (m, 3) residual array of run b
@@ -502,19 +563,24 @@ int enqueue_tr_steps(const fm_dir_graph& g, double* c0, double* c1, const TrScra
     double* nxt = (k & 1) ? c0 : c1;
     if (R == 1)
       tr_step_kernel<kTrAdam, 1><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
-                                                         b1, b2, eps, s.bc, k, flag);
+                                                         b1, b2, eps, s.ctrl, k, flag);
     else if (R == 2)
       tr_step_kernel<kTrAdam, 2><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
-                                                         b1, b2, eps, s.bc, k, flag);
+                                                         b1, b2, eps, s.ctrl, k, flag);
     else if (R == 8)
       tr_step_kernel<kTrAdam, 8><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
-                                                         b1, b2, eps, s.bc, k, flag);
+                                                         b1, b2, eps, s.ctrl, k, flag);
     else
       tr_step_kernel<kTrAdam, 4><<<blocks, 256, 0, st>>>(g, s.rec, cur, nxt, s.m, s.v, s.lpart, B, lr,
-                                                         b1, b2, eps, s.bc, k, flag);
+                                                         b1, b2, eps, s.ctrl, k, flag);
     FM_LAUNCHED(tr_step_kernel);
   }
   return FM_OK;
+}
+
+__global__ void tr_set_ctrl_kernel(const double** ctrl, const double* c1, const double* c2) {
+  ctrl[0] = c1;
+  ctrl[1] = c2;
 }
 
 // loss_out[b] = np.abs(r).sum() / m at centres c (ref/translation.py:119),
@@ -592,22 +658,31 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
   FM_CUDA(cudaMemsetAsync(s.m, 0, nb3 * sizeof(double), st));
   FM_CUDA(cudaMemsetAsync(s.v, 0, nb3 * sizeof(double), st));
   if (int rc = build_incidence(*g, s, st)) return rc;
-  std::vector<double> bc(2 * kGraphSteps, 1.0);
+  // bias corrections 1 - beta^t of every step with the host's pow (the
+  // reference's Python `beta ** t`), one stream-ordered table per call
+  std::vector<double> bc(2 * (size_t)steps);
+  for (int k = 0; k < steps; ++k) {
+    bc[k] = 1.0 - pow(beta1, (double)(k + 1));
+    bc[steps + k] = 1.0 - pow(beta2, (double)(k + 1));
+  }
+  double* table = nullptr;
+  FM_CUDA(cudaMallocAsync(&table, bc.size() * sizeof(double), st));
+  FM_CUDA(cudaMemcpyAsync(table, bc.data(), bc.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  // the descent ping-pongs between two scratch buffers, so the captured
+  // graphs depend only on the scratch / graph pointers and are reused
+  // across calls
+  FM_CUDA(cudaMemcpyAsync(s.cA, centers, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   int done = 0;
-  // steps in graph-sized chunks; every chunk starts from `centers` (even length)
   while (done < steps) {
     const int chunk = std::min(kGraphSteps, steps - done);
-    for (int k = 0; k < chunk; ++k) {
-      const double t = (double)(done + k + 1);
-      bc[k] = 1.0 - pow(beta1, t);
-      bc[kGraphSteps + k] = 1.0 - pow(beta2, t);
-    }
-    FM_CUDA(cudaMemcpyAsync(s.bc, bc.data(), bc.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    tr_set_ctrl_kernel<<<1, 1, 0, st>>>(s.ctrl, table + done, table + steps + done);
+    FM_LAUNCHED(tr_set_ctrl_kernel);
     if (chunk == kGraphSteps) {
       TrKey key;
       for (const void* p : {(const void*)g->edge_i, (const void*)g->edge_j, (const void*)g->dirs,
-                            (const void*)g->node_off, (const void*)g->node_inc, (const void*)centers,
-                            (const void*)s.buf, (const void*)s.m, (const void*)flag})
+                            (const void*)g->node_off, (const void*)g->node_inc, (const void*)s.rec,
+                            (const void*)s.cA, (const void*)s.buf, (const void*)s.m, (const void*)s.v,
+                            (const void*)s.lpart, (const void*)s.ctrl, (const void*)flag})
         key.k.push_back(reinterpret_cast<uintptr_t>(p));
       key.k.push_back((uintptr_t)n);
       key.k.push_back((uintptr_t)g->n_edges);
@@ -627,7 +702,7 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
         cudaStream_t cs;
         FM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         FM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_tr_steps(*g, centers, s.buf, s, B, chunk, lr, beta1, beta2, eps, flag, cs);
+        int rc = enqueue_tr_steps(*g, s.cA, s.buf, s, B, chunk, lr, beta1, beta2, eps, flag, cs);
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(cs, &graph);
         cudaStreamDestroy(cs);
@@ -648,20 +723,20 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
       }
       FM_CUDA(cudaGraphLaunch(exec, st));
     } else {
-      if (int rc = enqueue_tr_steps(*g, centers, s.buf, s, B, chunk, lr, beta1, beta2, eps, flag, st))
+      if (int rc = enqueue_tr_steps(*g, s.cA, s.buf, s, B, chunk, lr, beta1, beta2, eps, flag, st))
         return rc;
-      if (chunk & 1) {
-        // odd tail: the last step read `centers`; its loss before the copy-back
-        if (int rc = enqueue_exact_loss(*g, centers, B, s, loss_out, st)) return rc;
-        FM_CUDA(cudaMemcpyAsync(centers, s.buf, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        return FM_OK;
-      }
     }
     done += chunk;
   }
-  // even step count per chunk: the last step read the ping-pong buffer; the
-  // loss the reference returns is the one evaluated there (before the update)
-  return enqueue_exact_loss(*g, s.buf, B, s, loss_out, st);
+  // full chunks (even) end in cA; an odd tail ends in buf.  The reference
+  // returns the loss evaluated at the last step, i.e. before its update.
+  const bool odd = (steps % kGraphSteps) & 1;
+  const double* fin = odd ? s.buf : s.cA;
+  const double* pre = odd ? s.cA : s.buf;
+  if (int rc = enqueue_exact_loss(*g, pre, B, s, loss_out, st)) return rc;
+  FM_CUDA(cudaMemcpyAsync(centers, fin, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  FM_CUDA(cudaFreeAsync(table, st));
+  return FM_OK;
 }
 
 int fm_tr_canonicalize(double* centers, int32_t n_nodes, int32_t B, void* scratch,

@@ -417,5 +417,18 @@ class DirGraphDevice:
         return self._struct
 
     def scratch(self, runs):
-        nbytes = N.lib().fm_tr_scratch_bytes(self.n, self.m, runs)
-        return torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        """Scratch of a B-run call, kept per B: fm_tr_align's captured CUDA
+        graphs are keyed on the scratch pointers, so reusing it replays them
+        (calls on one graph object are stream-ordered, not concurrent)."""
+        cache = self.__dict__.setdefault("_scratch", {})
+        if runs not in cache:
+            nbytes = N.lib().fm_tr_scratch_bytes(self.n, self.m, runs)
+            cache[runs] = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        return cache[runs]
+
+    def flag(self):
+        """The device error word of this graph's descents (zeroed per call)."""
+        if "_flag" not in self.__dict__:
+            self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._flag.zero_()
+        return self._flag

@@ -232,7 +232,7 @@ def _align(dg, init, cfg, steps):
     if steps == 0:
         return c, np.full(B, np.inf)
     loss = torch.empty(B, dtype=torch.float64, device=dg.device)
-    flag = torch.zeros(1, dtype=torch.int32, device=dg.device)
+    flag = dg.flag()
     scratch = dg.scratch(B)
     N.check(N.lib().fm_tr_align(ctypes.byref(dg.struct()), N.ptr(c), B, int(steps),
                                 cfg.translation_lr, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
