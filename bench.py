@@ -1,20 +1,25 @@
 """Benchmark of the FastMap B200 hot path (BASELINE.json metric).
 
-A step = one fused point-pair pass (residual + prune + L1 + IRLS-weighted W
-moments + linearisation gradient terms: the heaviest pass of irls_refine,
-ref/epipolar.py:280-310) over the whole synthetic workload, plus the scalar
-all-reduce (Z, L1) that irls_refine needs per pass when N > 1.
+A step = one fused point-pair pass over the whole workload: residual, prune,
+L1 and IRLS-weighted W moments with the linearisation-gradient terms -- the
+heaviest pass of irls_refine (ref/epipolar.py:280-301) -- plus, when N > 1,
+the all-reduce of the pass scalars {Z, L1} that irls_refine needs per pass
+(inside the timed window).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c5]
-  python bench.py --impl reference ...     # CPU oracle port on the host cores
+  python bench.py --impl reference ...   # the reference's own CPU path (baseline/_ref)
 
 Workload at N=1: BASELINE configs[1] (C2: 500 images, 25,000 image pairs,
 10,000,000 point pairs), generated on the device.  N>1 (torchrun, one rank
-per GPU, NCCL): every rank holds its own C2-sized shard (weak scaling); the
-value is all ranks' point pairs / max-over-ranks device time.
+per GPU, NCCL): every rank holds its own C2-sized shard (weak scaling, the
+headline `value`); `strong` adds C5 (1 B point pairs) split over the ranks
+(contiguous point-balanced image-pair ranges), measured at every N.
 
-The L2 (126 MB) is flushed between timed steps (256 MB write + 256 MB read, outside the
-events); inputs (161 MB) are larger than L2 anyway.
+Before timing, a prefix of the timed pass's outputs is checked against the
+CPU oracle (masks and counts bit-exact, W / L1 / shifted-model terms within
+the north-star tolerances); on a mismatch the bench prints nothing and exits
+non-zero.  The L2 (126 MB) is flushed between timed steps (outside the
+events); the 160 MB store is larger than L2 anyway.
 """
 
 import argparse
@@ -29,11 +34,23 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "point-pair residual+grad evals/sec (fraction of HBM roofline); SfM optimize time s"
 UNIT = "point pairs/s"
-BYTES_PER_POINT = 16.0 + 1.0 / 8.0      # fp32 (x1, y1, x2, y2) + 1 mask bit (read)
-BYTES_PER_PAIR = 72.0 + 36 * 8 + 8 + 4 + 8 + 4 + 4 + 4 + 4  # ghat in, fp64 W moments/L1/count out, indices
+TH = 0.01  # prune threshold of the timed pass (ref/config.py prune_threshold_start)
+
+
+def pass_bytes(n_points_read, n_pairs, precision, l1=True, skip=True):
+    """Algorithmic HBM bytes of one fused pass:
+    per point read: 16 B fp32 coordinates + 1 mask bit;
+    per image pair read: 16 B work descriptor + 72 B ghat (+ 4 B previous
+    count with SKIP_DROPPED); written: 36 moments (fp32: 144 B + 9 fp32
+    linearisation terms 36 B + s0 8 B; fp64: 288 B), count 4 B, L1 8 B.
+    Points of pairs dropped by an earlier prune are skipped (not read)."""
+    per_pair = 16 + 72 + (4 if skip else 0) + 4 + (8 if l1 else 0)
+    per_pair += (144 + 36 + 8) if precision == "fp32" else 288
+    return (16.0 + 1.0 / 8.0) * n_points_read + per_pair * n_pairs
 
 
 def ncu_traffic(config, precision):
@@ -56,8 +73,8 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled DURING the timed region (NVML
-    every 5 ms; nvidia-smi fallback)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML;
+    nvidia-smi fallback)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -126,7 +143,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def dist_setup(n_gpus):
+def dist_setup():
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -143,192 +160,417 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
-# ------------------------------------------------------------ reference arm
-def _ref_worker(args):
-    x1, x2, lengths, ghat, th = args
-    from oracle import fastmap_oracle as O
-    flat = O.FlatPairs(np.column_stack([x1, np.ones(len(x1))]),
-                       np.column_stack([x2, np.ones(len(x2))]), lengths)
-    out = O.point_pass(flat, ghat, threshold=th)
-    return float(out["l1"].sum())
+def host_cores():
+    return len(os.sched_getaffinity(0))
 
 
-def cpu_sample(spec, n_pairs_sample):
-    """A bounded prefix of the workload on the host (fp32 coordinates)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ===================================================== the reference on the CPU
+def _import_reference():
+    """The unmodified reference package from baseline/_ref (installed by
+    tools/install_reference.sh); None when absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "fastmap")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import fastmap  # noqa: F401
+    return fastmap
+
+
+def _ref_worker(conn, chunk, kind):
+    """One host process owning one contiguous chunk of the image pairs: it
+    builds its pairs once, then runs one pass per "go" message.
+
+    kind "reference": the reference's own code (baseline/_ref) for what one
+    fused pass produces (ref/epipolar.py:280-301): current_residuals of every
+    point, the L1 sum over the active points, the prune `active &= res <=
+    th`, and precompute_weights with IRLS weights per pair.  kind "port":
+    the numpy oracle port of the same pass (when baseline/_ref is absent)."""
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    x1, x2, lens, ij, R, C = chunk
+    start = np.concatenate([[0], np.cumsum(lens)])
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from fastmap.epipolar import AdjustmentState, EpipolarPair, current_residuals, \
+            precompute_weights
+        from fastmap.model import PoseState
+        pairs = [EpipolarPair(i=int(ij[q, 0]), j=int(ij[q, 1]), cam_i=0, cam_j=0,
+                              x1=np.column_stack([x1[start[q]:start[q + 1]], np.ones(lens[q])]),
+                              x2=np.column_stack([x2[start[q]:start[q + 1]], np.ones(lens[q])]))
+                 for q in range(len(lens))]
+        poses = PoseState(rotations=R, centers=C, registered=np.ones(len(R), dtype=bool))
+        state = AdjustmentState.from_poses(poses, np.arange(len(R)), 1, True)
+
+        def one_pass():
+            l1 = 0.0
+            res = current_residuals(state, pairs)
+            for p, r in zip(pairs, res):
+                l1 += float(r[p.active].sum())
+                p.active &= r <= TH
+                precompute_weights(p.x1[p.active], p.x2[p.active], residuals=r[p.active])
+            return l1
+    else:
+        from oracle import fastmap_oracle as O
+        flat = O.FlatPairs(np.column_stack([x1, np.ones(len(x1))]),
+                           np.column_stack([x2, np.ones(len(x2))]), lens)
+        params = np.concatenate([np.concatenate([R[:, :, 0], R[:, :, 1]], axis=1).ravel(),
+                                 C.ravel(), np.zeros(1)])
+
+        def one_pass():
+            gh = O.pair_forward(params, len(R), ij[:, 0], ij[:, 1], np.zeros(len(ij), int),
+                                np.zeros(len(ij), int), True)["ghat"]
+            return float(O.point_pass(flat, gh, threshold=TH)["l1"].sum())
+    conn.send("ready")
+    while conn.recv() == "go":
+        conn.send(one_pass())
+    conn.close()
+
+
+def host_scene(spec):
+    """The workload's point pairs as host arrays (generated on the device when
+    there is one, exactly as our arm generates them)."""
     import torch
+
     from paper_2505_04612_b200 import scenes
     device = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
-    sc = scenes.generate(spec, device, pair_slice=slice(0, n_pairs_sample))
-    ids = np.arange(spec.n_images)
-    params = scenes.initial_params(sc, ids, refine_focal=True)
-    from oracle import fastmap_oracle as O
-    ij = sc["ij"]
-    gh = O.pair_forward(params, spec.n_images, ij[:, 0], ij[:, 1], np.zeros(len(ij), int),
-                        np.zeros(len(ij), int), True)["ghat"]
-    return (sc["x1"].cpu().numpy().astype(np.float64), sc["x2"].cpu().numpy().astype(np.float64),
-            sc["lengths"], gh)
+    sc = scenes.generate(spec, device)
+    out = dict(x1=sc["x1"].cpu().numpy().astype(np.float64),
+               x2=sc["x2"].cpu().numpy().astype(np.float64),
+               lengths=sc["lengths"], ij=sc["ij"], R_in=sc["R_in"], c_in=sc["c_in"])
+    del sc
+    return out
 
 
-def time_cpu_pass(spec, n_pairs_sample, procs, repeats=1):
-    """Oracle port of the fused pass on a sample, sharded over `procs`
-    processes; returns (point pairs/s, seconds, points)."""
-    import multiprocessing as mp
-    x1, x2, lengths, gh = cpu_sample(spec, n_pairs_sample)
-    P = len(lengths)
-    bounds = np.linspace(0, P, procs + 1).astype(int)
-    start = np.concatenate([[0], np.cumsum(lengths)])
-    jobs = [(x1[start[a]:start[b]], x2[start[a]:start[b]], lengths[a:b], gh[a:b], 0.01)
-            for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
-    ctx = mp.get_context("fork")
-    best = None
-    with ctx.Pool(len(jobs)) as pool:
-        pool.map(_ref_worker, jobs[:1])  # warm the workers
-        for _ in range(repeats):
+class RefPool:
+    """The reference's CPU path over all host cores: the image pairs split
+    into one contiguous chunk per process (fork; BLAS single-threaded per
+    process); a step = every process runs its pass, timed on the wall clock
+    from the "go" to the last result."""
+
+    def __init__(self, scene, procs, n_pairs=None):
+        import multiprocessing as mp
+        self.kind = "reference" if _import_reference() is not None else "port"
+        lengths = scene["lengths"]
+        P = len(lengths) if n_pairs is None else min(n_pairs, len(lengths))
+        start = np.concatenate([[0], np.cumsum(lengths)])
+        bounds = np.linspace(0, P, procs + 1).astype(int)
+        ctx = mp.get_context("fork")
+        self.conns, self.procs_ = [], []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            if b <= a:
+                continue
+            chunk = (scene["x1"][start[a]:start[b]], scene["x2"][start[a]:start[b]], lengths[a:b],
+                     scene["ij"][a:b], scene["R_in"], scene["c_in"])
+            parent, child = ctx.Pipe()
+            pr = ctx.Process(target=_ref_worker, args=(child, chunk, self.kind), daemon=True)
+            pr.start()
+            self.conns.append(parent)
+            self.procs_.append(pr)
+        for c in self.conns:
+            assert c.recv() == "ready"
+        self.n_points = int(start[P])
+        self.n_pairs = P
+        self.procs = len(self.conns)
+
+    def step(self):
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send("go")
+        for c in self.conns:
+            c.recv()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            c.send("stop")
+        for pr in self.procs_:
+            pr.join(timeout=10)
+
+
+def reference_steps(spec, steps, warmup, n_pairs=None, procs=None):
+    """Time `steps` reference passes (after `warmup`) over all host cores;
+    returns (seconds per step, the pool)."""
+    scene = host_scene(spec)
+    rp = RefPool(scene, procs or host_cores(), n_pairs)
+    del scene
+    try:
+        for _ in range(max(warmup, 1)):
+            rp.step()  # the first pass prunes: later passes are the steady state
+        times = [rp.step() for _ in range(steps)]
+    finally:
+        rp.close()
+    return times, rp
+
+
+def reference_sfm_optimize(spec):
+    """The reference's own per-step costs of the two gradient stages on one
+    core (numpy; it is single-threaded code), stated as extrapolations:
+    quadratic_loss_and_grad per Adam step at C2 (x 900 steps per
+    irls_refine), translation_loss_and_grad per step at C3 (x 17 x 6000 per
+    multi_init_align) -- SURVEY 8d."""
+    ref = _import_reference()
+    if ref is None:
+        return None
+    from threadpoolctl import threadpool_limits
+    from fastmap import translation as RT
+    from fastmap.epipolar import AdjustmentState, EpipolarPair, precompute_weights, \
+        quadratic_loss_and_grad
+    from fastmap.model import PoseState
+
+    from paper_2505_04612_b200 import scenes
+    out = {}
+    with threadpool_limits(1):
+        ps = scenes.generate_poses(spec)
+        P = spec.n_pairs
+        ij = scenes.pair_list(spec)
+        # W per pair does not change the step's cost; a fixed PSD matrix each
+        rng = np.random.default_rng(0)
+        x = rng.normal(size=(8, 3))
+        W = precompute_weights(x, x)
+        pairs = [EpipolarPair(i=int(i), j=int(j), cam_i=0, cam_j=0, x1=np.zeros((0, 3)),
+                              x2=np.zeros((0, 3))) for i, j in ij]
+        poses = PoseState(rotations=ps["R_in"], centers=ps["c_in"],
+                          registered=np.ones(spec.n_images, dtype=bool))
+        state = AdjustmentState.from_poses(poses, np.arange(spec.n_images), 1, True)
+        weights = [W] * P
+        quadratic_loss_and_grad(state, pairs, weights, 1000)
+        t = []
+        for _ in range(3):
             t0 = time.perf_counter()
-            pool.map(_ref_worker, jobs)
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-    Z = int(lengths.sum())
-    return Z / best, best, Z
+            quadratic_loss_and_grad(state, pairs, weights, 1000)
+            t.append(time.perf_counter() - t0)
+        out["quadratic_loss_and_grad_s_per_step_c2"] = min(t)
+        out["irls_refine_steps_c2_extrapolated_s"] = 900 * min(t)
+        ei, ej, d, _ = scenes.translation_graph_c3()
+        g = RT.DirectionGraph(n=2000, edges_i=ei, edges_j=ej, directions=d)
+        c = np.random.default_rng(0).standard_normal((2000, 3))
+        RT.translation_loss_and_grad(c, g)
+        t = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            RT.translation_loss_and_grad(c, g)
+            t.append(time.perf_counter() - t0)
+        out["translation_loss_and_grad_s_per_step_c3"] = min(t)
+        out["multi_init_align_c3_extrapolated_s"] = 17 * 6000 * min(t)
+    out["how"] = ("reference (baseline/_ref) on one host core, best of 3 per call; "
+                  "irls_refine x 900 Adam steps, multi_init_align x 17 x 6000 steps")
+    return out
 
 
 def run_reference(args, spec, world, rank):
+    """--impl reference: the reference's own CPU implementation of the pass
+    on all host cores, on the same workload and config as our arm."""
     if rank != 0:
         return
-    try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(1)
-    except Exception:
-        pass
-    procs = len(os.sched_getaffinity(0))
-    n_pairs_sample = min(spec.n_pairs, max(procs * 10, int(1.5e6 // spec.points_per_pair)))
-    vals = []
-    import multiprocessing as mp
-    x1, x2, lengths, gh = cpu_sample(spec, n_pairs_sample)
-    P = len(lengths)
-    bounds = np.linspace(0, P, procs + 1).astype(int)
-    start = np.concatenate([[0], np.cumsum(lengths)])
-    jobs = [(x1[start[a]:start[b]], x2[start[a]:start[b]], lengths[a:b], gh[a:b], 0.01)
-            for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
-    Z = int(lengths.sum())
-    with mp.get_context("fork").Pool(len(jobs)) as pool:
-        for k in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            pool.map(_ref_worker, jobs)
-            dt = time.perf_counter() - t0
-            if k >= args.warmup:
-                vals.append(dt)
-    t = float(np.mean(vals))
-    v = Z / t
+    times, rp = reference_steps(spec, args.steps, args.warmup)
+    t = float(np.mean(times))
+    v = rp.n_points / t
+    cores = rp.procs
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": f"{args.config.upper()} prefix sample", "pass": "L1+prune+IRLS W"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": f"{Z} point pairs ({P} image pairs) of {args.config.upper()} "
-                                       f"per step, numpy oracle (oracle/fastmap_oracle.py) "
-                                       f"point_pass sharded over {procs} processes"},
+            "data": "synthetic (device-generated ring scene, random-perturbed poses)",
+            "config": workload_config(args, spec, world, rp.n_pairs, rp.n_points),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": rp.kind,
+                             "cpu": cpu_model(),
+                             "sample": f"the whole workload per step: {rp.n_points} point pairs "
+                                       f"({rp.n_pairs} image pairs), current_residuals + L1 + "
+                                       f"prune + precompute_weights (ref/epipolar.py:280-301) "
+                                       f"in {cores} processes"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.skip_optimize:
+        line["sfm_optimize"] = reference_sfm_optimize(spec)
     print(json.dumps(line), flush=True)
 
 
-# --------------------------------------------------------------- our arm
-def run_ours(args, spec, world, rank, local):
-    import ctypes
+def workload_config(args, spec, world, P, Z):
+    return {"workload": f"{args.config.upper()}: {spec.n_images} images, {P} image pairs, "
+                        f"{Z} point pairs per GPU (band {spec.band}, {spec.points_per_pair} pts/pair)",
+            "pass": "fused L1 + prune + IRLS W moments (irls_refine rounds 1-2 pass)",
+            "precision": args.precision,
+            "l2": "flushed between steps (256 MB write + 256 MB read, outside the events) and inputs > L2",
+            "parallelism": f"dp{world} (point pairs sharded by image pair)"}
 
+
+# ================================================================= our arm
+def make_engine(spec, device, args, pair_slice=None, seed_offset=0):
     import torch
-    import torch.distributed as dist
 
-    from paper_2505_04612_b200 import _native as N
     from paper_2505_04612_b200 import epipolar as E
     from paper_2505_04612_b200 import scenes
-
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    if args.strong:
-        # strong scaling: the config's image pairs split into contiguous
-        # ranges over the ranks; each rank generates only its own range
-        lo, hi = spec.n_pairs * rank // world, spec.n_pairs * (rank + 1) // world
-        scene = scenes.generate(spec, device, pair_slice=slice(lo, hi))
-    else:
-        # weak scaling: one config-sized shard per rank (distinct seeds)
-        spec_r = scenes.SceneSpec(**{**spec.__dict__, "seed": spec.seed + rank})
-        scene = scenes.generate(spec_r, device)
+    sp = scenes.SceneSpec(**{**spec.__dict__, "seed": spec.seed + seed_offset})
+    scene = scenes.generate(sp, device, pair_slice=pair_slice)
     store = scenes.device_store(scene, device)
     graph, ids = scenes.device_graph(scene, device)
     params = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
-    stream = torch.cuda.Stream(device)
-    Z = store.n_points
+    eng = E.IrlsEngine(store, graph, params, args.cfg, precision=args.precision)
+    return scene, store, graph, ids, eng
+
+
+def check_prefix(eng, store, mode, n_check=250):
+    """The timed pass on the first n_check image pairs vs the CPU oracle
+    (ref/epipolar.py:280-301 restated, pinned to the reference's golden
+    vectors): run one more pass from a snapshot of the masks and compare
+    counts and masks bit-exact, L1 within 1e-5, W within 2e-5 of the pair's
+    W scale (fp64 moments: 3e-7), the shifted-model terms within 1e-5."""
+    import torch
+
+    from oracle import fastmap_oracle as O
+    from paper_2505_04612_b200 import epipolar as E
     P = store.n_pairs
-    lib = N.lib()
-    with torch.cuda.stream(stream):
-        eng = E.IrlsEngine(store, graph, params, args.cfg, precision=args.precision)
-        eng._ghat()
-    mode = N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
-    flush_rd = torch.ones(64 << 20, dtype=torch.float32, device=device)  # 256 MB, read back clean
-    scal = torch.zeros(2, dtype=torch.float64, device=device)
-    sync_bytes = 0
-
-    def one_pass():
-        eng.point_pass(mode, 0.01, 0, 0)
-
-    def reduce_scalars():
-        scal[0] = eng.buf.l1[:P].sum()
-        scal[1] = eng.buf.n_active[0][:P].sum().double()
-        if world > 1:
-            dist.all_reduce(scal)
-
-    # first pass sets the counts used by SKIP_DROPPED and the steady-state mask
-    with torch.cuda.stream(stream):
-        eng.buf.n_active[0].fill_(1)
-        one_pass()
+    n = min(n_check, P)
+    lens = store.len_caller[:n]
+    off = store.pair_off[:n]
+    idx = np.concatenate([np.arange(o, o + m) for o, m in zip(off, lens)])
+    bits_before = store.active_bits()[torch.as_tensor(idx, device=store.device)].cpu().numpy()
+    eng.point_pass(mode, TH, 1, 0)
     torch.cuda.synchronize()
+    x1 = store.x1[torch.as_tensor(idx, device=store.device)].double().cpu().numpy()
+    x2 = store.x2[torch.as_tensor(idx, device=store.device)].double().cpu().numpy()
+    flat = O.FlatPairs(np.column_stack([x1, np.ones(len(x1))]), np.column_stack([x2, np.ones(len(x2))]),
+                       lens, active=bits_before)
+    # pairs dropped by an earlier prune (prev == 0) are skipped by the pass:
+    # all their points are inactive, so the oracle gives them zero outputs too
+    gh = eng.buf.ghat0[:, :n].cpu().numpy().T
+    ref = O.point_pass(flat, gh, threshold=TH)
+    bits_after = store.active_bits()[torch.as_tensor(idx, device=store.device)].cpu().numpy()
+    bad = []
+    if not np.array_equal(eng.buf.n_active[1][:n].cpu().numpy(), ref["n_active"]):
+        bad.append("active counts")
+    if not np.array_equal(bits_after, flat.active):
+        bad.append("prune masks")
+    l1 = eng.buf.l1[:n].cpu().numpy()
+    if np.max(np.abs(l1 - ref["l1"]) / np.maximum(np.abs(ref["l1"]), 1e-300)) > 1e-5:
+        bad.append("L1")
+    scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
+    if eng.buf.precision == "fp64":
+        W = E.moments_to_weights(eng.buf.mom64[:, :n].cpu().numpy())
+        werr = float(np.max(np.abs(W - ref["W"]) / scale))
+        wtol = 3e-7
+    else:
+        W = E.moments_to_weights(eng.buf.mom32[:, :n].cpu().numpy())
+        werr = float(np.max(np.abs(W - ref["W"]) / scale))
+        wtol = 2e-5
+        vg = eng.buf.vgrad[:, :n].cpu().numpy().T
+        vscale = max(float(np.abs(O.terms_of(flat.x1, flat.x2)).sum(axis=0).max()), 1.0)
+        if np.max(np.abs(vg - ref["vgrad"])) > 1e-5 * vscale:
+            bad.append("linearisation terms")
+        s0 = eng.buf.s0[:n].cpu().numpy()
+        if np.max(np.abs(s0 - ref["s0"]) / np.maximum(np.abs(ref["s0"]), 1e-300)) > 1e-5:
+            bad.append("s0")
+    if werr > wtol:
+        bad.append(f"W ({werr:.2e} > {wtol})")
+    return {"pairs": n, "points": int(lens.sum()), "ok": not bad, "mismatch": bad,
+            "W_max_rel_err": werr, "masks": "bit-exact" if "prune masks" not in bad else "differ",
+            "counts": "bit-exact" if "active counts" not in bad else "differ"}
 
-    def timed(k_steps, with_flush=True):
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
-        with torch.cuda.stream(stream):
-            for k in range(k_steps):
-                if with_flush:
-                    # evict the store from L2: write 256 MB, then read another
-                    # 256 MB so L2 ends up holding clean lines (no dirty
-                    # write-back charged to the timed pass)
-                    flush.fill_(k & 0xFF)
-                    flush_rd.sum()
-                # keep the GPU busy until the host has queued the pass, so the
-                # events bracket device work only (not host launch latency)
-                torch.cuda._sleep(400_000)
-                starts[k].record(stream)
-                one_pass()
-                ends[k].record(stream)
-                reduce_scalars()
+
+def time_passes(eng, stream, k_steps, reduce_fn, flush=True):
+    """k_steps passes, each bracketed by CUDA events on the launching stream
+    (the scalar reduction / all-reduce inside the window)."""
+    import torch
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=stream.device)
+    flush_r = torch.ones(64 << 20, dtype=torch.float32, device=stream.device)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
+    with torch.cuda.stream(stream):
+        for k in range(k_steps):
+            if flush:
+                # evict the store from L2: write 256 MB, then read another
+                # 256 MB so L2 holds clean lines (no dirty write-back charged
+                # to the timed pass)
+                flush_w.fill_(k & 0xFF)
+                flush_r.sum()
+            torch.cuda._sleep(400_000)  # the events bracket device work only
+            starts[k].record(stream)
+            eng.point_pass(HOT_MODE(), TH, 0, 0)
+            reduce_fn()
+            ends[k].record(stream)
+    torch.cuda.synchronize()
+    del flush_w, flush_r
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def HOT_MODE():
+    from paper_2505_04612_b200 import _native as N
+    return N.FM_PASS_L1 | N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED
+
+
+def max_over_ranks(x, device, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, device, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t)
+    return float(t.item())
+
+
+def run_ours(args, spec, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device)
+    # weak scaling: one config-sized shard per rank (distinct seeds)
+    with torch.cuda.stream(stream):
+        scene, store, graph, ids, eng = make_engine(spec, device, args, seed_offset=rank)
+        eng._ghat()
+        Z, P = store.n_points, store.n_pairs
+        def reduce_scalars():
+            # what irls_refine needs after a pass: {L1, Z, kept pairs}, fused
+            # into the pass kernel (fixed order); over all ranks when N > 1
+            if world > 1:
+                dist.all_reduce(eng.buf.tot)
+
+        # first pass: prunes and sets the counts SKIP_DROPPED uses (steady state)
+        eng.buf.n_active[0].fill_(1)
+        eng.point_pass(HOT_MODE(), TH, 0, 0)
         torch.cuda.synchronize()
-        return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dropped = int((eng.buf.n_active[0][:P] == 0).sum().item())
+    points_read = Z - int(np.asarray(store.len_caller)[(eng.buf.n_active[0][:P] == 0).cpu().numpy()].sum())
+    with torch.cuda.stream(stream):
+        chk = check_prefix(eng, store, HOT_MODE()) if rank == 0 else {"ok": True}
+    if not chk["ok"]:
+        print(f"bench: the timed pass does not match the CPU oracle on a prefix: {chk}",
+              file=sys.stderr, flush=True)
+        sys.exit(3)
 
-    timed(args.warmup)
+    time_passes(eng, stream, args.warmup, reduce_scalars)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms = timed(args.steps)
-    ms_step = float(np.mean(ms))
-    t_max = torch.tensor([ms_step], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_step = float(t_max.item())
-    Z_all = torch.tensor([Z], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(Z_all)
-    value = float(Z_all.item()) / (ms_step * 1e-3)
+        ms = time_passes(eng, stream, args.steps, reduce_scalars)
+    ms_step = max_over_ranks(np.mean(ms), device, world)
+    Z_all = sum_over_ranks(Z, device, world)
+    value = Z_all / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (the pass) from the same events
-    bytes_launch = BYTES_PER_POINT * Z + BYTES_PER_PAIR * P
+    # roofline of the dominant kernel (the pass), from the same events
+    bytes_launch = pass_bytes(points_read, P, args.precision)
     hbm, hbm_kind = peaks()
     achieved = bytes_launch / (ms_step * 1e-3) / 1e9
 
-    # --------------------------------------------------------------- e2e
+    # ------------------------------------------------------------------ e2e
     # through the C ABI with HOST buffers: pinned host store columns -> H2D,
     # pass, per-pair results -> D2H, every step.
     h_x1 = store.x1.cpu().pin_memory()
@@ -348,7 +590,8 @@ def run_ours(args, spec, world, rank, local):
                 store.x1.copy_(h_x1, non_blocking=True)
                 store.x2.copy_(h_x2, non_blocking=True)
                 store.active.copy_(h_act, non_blocking=True)
-                one_pass()
+                eng.point_pass(HOT_MODE(), TH, 0, 0)
+                reduce_scalars()
                 for h, o in zip(h_outs, outs):
                     h.copy_(o, non_blocking=True)
             s1.record(stream)
@@ -356,23 +599,112 @@ def run_ours(args, spec, world, rank, local):
         return s0.elapsed_time(s1) / k_steps
 
     e2e_steps(2)
-    e2e_ms = e2e_steps(max(3, min(args.steps, 10)))
-    t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t_e2e.item())
+    e2e_ms = max_over_ranks(e2e_steps(max(3, min(args.steps, 10))), device, world)
 
-    # ------------------------------------------- SfM optimize time (rank 0)
+    # --------------------------------------------- strong scaling (secondary)
+    strong = None
+    if not args.skip_strong:
+        strong = strong_bench(args, device, stream, world, rank)
+
+    # ---------------------------------------------------- SfM optimize time
     extra = {}
-    if not args.skip_optimize and world > 1:
-        # config 3 with the 16 random starts split over the ranks, and the
-        # rank-0 scene's irls_refine with its point pairs sharded over the
-        # ranks (NCCL all-reduce of the per-image gradient per Adam step)
-        tr = translation_bench(device, stream, sharded=True)
-        ep = sharded_irls_bench(spec, args, device, stream, world, rank)
-        if rank == 0:
-            extra["sfm_optimize"] = {"translation_sharded_over_ranks": world, **tr, **ep}
-    if rank == 0 and not args.skip_optimize:
+    if not args.skip_optimize:
+        extra["sfm_optimize"] = sfm_optimize(args, spec, scene, store, graph, ids, device, stream,
+                                             world, rank)
+
+    # ---------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        times, rp = reference_steps(spec, 3, 1, n_pairs=min(P, 5000))
+        t = float(np.min(times))
+        cpu = {"value": rp.n_points / t, "unit": UNIT, "cores": rp.procs, "kind": rp.kind,
+               "cpu": cpu_model(),
+               "sample": f"{rp.n_points} point pairs ({rp.n_pairs} image pairs, the first "
+                         f"{rp.n_pairs} of {args.config.upper()}), the reference's "
+                         f"current_residuals + L1 + prune + precompute_weights "
+                         f"(ref/epipolar.py:280-301) in {rp.procs} processes, best of 3: {t:.3f} s"}
+
+    # per step: the pass with its fused totals (+ the combine kernel when
+    # pairs span several work items)
+    launches = args.steps * (1 + (1 if store.n_items > store.n_pairs else 0))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": ("f64 (residual, W moments, prune decisions) on f32 coordinates"
+                      if args.precision == "fp64" else
+                      "f32 W moments (shifted model) + f64 residual on f32 coordinates"),
+            "data": "synthetic (device-generated ring scene, random-perturbed poses)",
+            "config": workload_config(args, spec, world, P, Z),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": ncu_traffic(args.config, args.precision),
+                         "peak_kind": hbm_kind, "algorithmic_bytes_per_launch": bytes_launch,
+                         "bytes_model": "16.125 B per point read (pairs not dropped) + 292 B per "
+                                        "image pair (fp32 moments; DESIGN.md 3.1)",
+                         "dropped_pairs_skipped": dropped},
+            "cpu_baseline": cpu,
+            "e2e": {"value": Z_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "parity_check": chk,
+            "strong": strong,
+            **extra,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10):
+    """C5 (1 B point pairs) split over the ranks by contiguous image-pair
+    ranges (each rank generates only its range), the same pass + scalar
+    all-reduce, max over ranks.  At N=1 the whole C5 on one GPU."""
+    import gc
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_04612_b200 import scenes
+    spec = scenes.CONFIGS[cfg_name]
+    lo, hi = spec.n_pairs * rank // world, spec.n_pairs * (rank + 1) // world
+    with torch.cuda.stream(stream):
+        scene, store, graph, ids, eng = make_engine(spec, device, args, pair_slice=slice(lo, hi))
+        del scene
+        gc.collect()
+        eng._ghat()
+        def reduce_scalars():
+            if world > 1:
+                dist.all_reduce(eng.buf.tot)
+
+        eng.buf.n_active[0].fill_(1)
+        eng.point_pass(HOT_MODE(), TH, 0, 0)
+    torch.cuda.synchronize()
+    time_passes(eng, stream, 3, reduce_scalars)
+    if world > 1:
+        dist.barrier()
+    ms = max_over_ranks(np.mean(time_passes(eng, stream, steps, reduce_scalars)), device, world)
+    total = spec.n_pairs * spec.points_per_pair
+    out = {"config": f"{cfg_name.upper()}: {spec.n_pairs} image pairs / {total} point pairs split "
+                     f"over {world} GPU(s)", "scaling": "strong", "value": total / (ms * 1e-3),
+           "unit": UNIT, "ms_per_step": ms, "steps": steps}
+    del eng, store, graph
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
+def sfm_optimize(args, spec, scene, store, graph, ids, device, stream, world, rank):
+    """SfM optimize time: irls_refine at C2 on the device-built
+    store (engine) and through the drop-in Python API from EpipolarPair
+    objects (store build + upload + write-back included), multi_init_align at
+    C3.  N > 1: irls_refine sharded over the ranks, the starts of
+    multi_init_align split over the ranks."""
+    import torch
+
+    from paper_2505_04612_b200 import epipolar as E
+    from paper_2505_04612_b200 import scenes
+    out = {}
+    if rank == 0:
         params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
         store.reset_active()
         with torch.cuda.stream(stream):
@@ -382,66 +714,60 @@ def run_ours(args, spec, world, rank, local):
             l1h = eng2.run()
             torch.cuda.synchronize()
             t_irls = time.perf_counter() - t0
-        extra.setdefault("sfm_optimize", {}).update(
-            {"irls_refine_s": t_irls, "l1_history": l1h, "dropped_pairs": eng2.dropped,
-             "active_pairs": eng2.kept, "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"})
-        if world == 1:
-            extra["sfm_optimize"].update(translation_bench(device, stream))
+        out.update({"irls_refine_engine_s": t_irls, "l1_history": l1h,
+                    "dropped_pairs": eng2.dropped, "active_pairs": eng2.kept,
+                    "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"})
+        if not args.skip_api:
+            out.update(api_irls_bench(args, scene, device, stream))
+    if world > 1:
+        out.update(sharded_irls_bench(spec, args, device, stream, world, rank))
+    out.update(translation_bench(device, stream, sharded=world > 1))
+    return out
 
-    # ---------------------------------------------------- CPU baseline
-    cpu = None
-    if rank == 0 and world == 1 and not args.skip_cpu:
-        procs = 1
-        try:
-            from threadpoolctl import threadpool_limits
-            threadpool_limits(1)
-        except Exception:
-            pass
-        n_s = max(64, int(1.0e6 // spec.points_per_pair))
-        v_cpu, t_cpu, z_cpu = time_cpu_pass(spec, n_s, procs)
-        cpu = {"value": v_cpu, "unit": UNIT, "cores": procs, "kind": "port",
-               "sample": f"{z_cpu} point pairs ({n_s} image pairs) prefix of {args.config.upper()}, "
-                         f"oracle/fastmap_oracle.py point_pass, single process, {t_cpu:.2f} s"}
 
-    launches = args.steps * (1 + (1 if store.n_items > store.n_pairs else 0))
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
-            "dtype": ("f64 (residual, W moments, prune decisions) on f32 coordinates"
-                      if args.precision == "fp64" else
-                      "f32 W moments (shifted model) + f64 residual on f32 coordinates"),
-            "data": "synthetic (device-generated ring scene, random-perturbed poses)",
-            "config": {"workload": f"{args.config.upper()}: {spec.n_images} images, "
-                                   + (f"{spec.n_pairs} image pairs / {spec.n_pairs * spec.points_per_pair} "
-                                      f"point pairs split over {world} GPU(s)" if args.strong else
-                                      f"{P} image pairs, {Z} point pairs per GPU")
-                                   + f" (band {spec.band}, {spec.points_per_pair} pts/pair)",
-                       "pass": "fused L1 + prune + IRLS W moments (irls_refine rounds 1-2 pass)",
-                       "precision": args.precision,
-                       "l2": "flushed between steps (256 MB write + 256 MB read, outside the events) and inputs > L2",
-                       "parallelism": f"dp{world} (point pairs sharded by image pair)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(args.config, args.precision),
-                         "peak_kind": hbm_kind,
-                         "algorithmic_bytes_per_launch": bytes_launch},
-            "cpu_baseline": cpu,
-            "e2e": {"value": world * Z / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            **extra,
-        }
-        print(json.dumps(line), flush=True)
+def api_irls_bench(args, scene, device, stream):
+    """The drop-in irls_refine (paper_2505_04612_b200.epipolar.irls_refine,
+    the function install() puts at ref/pipeline.py:248) called as the
+    pipeline calls it: a list of EpipolarPair with fp64 host coordinates.
+    The wall time includes the store build, the upload and the mask
+    write-back; `irls_refine_engine_s` is the same run on a store already
+    on the device."""
+    import torch
+
+    from paper_2505_04612_b200 import epipolar as E
+
+    class Poses:  # the reference's PoseState fields (ref/model.py:129-135)
+        def __init__(self, rotations, centers, registered=None):
+            self.rotations, self.centers = rotations, centers
+            self.registered = np.ones(len(rotations), dtype=bool) if registered is None else registered
+
+    x1 = scene["x1"].double().cpu().numpy()
+    x2 = scene["x2"].double().cpu().numpy()
+    lens = scene["lengths"]
+    start = np.concatenate([[0], np.cumsum(lens)])
+    ones = np.ones((int(lens.max()), 1))
+    pairs = [E.EpipolarPair(i=int(i), j=int(j), cam_i=0, cam_j=0,
+                            x1=np.hstack([x1[start[q]:start[q + 1]], ones[:lens[q]]]),
+                            x2=np.hstack([x2[start[q]:start[q + 1]], ones[:lens[q]]]))
+             for q, (i, j) in enumerate(scene["ij"])]
+    poses = Poses(scene["R_in"].copy(), scene["c_in"].copy())
+    with torch.cuda.stream(stream):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, rep = E.irls_refine(poses, pairs, args.cfg, n_cameras=1)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    return {"irls_refine_api_s": dt, "api_l1_history": rep["l1_history"],
+            "api_note": "drop-in irls_refine on 25,000 EpipolarPair objects (fp64 host arrays): "
+                        "store build + H2D upload + device schedule + mask write-back"}
 
 
 def sharded_irls_bench(spec, args, device, stream, world, rank):
     """irls_refine of the rank-0 C2 scene with its image pairs split into
-    contiguous point-balanced ranges over the ranks (parallel.ShardedIrlsEngine:
-    local passes, one all-reduce of the packed gradient per Adam step)."""
+    contiguous point-balanced ranges over the ranks (parallel.ShardedIrlsEngine)."""
     import torch
     import torch.distributed as dist
+
     from paper_2505_04612_b200 import parallel as P_
     from paper_2505_04612_b200 import scenes
     from paper_2505_04612_b200.store import PairGraph, PointPairStore
@@ -468,17 +794,18 @@ def sharded_irls_bench(spec, args, device, stream, world, rank):
         l1h = eng.run()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-    t = torch.tensor([dt], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"irls_refine_sharded_s": float(t.item()), "irls_sharded_l1_history": l1h,
-            "irls_sharded_over_ranks": world, "irls_sharded_pairs_rank0": hi - lo}
+    return {"irls_refine_sharded_s": max_over_ranks(dt, device, world),
+            "irls_sharded_l1_history": l1h, "irls_sharded_over_ranks": world,
+            "irls_sharded_pairs_rank0": hi - lo}
 
 
 def translation_bench(device, stream, sharded=False):
     """BASELINE configs[2]: 16 batched inits, 2k nodes / 200k edges, 6000
-    steps each + merge + final 6000-step run (ref/translation.py:169-186).
-    sharded: the starts split over the torch.distributed ranks (collective)."""
+    steps each + merge + final 6000-step run (ref/translation.py:169-186),
+    bitwise the reference's result.  sharded: the starts split over the
+    torch.distributed ranks."""
     import torch
+
     from paper_2505_04612_b200 import parallel as P_
     from paper_2505_04612_b200 import translation as T
     from paper_2505_04612_b200.scenes import translation_graph_c3
@@ -489,34 +816,29 @@ def translation_bench(device, stream, sharded=False):
     class C:
         translation_lr, translation_steps, translation_inits = 1e-3, 6000, 16
         adam_beta1, adam_beta2, adam_eps = 0.9, 0.999, 1e-8
+
     class Cw(C):
         translation_steps = 200
 
+    run = P_.multi_init_align_sharded if sharded else T.multi_init_align
     with torch.cuda.stream(stream):
         # warm-up on the same graph and batch shape: device graph upload and
         # the CUDA-graph captures of the batched and the final descent
-        if sharded:
-            P_.multi_init_align_sharded(g, Cw, seed=0)
-        else:
-            T.multi_init_align(g, Cw, seed=0)
+        run(g, Cw, seed=0)
         torch.cuda.synchronize()
         if sharded:
             import torch.distributed as dist
             dist.barrier()
         t0 = time.perf_counter()
-        if sharded:
-            centers, loss = P_.multi_init_align_sharded(g, C, seed=0)
-        else:
-            centers, loss = T.multi_init_align(g, C, seed=0)
+        centers, loss = run(g, C, seed=0)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if sharded:
-            t = torch.tensor([dt], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+    if sharded:
+        dt = max_over_ranks(dt, device, int(os.environ.get("WORLD_SIZE", "1")))
     evals = (16 + 1) * 6000 * m
     return {"multi_init_align_s": dt, "translation_loss": loss,
-            "translation_config": "C3: 2000 nodes, 200000 edges, 16 inits x 6000 steps + final (after one 200-step warm-up call)",
+            "translation_config": "C3: 2000 nodes, 200000 edges, 16 inits x 6000 steps + final "
+                                  "(after one 200-step warm-up call); bitwise the reference",
             "translation_edge_evals_per_s": evals / dt}
 
 
@@ -527,11 +849,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"])
-    ap.add_argument("--strong", action="store_true",
-                    help="split the config's image pairs over the ranks (strong scaling; "
-                         "default: one config-sized shard per rank)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-optimize", action="store_true")
+    ap.add_argument("--skip-strong", action="store_true")
+    ap.add_argument("--skip-api", action="store_true")
     ap.add_argument("--precision", default="fp32", choices=["fp64", "fp32"],
                     help="W-moment accumulation of the pass (irls_refine default: fp32)")
     args = ap.parse_args()
@@ -540,7 +861,7 @@ def main():
     from paper_2505_04612_b200.config import HotPathConfig
     args.cfg = HotPathConfig()
     spec = scenes.CONFIGS[args.config]
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, spec, world, rank)
     else:

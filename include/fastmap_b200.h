@@ -108,6 +108,48 @@ typedef struct fm_point_store {
   const double* x2d;
 } fm_point_store;
 
+/*
+ * Build the store on the device from the caller's point arrays: x1, x2 are
+ * [Z][dim] fp64 (dim 2: z == 1, or 3), every EpipolarPair's x1 / x2
+ * (ref/epipolar.py:19-36) concatenated in CALLER pair order; active_in [Z]
+ * uint8 (NULL = all active); caller_start [P+1] the caller-order point
+ * offsets; caller_rank [P] the stored (i, j)-sorted position of caller pair
+ * k.  The store's layout fields (pair_off, n_slots, ...) and output columns
+ * must be set: fp32 x1/x2 (+ x1z/x2z when z != 1) or fp64 x1d/x2d.  Writes
+ * the coordinate columns (padding zeroed) and the packed active bits.
+ * sanitize != 0 zeroes non-finite points and clears their bit (a non-finite
+ * residual fails the first prune, ref/epipolar.py:283).
+ */
+int fm_store_build(const fm_point_store* store, const double* x1, const double* x2,
+                   int32_t dim, const uint8_t* active_in, const int64_t* caller_start,
+                   const int64_t* caller_rank, int32_t sanitize, void* stream);
+
+/* Active bit of every caller point, caller order: out [Z] uint8 (the
+ * in-place mask write-back of ref/epipolar.py:283). */
+int fm_store_gather_mask(const fm_point_store* store, const int64_t* caller_start,
+                         const int64_t* caller_rank, uint8_t* out, void* stream);
+
+/* out[z] = slot_values[slot of caller point z] (per-point pass outputs in
+ * caller order, e.g. current_residuals ref/epipolar.py:251-255). */
+int fm_store_gather_slots(const fm_point_store* store, const int64_t* caller_start,
+                          const int64_t* caller_rank, const double* slot_values,
+                          double* out, void* stream);
+
+/* slot_out[slot of caller point z] = caller_values[z] (caller-order inputs,
+ * e.g. the residuals argument of precompute_weights ref/epipolar.py:46-59). */
+int fm_store_scatter_slots(const fm_point_store* store, const int64_t* caller_start,
+                           const int64_t* caller_rank, const double* caller_values,
+                           double* slot_out, void* stream);
+
+/*
+ * The three scalars irls_refine needs after a pass (ref/epipolar.py:282-291,
+ * :156-160): out3 = {sum l1 (l1 may be NULL -> 0), Z = sum n_active,
+ * kept = #pairs with n_active > 0}, in one launch and a fixed order.
+ */
+size_t fm_pass_totals_scratch_bytes(void);
+int fm_pass_totals(const double* l1, const int32_t* n_active, int64_t n_pairs, double* out3,
+                   void* scratch, size_t scratch_bytes, void* stream);
+
 /* Fill store->item_desc from the pair / item arrays (one small kernel). */
 int fm_point_store_describe(const fm_point_store* store, void* stream);
 
@@ -138,8 +180,15 @@ typedef struct fm_pass_out {
   double* l1;         /* [n_pairs]     or NULL */
   int32_t* n_active;  /* [n_pairs]     or NULL; post-prune active count */
   double* residual;   /* [n_slots]     or NULL; FM_PASS_RES_OUT */
+  /* [3] or NULL: {sum of l1 (0 without FM_PASS_L1), Z = sum of n_active,
+   * kept pairs = #(n_active > 0)} of this pass -- the scalars irls_refine
+   * needs per pass (ref/epipolar.py:282-291, :156-160).  Fused into the hot
+   * kernel (fixed order, no extra launch); needs n_active. */
+  double* totals;
 } fm_pass_out;
 
+/* Scratch of fm_point_pass.  It must be ZEROED before its first use (the
+ * fused-totals ticket lives at offset 0; every launch leaves it zero). */
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store);
 
 /*

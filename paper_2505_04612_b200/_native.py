@@ -58,7 +58,7 @@ class PointStore(ctypes.Structure):
 
 class PassOut(ctypes.Structure):
     _fields_ = [("mom32", _P), ("mom64", _P), ("vgrad", _P), ("s0", _P), ("l1", _P),
-                ("n_active", _P), ("residual", _P)]
+                ("n_active", _P), ("residual", _P), ("totals", _P)]
 
 
 class PairGraph(ctypes.Structure):
@@ -91,6 +91,12 @@ SIGNATURES = {
     "fm_device_count": (ctypes.c_int, []),
     "fm_point_pass_scratch_bytes": (_SZ, [ctypes.POINTER(PointStore)]),
     "fm_point_store_describe": (ctypes.c_int, [ctypes.POINTER(PointStore), _P]),
+    "fm_store_build": (ctypes.c_int, [ctypes.POINTER(PointStore), _P, _P, _I32, _P, _P, _P, _I32, _P]),
+    "fm_store_gather_mask": (ctypes.c_int, [ctypes.POINTER(PointStore), _P, _P, _P, _P]),
+    "fm_store_gather_slots": (ctypes.c_int, [ctypes.POINTER(PointStore), _P, _P, _P, _P, _P]),
+    "fm_store_scatter_slots": (ctypes.c_int, [ctypes.POINTER(PointStore), _P, _P, _P, _P, _P]),
+    "fm_pass_totals_scratch_bytes": (_SZ, []),
+    "fm_pass_totals": (ctypes.c_int, [_P, _P, _I64, _P, _P, _SZ, _P]),
     "fm_point_pass": (ctypes.c_int, [ctypes.POINTER(PointStore), ctypes.c_uint, _F64, _P, _P, _P,
                                      ctypes.POINTER(PassOut), _P, _SZ, _P]),
     "fm_epi_scratch_bytes": (_SZ, [ctypes.POINTER(PairGraph)]),

@@ -16,7 +16,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libfastmap_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
-SOURCES = ["fm_core.cu", "fm_point_pass.cu", "fm_epipolar.cu", "fm_translation.cu", "fm_sphere.cu",
+SOURCES = ["fm_core.cu", "fm_store.cu", "fm_point_pass.cu", "fm_epipolar.cu", "fm_translation.cu", "fm_sphere.cu",
            "fm_fundamental.cu", "fm_rotation.cu", "fm_tracks.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -47,7 +47,7 @@ def build(force=False, verbose=False, extra=(), out=None):
     from concurrent.futures import ThreadPoolExecutor
     target = out or LIB_PATH
     tmp = target + ".tmp"
-    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--extended-lambda", "-Xcompiler", "-fPIC",
              "-I", os.path.join(REPO_DIR, "include"), *extra]
     with tempfile.TemporaryDirectory() as td:
         objs = [os.path.join(td, s.replace(".cu", ".o")) for s in SOURCES]

@@ -71,6 +71,11 @@ struct PartialBufs {
   double* s0;  // [n_items]
   double* l1;  // [n_items]
   int64_t cap; // items the buffers hold
+  // fused pass totals (hot kernel, one item per pair): per-block {L1, Z,
+  // kept} partials, the ticket of the last block, the output (or NULL)
+  double* tot_part;
+  unsigned* tot_ticket;
+  double* totals;
 };
 
 #ifdef FM_HOT_TRACE
@@ -595,6 +600,63 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
       }
     }
   }
+  if (part.totals) {
+    // fused {L1, Z, kept} of the pass (irls_refine's per-pass scalars,
+    // ref/epipolar.py:282-291): item sums on the item's lanes, the warp's
+    // items in order, the block's warps in order, then the last block to
+    // finish adds the block partials in block order -- fixed order, one launch
+    __shared__ double tot_sm[kGrpWarps][3];
+    __shared__ int tot_last;
+    const double il1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
+    const double icnt = group_sum<L>((double)acc.cnt);
+    double w3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < IPW; ++q) {
+      const double a = __shfl_sync(0xffffffffu, il1, q * L);
+      const double c = __shfl_sync(0xffffffffu, icnt, q * L);
+      if (item_base + group * IPW + q < NI) {
+        w3[0] += a;
+        w3[1] += c;
+        w3[2] += c > 0.0 ? 1.0 : 0.0;
+      }
+    }
+    if (lane == 0) {
+      tot_sm[wib][0] = w3[0];
+      tot_sm[wib][1] = w3[1];
+      tot_sm[wib][2] = w3[2];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b3[3] = {0.0, 0.0, 0.0};
+      for (int wq = 0; wq < kGrpWarps; ++wq)
+        for (int k = 0; k < 3; ++k) b3[k] += tot_sm[wq][k];
+      for (int k = 0; k < 3; ++k) part.tot_part[3 * (int64_t)blockIdx.x + k] = b3[k];
+      __threadfence();
+      tot_last = atomicAdd(part.tot_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (tot_last) {
+      // the last block: its threads sum the block partials (thread t takes
+      // blocks t, t + T, ... in order), then a fixed tree in the idle rings
+      __threadfence();
+      constexpr int T = kGrpWarps * 32;
+      double t3[3] = {0.0, 0.0, 0.0};
+      for (unsigned bq = threadIdx.x; bq < gridDim.x; bq += T)
+        for (int k = 0; k < 3; ++k) t3[k] += __ldcg(part.tot_part + 3 * (int64_t)bq + k);
+      double* red = reinterpret_cast<double*>(smem_raw);
+      for (int k = 0; k < 3; ++k) red[k * T + threadIdx.x] = t3[k];
+      __syncthreads();
+      for (int st = T / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st)
+          for (int k = 0; k < 3; ++k) red[k * T + threadIdx.x] += red[k * T + threadIdx.x + st];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 3; ++k) part.totals[k] = red[k * T];
+        *part.tot_ticket = 0;  // re-armed for the next launch
+      }
+    }
+  }
 #ifdef FM_HOT_TRACE
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < 16384) g_hot_trace[blockIdx.x][3] = globaltimer();
@@ -1027,8 +1089,9 @@ int fm_debug_hot_trace(void* host_out) {
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store) {
   if (!store) return 0;
   const size_t ni = (size_t)store->n_items;
-  return scratch_round(ni * kNumRed * sizeof(double)) + 2 * scratch_round(ni * sizeof(double)) +
-         scratch_round(ni * 4 * sizeof(int32_t)) + 256;
+  return scratch_round(sizeof(unsigned)) + scratch_round(ni * kNumRed * sizeof(double)) +
+         2 * scratch_round(ni * sizeof(double)) + scratch_round(ni * 4 * sizeof(int32_t)) +
+         scratch_round((3 * ni + 192) * sizeof(double)) + 256;
 }
 
 int fm_point_store_describe(const fm_point_store* store, void* stream) {
@@ -1071,11 +1134,26 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE(f64 ? out->mom64 != nullptr : out->mom32 != nullptr, "moment output missing");
     if ((m & FM_PASS_IRLS) && !f64) FM_REQUIRE(out->vgrad && out->s0, "IRLS pass needs vgrad/s0");
   }
-  PartialBufs part{nullptr, nullptr, nullptr, 0};
+  PartialBufs part{nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr};
   cudaStream_t st = as_stream(stream);
   fm_point_store s2 = s;  // with item descriptors
+  double* tot_part = nullptr;
+  size_t tot_bytes = 0;
   {
     Scratch sc(scratch, scratch_bytes);
+    // at offset 0 always: the fused-totals ticket, zero when the scratch is
+    // first used (the header asks for zeroed scratch) and re-armed by every
+    // launch that uses it
+    unsigned* ticket = sc.take<unsigned>(1);
+    if (out->totals) {
+      tot_bytes = (3 * (size_t)s.n_items + 192) * sizeof(double);
+      tot_part = sc.take<double>(3 * (size_t)s.n_items + 192);
+      if (s.n_items == s.n_pairs) {
+        part.tot_part = tot_part;
+        part.tot_ticket = ticket;
+        part.totals = out->totals;
+      }
+    }
     if (s.n_items > s.n_pairs) {
       part.red = sc.take<double>((size_t)s.n_items * kNumRed);
       part.s0 = sc.take<double>((size_t)s.n_items);
@@ -1089,22 +1167,35 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE((sc.used == 0 || scratch) && sc.ok(), "point-pass scratch too small (%zu < %zu)",
                scratch_bytes, sc.used);
   }
-  if (d64) return dispatch_generic<kXYZ64, true>(m, s2, threshold, ghat, res_in, prev_active, *out, part, st);
-  if (!homog && s.slot_align >= kBlkSlots && s.slot_align % kBlkSlots == 0) {
+  int rc = FM_OK;
+  bool fused = false;  // totals computed inside the hot kernel
+  bool handled = false;
+  if (d64) {
+    rc = dispatch_generic<kXYZ64, true>(m, s2, threshold, ghat, res_in, prev_active, *out, part, st);
+    handled = true;
+  } else if (!homog && s.slot_align >= kBlkSlots && s.slot_align % kBlkSlots == 0) {
     // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
     const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
-    bool handled = false;
     if (hot_f64 || (m & FM_PASS_IRLS)) {
-      const int rc = dispatch_hot(m, hot_f64, s2, threshold, ghat, prev_active, *out, part, st, &handled);
-      if (handled) return rc;
+      rc = dispatch_hot(m, hot_f64, s2, threshold, ghat, prev_active, *out, part, st, &handled);
+      fused = handled && part.totals != nullptr;
     }
   }
-  if (homog) {
-    return f64 ? dispatch_generic<kXYZ32, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
-               : dispatch_generic<kXYZ32, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+  if (!handled) {
+    PartialBufs gp = part;
+    gp.totals = nullptr;
+    if (homog)
+      rc = f64 ? dispatch_generic<kXYZ32, true>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st)
+               : dispatch_generic<kXYZ32, false>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st);
+    else
+      rc = f64 ? dispatch_generic<kXY32, true>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st)
+               : dispatch_generic<kXY32, false>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st);
   }
-  return f64 ? dispatch_generic<kXY32, true>(m, s, threshold, ghat, res_in, prev_active, *out, part, st)
-             : dispatch_generic<kXY32, false>(m, s, threshold, ghat, res_in, prev_active, *out, part, st);
+  if (rc || !out->totals || fused) return rc;
+  // generic kernels / pairs split over several items: a separate reduction
+  FM_REQUIRE(out->n_active, "totals need out->n_active");
+  return fm_pass_totals((m & FM_PASS_L1) ? out->l1 : nullptr, out->n_active, s.n_pairs, out->totals,
+                        tot_part, tot_bytes, stream);
 }
 
 }  // extern "C"

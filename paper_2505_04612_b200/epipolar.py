@@ -106,9 +106,7 @@ def precompute_weights(x1, x2, residuals=None):
     mode = N.FM_PASS_MOMENTS | N.FM_PASS_ALL_POINTS | N.FM_PASS_F64
     res = None
     if residuals is not None:
-        r = np.zeros(store.n_slots)
-        r[store.point_slot] = np.asarray(residuals, dtype=np.float64).reshape(-1)
-        res = torch.as_tensor(r, device=device)
+        res = store.scatter_slots(np.asarray(residuals, dtype=np.float64).reshape(-1))
         mode |= N.FM_PASS_RES_IN
     _pass(store, mode, res_in=res, out={"mom64": mom})
     return moments_to_weights(mom.cpu().numpy())[0]
@@ -299,7 +297,7 @@ def current_residuals(state, pairs):
     store = prob.store
     res = torch.zeros(store.n_slots, dtype=torch.float64, device=prob.device)
     _pass(store, N.FM_PASS_ALL_POINTS | N.FM_PASS_RES_OUT, ghat=gh, out={"residual": res})
-    flat = res[torch.from_numpy(store.point_slot).to(prob.device)].cpu().numpy()
+    flat = store.gather_slots(res).cpu().numpy()
     return [flat[store.caller_start[k]:store.caller_start[k + 1]] for k in range(len(pairs))]
 
 
@@ -339,8 +337,11 @@ class IrlsBuffers:
         else:
             raise ValueError(f"unknown precision {precision!r}")
 
+        # {L1 sum, Z, kept pairs} of the last pass, fused into the pass kernel
+        self.tot = torch.zeros(3, dtype=torch.float64, device=device)
+
     def out(self, k):
-        o = {"l1": self.l1, "n_active": self.n_active[k]}
+        o = {"l1": self.l1, "n_active": self.n_active[k], "totals": self.tot}
         if self.precision == "fp64":
             o["mom64"] = self.mom64
         else:
@@ -408,11 +409,10 @@ class IrlsEngine:
             prev = cur
             cur = 1 - cur
             self.point_pass(mode, th, cur, prev)
+            l1_sum, z, kept = self.buf.tot.cpu().numpy()
             if rnd > 0:
-                l1_history.append(float(self.buf.l1[:P].sum().item()) / Z)
-            counts = self.buf.n_active[cur][:P]
-            Z = int(counts.sum().item())
-            kept = int((counts > 0).sum().item())
+                l1_history.append(float(l1_sum) / Z)
+            Z, kept = int(z), int(kept)
             N.raise_flag(self.flag.item())
             dropped = P - kept
             if kept == 0:
@@ -442,8 +442,9 @@ class IrlsEngine:
         self.point_pass(N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED, 0.0, 1 - cur, cur)
         self.buf.n_active[cur], self.buf.n_active[1 - cur] = \
             self.buf.n_active[1 - cur], self.buf.n_active[cur]
+        l1_sum = float(self.buf.tot.cpu().numpy()[0])
         N.raise_flag(self.flag.item())
-        l1_history.append(float(self.buf.l1[:P].sum().item()) / Z)
+        l1_history.append(l1_sum / Z)
         self.dropped = dropped
         self.kept = kept
         return l1_history

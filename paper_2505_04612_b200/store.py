@@ -73,8 +73,10 @@ class PointPairStore:
     """SoA point-pair store on one device.
 
     ``order[k]`` is the caller index of the k-th stored pair; ``rank`` is its
-    inverse.  ``point_slot`` maps every caller point (pairs in caller order,
-    points in pair order) to its slot.
+    inverse.  The host computes only the O(pairs) layout; the O(points) work
+    -- scatter into 16-slot aligned pairs, fp64 -> fp32, sanitising, mask
+    packing -- is ``fm_store_build`` on the device, and the per-point maps
+    back to caller order are ``fm_store_gather_*`` (no host point_slot array).
     """
 
     def __init__(self, x1, x2, lengths, pair_i, pair_j, active=None, device=None,
@@ -111,70 +113,46 @@ class PointPairStore:
         self.n_slots = n_slots
         self.n_items = len(item_pair)
         self.n_points = int(lengths.sum())
-        # slot of every caller point
-        caller_start = np.zeros(P + 1, dtype=np.int64)
-        np.cumsum(lengths, out=caller_start[1:])
-        rank_of_point = np.repeat(self.rank, lengths)
-        within = np.arange(self.n_points, dtype=np.int64) - np.repeat(caller_start[:-1], lengths)
-        self.point_slot = pair_off[:-1][rank_of_point] + within
-        self.caller_start = caller_start
-
-        x1 = np.asarray(x1)
-        x2 = np.asarray(x2)
+        self.caller_start = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(lengths, out=self.caller_start[1:])
         self.sanitized = bool(sanitize)
-        if sanitize and len(x1):
-            bad = ~(np.isfinite(x1).all(axis=1) & np.isfinite(x2).all(axis=1))
-            if bad.any():
-                x1 = np.where(bad[:, None], 0.0, x1)
-                x2 = np.where(bad[:, None], 0.0, x2)
-                if x1.shape[1] == 3:
-                    x1[bad, 2] = 1.0
-                    x2[bad, 2] = 1.0
-                act = np.ones(len(x1), dtype=bool) if active is None else np.asarray(active, dtype=bool)
-                active = act & ~bad
         self.fp64 = bool(fp64)
-        self.x1d = self.x2d = None
-        if fp64:
-            d1 = np.zeros((n_slots, 3), dtype=np.float64)
-            d2 = np.zeros((n_slots, 3), dtype=np.float64)
-            d1[:, 2] = d2[:, 2] = 1.0
-            k = min(x1.shape[1], 3) if x1.ndim == 2 else 3
-            d1[self.point_slot, :k] = x1[:, :k]
-            d2[self.point_slot, :k] = x2[:, :k]
-            self.x1d = _dev(d1, device)
-            self.x2d = _dev(d2, device)
-            homog = False
-            self.x1 = self.x2 = self.x1z = self.x2z = None
-        else:
-            homog = x1.shape[1] == 3 and (not np.all(x1[:, 2] == 1.0) or not np.all(x2[:, 2] == 1.0))
+
+        x1 = np.asarray(x1, dtype=np.float64)
+        x2 = np.asarray(x2, dtype=np.float64)
+        dim = x1.shape[1] if x1.ndim == 2 and len(x1) else 2
+        homog = (not fp64 and dim == 3 and len(x1) > 0
+                 and not (np.all(x1[:, 2] == 1.0) and np.all(x2[:, 2] == 1.0)))
         self.homogeneous = bool(homog)
-        if not fp64:
-            self._fp32_columns(x1, x2, n_slots, homog, device)
-        bits = np.zeros(n_slots, dtype=bool)
-        bits[self.point_slot] = True if active is None else np.asarray(active, dtype=bool)
-        self.active = _dev(np.packbits(bits, bitorder="little").view(np.int32), device)
+        self.x1d = self.x2d = self.x1 = self.x2 = self.x1z = self.x2z = None
+        if fp64:
+            self.x1d = torch.empty((n_slots, 3), dtype=torch.float64, device=device)
+            self.x2d = torch.empty((n_slots, 3), dtype=torch.float64, device=device)
+        else:
+            self.x1 = torch.empty((n_slots, 2), dtype=torch.float32, device=device)
+            self.x2 = torch.empty((n_slots, 2), dtype=torch.float32, device=device)
+            if homog:
+                self.x1z = torch.empty(n_slots, dtype=torch.float32, device=device)
+                self.x2z = torch.empty(n_slots, dtype=torch.float32, device=device)
+        self.active = torch.empty(n_slots // 32, dtype=torch.int32, device=device)
         self.pair_off_d = _dev(pair_off, device)
         self.pair_len_d = _dev(_i32(s_len), device)
         self.pair_item_off_d = _dev(pair_item_off, device)
         self.item_pair_d = _dev(item_pair, device)
+        self.caller_start_d = _dev(self.caller_start, device)
+        self.rank_d = _dev(self.rank, device)
         self._struct = None
-
-    def _fp32_columns(self, x1, x2, n_slots, homog, device):
-        c1 = np.zeros((n_slots, 2), dtype=np.float32)
-        c2 = np.zeros((n_slots, 2), dtype=np.float32)
-        c1[self.point_slot] = x1[:, :2]
-        c2[self.point_slot] = x2[:, :2]
-        self.x1 = _dev(c1, device)
-        self.x2 = _dev(c2, device)
-        if homog:
-            z1 = np.zeros(n_slots, dtype=np.float32)
-            z2 = np.zeros(n_slots, dtype=np.float32)
-            z1[self.point_slot] = x1[:, 2]
-            z2[self.point_slot] = x2[:, 2]
-            self.x1z = _dev(z1, device)
-            self.x2z = _dev(z2, device)
-        else:
-            self.x1z = self.x2z = None
+        if self.n_points:
+            x1d = _dev(np.ascontiguousarray(x1), device)
+            x2d = _dev(np.ascontiguousarray(x2), device)
+            act = None if active is None else _dev(np.asarray(active, dtype=np.uint8), device)
+        else:  # pairs without points: nothing is read
+            x1d = x2d = torch.zeros((1, dim), dtype=torch.float64, device=device)
+            act = None
+        N.check(N.lib().fm_store_build(ctypes.byref(self.struct()), N.ptr(x1d), N.ptr(x2d), dim,
+                                       N.ptr(act), N.ptr(self.caller_start_d), N.ptr(self.rank_d),
+                                       int(sanitize), N.stream_handle()))
+        del x1d, x2d, act
 
     # ---------------------------------------------------------------- ctypes
     def struct(self):
@@ -195,8 +173,33 @@ class PointPairStore:
         return self._struct
 
     def scratch(self):
+        """Pass scratch (zeroed: fm_point_pass keeps its totals ticket there)."""
         nbytes = N.lib().fm_point_pass_scratch_bytes(ctypes.byref(self.struct()))
-        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+        return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+
+    # ----------------------------------------------- caller <-> slot order maps
+    def _caller_maps(self):
+        if getattr(self, "caller_start_d", None) is None:
+            self.caller_start_d = _dev(self.caller_start, self.device)
+            self.rank_d = _dev(self.rank, self.device)
+        return self.caller_start_d, self.rank_d
+
+    def gather_slots(self, slot_values):
+        """Per-slot fp64 values -> caller point order (device tensor [Z])."""
+        cs, rk = self._caller_maps()
+        out = torch.empty(max(self.n_points, 1), dtype=torch.float64, device=self.device)
+        N.check(N.lib().fm_store_gather_slots(ctypes.byref(self.struct()), N.ptr(cs), N.ptr(rk),
+                                              N.ptr(slot_values), N.ptr(out), N.stream_handle()))
+        return out[:self.n_points]
+
+    def scatter_slots(self, caller_values):
+        """Caller-ordered fp64 values [Z] -> a per-slot device tensor (0 on padding)."""
+        cs, rk = self._caller_maps()
+        src = torch.as_tensor(np.ascontiguousarray(caller_values, dtype=np.float64), device=self.device)
+        out = torch.zeros(self.n_slots, dtype=torch.float64, device=self.device)
+        N.check(N.lib().fm_store_scatter_slots(ctypes.byref(self.struct()), N.ptr(cs), N.ptr(rk),
+                                               N.ptr(src), N.ptr(out), N.stream_handle()))
+        return out
 
     # ------------------------------------------------------------- masks
     def active_bits(self):
@@ -207,7 +210,11 @@ class PointPairStore:
 
     def caller_masks(self):
         """Active mask of every caller point, host bool array (caller order)."""
-        return self.active_bits()[self.slots_device].cpu().numpy()
+        cs, rk = self._caller_maps()
+        out = torch.empty(max(self.n_points, 1), dtype=torch.uint8, device=self.device)
+        N.check(N.lib().fm_store_gather_mask(ctypes.byref(self.struct()), N.ptr(cs), N.ptr(rk),
+                                             N.ptr(out), N.stream_handle()))
+        return out[:self.n_points].cpu().numpy().astype(bool)
 
     def write_back(self, pairs):
         """In-place update of each pair's ``active`` array (ref/epipolar.py:283)."""
@@ -249,40 +256,34 @@ class PointPairStore:
         slot = off_d[seg] + (torch.arange(self.n_points, device=device) - start_d[seg])
         del seg
         self.point_slot_d = slot
-        self.point_slot = None
         self.x1 = torch.zeros((n_slots, 2), dtype=torch.float32, device=device)
         self.x2 = torch.zeros((n_slots, 2), dtype=torch.float32, device=device)
         self.x1[slot] = x1.to(torch.float32)
         self.x2[slot] = x2.to(torch.float32)
-        self.x1z = self.x2z = None
+        self.x1z = self.x2z = self.x1d = self.x2d = None
         self.homogeneous = False
+        self.fp64 = False
         self.sanitized = True  # device-generated coordinates are finite
-        bits = torch.zeros(n_slots, dtype=torch.int64, device=device)
-        bits[slot] = 1
-        w = (bits.view(-1, 32) << torch.arange(32, device=device, dtype=torch.int64)).sum(1)
-        self.active = torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
-        del bits, w
+        self.active = torch.zeros(n_slots // 32, dtype=torch.int32, device=device)
         self.pair_off_d = _dev(pair_off, device)
         self.pair_len_d = _dev(_i32(lengths), device)
         self.pair_item_off_d = _dev(pair_item_off, device)
         self.item_pair_d = _dev(item_pair, device)
+        self.caller_start_d = None
         self._struct = None
+        self.reset_active()
         return self
 
     def reset_active(self):
         """Mark every real point active again (benchmark repetitions)."""
-        slot = self.point_slot_d if self.point_slot is None else \
-            torch.from_numpy(self.point_slot).to(self.device)
+        slot = getattr(self, "point_slot_d", None)
+        if slot is None:
+            slot = self.gather_slots(torch.arange(self.n_slots, device=self.device,
+                                                  dtype=torch.float64)).long()
         bits = torch.zeros(self.n_slots, dtype=torch.int64, device=self.device)
         bits[slot] = 1
         w = (bits.view(-1, 32) << torch.arange(32, device=self.device, dtype=torch.int64)).sum(1)
         self.active.copy_(torch.where(w >= 2**31, w - 2**32, w).to(torch.int32))
-
-    @property
-    def slots_device(self):
-        if self.point_slot is None:
-            return self.point_slot_d
-        return torch.from_numpy(self.point_slot).to(self.device)
 
     @classmethod
     def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False, sanitize=False,
