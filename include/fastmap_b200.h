@@ -212,7 +212,7 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold,
  * (ref/epipolar.py:167-168, not remapped).  Incidence lists make the per-image
  * and per-camera gradient reductions deterministic gathers (no float atomics):
  * entries are (pair << 1) | side, side 0 = the image/camera is the pair's i.
- * Camera lists are cut into chunks of <= 4096 incidences: chunk k covers
+ * Camera lists are cut into chunks of <= 1024 incidences (store.CAM_CHUNK): chunk k covers
  * cam_inc[cam_chunk_lo[k] .. cam_chunk_lo[k+1]) and belongs to camera
  * cam_chunk_cam[k]; camera c owns chunks [cam_chunk_off[c], cam_chunk_off[c+1]).
  */

@@ -359,9 +359,12 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
   const int64_t P = g.n_pairs;
   if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
     const int c = blockIdx.x - img_blocks;
-    if (ADAM && *flag) return;
+    // a raised flag skips the work but never the ticket: every chunk block
+    // counts, so the last one always re-arms it (the flag can be raised by
+    // image blocks of this same launch)
+    const bool skip = ADAM && *flag;
     double acc = 0;
-    const int lo = g.cam_chunk_lo[c], hi = g.cam_chunk_lo[c + 1];
+    const int lo = g.cam_chunk_lo[c], hi = skip ? lo : g.cam_chunk_lo[c + 1];
     // unrolled: the two dependent loads of several incidences in flight
     // together (same per-thread accumulation order)
 #pragma unroll 8
@@ -383,7 +386,7 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     __syncthreads();
     if (!last) return;
     __threadfence();
-    cam_finalise<ADAM>(g, params, R, cpart, grad, ad, flag);
+    if (!(ADAM && *(volatile int32_t*)flag)) cam_finalise<ADAM>(g, params, R, cpart, grad, ad, flag);
     if (threadIdx.x == 0) *ticket = 0u;  // ready for the next step
     return;
   }
