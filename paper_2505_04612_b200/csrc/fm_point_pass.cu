@@ -75,10 +75,8 @@ struct TotSlot {
   unsigned flags;  // 1: NaN L1, 2: +inf L1
   unsigned pad;
 };
-struct StreamCtl {  // zero-initialised scratch, re-armed after every launch
+struct TotCtl {  // zero-initialised scratch, re-armed after every launch
   TotSlot slot[kTotSlots];
-  unsigned work;  // stream kernel: dynamic group counter
-  unsigned pad[3];
 };
 
 struct PartialBufs {
@@ -88,15 +86,14 @@ struct PartialBufs {
   int64_t cap; // items the buffers hold
   double* tot_part;  // per-block partials of fm_pass_totals (generic / chunked passes)
   double* totals;
-  StreamCtl* ctl;  // fused totals of the one-shot hot kernel (exact integer sums)
+  TotCtl* ctl;  // fused totals of the one-shot hot kernel (exact integer sums)
 };
-struct StreamBufs;
 
 // Converts the exact sums of the launch before it into `totals` and re-arms
 // the control words.  Launched right after the pass as a programmatic
 // dependent launch: it is scheduled while the pass drains and waits for the
 // pass's completion and memory flush in griddepcontrol.wait.
-__global__ void totals_finalize_kernel(StreamCtl* c, double* totals) {
+__global__ void totals_finalize_kernel(TotCtl* c, double* totals) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   static_assert(kTotSlots == 64, "two slots per lane");
   const int lane = threadIdx.x;
@@ -119,7 +116,6 @@ __global__ void totals_finalize_kernel(StreamCtl* c, double* totals) {
     fl |= __shfl_xor_sync(0xffffffffu, fl, off);
   }
   if (lane != 0) return;
-  c->work = 0u;
   if (totals) {
     double l1 = (double)v[0] + ldexp((double)v[1], -32) + ldexp((double)v[2], -64);
     if (fl & 1u) l1 = __longlong_as_double(0x7ff8000000000000ll);
@@ -130,7 +126,7 @@ __global__ void totals_finalize_kernel(StreamCtl* c, double* totals) {
   }
 }
 
-int launch_totals_finalize(StreamCtl* c, double* totals, cudaStream_t st) {
+int launch_totals_finalize(TotCtl* c, double* totals, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);
   cfg.blockDim = dim3(32);
@@ -145,10 +141,13 @@ int launch_totals_finalize(StreamCtl* c, double* totals, cudaStream_t st) {
   return FM_OK;
 }
 
-// Exact, order-independent pass totals (see the stream kernel): a warp adds
-// its items' {L1, Z, kept} with fire-and-forget integer reductions; L1 is cut
-// into an integer part and two 32-bit fraction words (exact for the double).
-__device__ __forceinline__ void totals_add(StreamCtl* ctl, unsigned wid, double l1, double z,
+// Exact, order-independent pass totals: a warp adds its items' {L1, Z, kept}
+// with fire-and-forget integer reductions (no fence, no ticket: a block-exit
+// fence + atomic ticket cost ~3 us at C2 by delaying every block's
+// retirement); L1 is cut into an integer part and two 32-bit fraction words,
+// exact for the double, so the sum does not depend on the order the warps
+// finish in and the pass stays bitwise reproducible.
+__device__ __forceinline__ void totals_add(TotCtl* ctl, unsigned wid, double l1, double z,
                                            double kept) {
   TotSlot* c = &ctl->slot[wid % kTotSlots];
   if (isfinite(l1)) {
@@ -742,335 +741,6 @@ point_pass_hot_mixed(const fm_point_store s, const double* __restrict__ ghat, co
                               ((int64_t)blockIdx.x - nb1) * kGrpWarps + (threadIdx.x >> 5), n1, s.n_items);
 }
 
-// SM-pool form (one item per pair): one block of kSmWarps warps per SM owns a
-// contiguous range of pairs (equal pair counts); its warps take item groups
-// of that range from a shared-memory counter, one at a time, so the warps the
-// scheduler favours simply take more groups and the SM's warps finish within
-// about one group of each other -- one wave, no block retirement, and the
-// whole SM's warps share one pool.
-constexpr int kSmWarps = 16;
-template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kSmWarps * 32, 1)
-point_pass_sm(const fm_point_store s, const double* __restrict__ ghat, const double thr,
-              const int32_t* __restrict__ prev_active, const fm_pass_out out, const PartialBufs part) {
-  constexpr int IPW = 32 / L;
-  __shared__ int next_group;
-  const int64_t P = s.n_items;
-  const int64_t lo = P * blockIdx.x / gridDim.x;
-  const int64_t hi = P * (blockIdx.x + 1) / gridDim.x;
-  const int ng = (int)((hi - lo + IPW - 1) / IPW);
-  const int wib = threadIdx.x >> 5;
-  if (threadIdx.x == 0) next_group = kSmWarps;
-  __syncthreads();
-  int grp = wib;
-  while (grp < ng) {
-    hot_body<MODE, MOM64, L>(s, ghat, thr, prev_active, out, part, grp, lo, hi);
-    int nxt = 0;
-    if ((threadIdx.x & 31) == 0) nxt = atomicAdd(&next_group, 1);
-    grp = __shfl_sync(0xffffffffu, nxt, 0);
-  }
-}
-
-// ------------------------------------------------------------- stream kernel
-// Persistent form of the hot kernel for stores with one work item per pair
-// (n_items == n_pairs, the irls_refine case): one wave of blocks, every warp a
-// worker that walks a sequence of item groups (IPW = 32/L consecutive pairs)
-// through ONE continuous cp.async ring.  The fetch cursor runs kSRing-1
-// iterations ahead of the compute cursor across group boundaries, so a new
-// group's first copies are already in flight while the previous group's
-// epilogue (transpose-reduce + row-coalesced stores) runs; a group's
-// descriptors and its warp-queue record (first slot, blocks per lane, ghat
-// copied into shared memory by cp.async with its first iteration) are
-// prepared when the fetch cursor enters it.  Work: groups wid and
-// wid + nwarps statically, then dynamically from a device counter (a fetched
-// group's id is grabbed one group ahead, its descriptor loaded one group
-// ahead), so the warps that the scheduler favours take more groups and the
-// launch ends within about one group.  Every group has at least one
-// iteration (an all-skipped group gets one empty one), which bounds the
-// groups in flight by the ring depth and keeps wait_group<kSRing-1> exact.
-//
-// Totals {L1, Z, kept}: every group adds its item-order sums into exact
-// integer accumulators (L1 as fixed point: integer part + two 32-bit fraction
-// words, each group's value cut exactly, so the sum does not depend on the
-// order the groups finish in) with fire-and-forget reductions -- no fences in
-// the loop, which would wait for the ring's copies in flight.  The last warp
-// to exit converts them and re-arms the accumulators; non-finite L1 is kept as
-// a flag (NaN / +inf, as the fp64 sum would give).
-#ifndef FM_STREAM_RING
-#define FM_STREAM_RING 4
-#endif
-constexpr int kSRing = FM_STREAM_RING;  // ring stages per lane
-constexpr int kSQ = kSRing + 1;         // group records (>= groups in flight + 1)
-
-struct StreamBufs {
-  StreamCtl* ctl;
-  double* totals;  // [3] or NULL (no totals)
-};
-
-template <int L>
-struct StreamWarpSmem {
-  float4 c[kSRing][4][32];     // ring: chunk rows (see LaneRing)
-  uint32_t m[kSRing][32];      // ring: mask words
-  uint32_t q_lo[kSQ][32];      // group record: lane's item first slot / 16
-  int32_t q_nb[kSQ][32];       //               lane's 16-slot blocks (0: none)
-  int32_t q_grp[kSQ + 1];      //               group id
-  double G[kSQ][32 / L][9];    //               ghat per item
-  float stage[48 * (32 / L)];  // epilogue staging (row-coalesced stores)
-  double stage_l1[32 / L];
-};
-
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-
-template <unsigned MODE, bool MOM64, int L>
-__global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
-point_pass_stream(const fm_point_store s, const double* __restrict__ ghat, const double thr,
-                  const int32_t* __restrict__ prev_active, const fm_pass_out out,
-                  const StreamBufs sb) {
-  constexpr bool kPrune = MODE & FM_PASS_PRUNE;
-  constexpr bool kL1 = MODE & FM_PASS_L1;
-  constexpr bool kMom = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
-  constexpr bool kLin = kMom && !MOM64;
-  constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
-  constexpr int IPW = 32 / L;
-  constexpr int S = L / 4;
-  static_assert(L == 4 || L == 8 || L == 16, "L in {4, 8, 16}");
-  constexpr unsigned kFull = 0xffffffffu;
-
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  StreamWarpSmem<L>& sm = reinterpret_cast<StreamWarpSmem<L>*>(smem_raw)[wib];
-  const int64_t P = s.n_pairs;  // == n_items
-  const int NG = (int)((P + IPW - 1) / IPW);
-  const int nwarps = (int)gridDim.x * kGrpWarps;
-  const int wid = (int)blockIdx.x * kGrpWarps + wib;
-  const int g = lane % L, sg = g >> 2, h = g & 3, li = lane / L;
-  const int4* desc = reinterpret_cast<const int4*>(s.item_desc);
-  const int64_t dx2 = s.x2 - s.x1;  // x2 column relative to x1 (floats)
-
-#pragma unroll
-  for (int st = 0; st < kSRing; ++st)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sm.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();
-
-  constexpr uint32_t kChunkB = 32 * 16;
-  constexpr uint32_t kStageC = 4 * kChunkB;
-  constexpr uint32_t kStageM = 32 * 4;
-  const uint32_t ring_c = smem_u32(&sm.c[0][0][lane]);
-  const uint32_t ring_m = smem_u32(&sm.m[0][lane]);
-
-  // ------------------------------------------------------------ fetch cursor
-  int f_it = 0, f_nit = 0, f_nb = 0, f_half0 = 0;
-  const float* f_x1 = s.x1;
-  const uint32_t* f_mw = s.active;
-  bool f_done = false;
-  int pushed = 0;
-  // the next group (descriptor prefetched) and, on lane 0, the one after it
-  int nf_grp = wid;
-  int4 nf_desc = make_int4(0, 0, 0, 0);
-  int nf_prev = 0;
-  int pending = wid + nwarps;
-  auto prefetch = [&](int grp) {
-    const int64_t item = (int64_t)grp * IPW + li;
-    nf_desc = make_int4(0, 0, 0, 0);
-    nf_prev = 0;
-    if (grp < NG && item < P) {
-      nf_desc = __ldg(desc + item);
-      nf_prev = kSkip ? __ldg(prev_active + item) : 1;
-    }
-  };
-  prefetch(nf_grp);
-
-  auto fetch_enter = [&]() {
-    const int grp = nf_grp;
-    if (grp >= NG) {
-      f_done = true;
-      return;
-    }
-    const int4 dq = nf_desc;
-    const bool has = nf_prev != 0;  // an item, not dropped earlier
-    nf_grp = __shfl_sync(kFull, pending, 0);
-    prefetch(nf_grp);
-    if (lane == 0) pending = nf_grp < NG ? 2 * nwarps + (int)atomicAdd(&sb.ctl->work, 1u) : NG;
-    const ItemDesc d = decode_item(dq);
-    f_nb = has ? (d.len + kBlkSlots - 1) / kBlkSlots : 0;
-    f_nit = max(1, (int)__reduce_max_sync(kFull, (unsigned)((f_nb + S - 1) / S)));
-    f_it = 0;
-    f_x1 = s.x1 + 2 * d.lo;
-    f_half0 = (int)(d.lo & 16) + kBlkSlots * sg;
-    f_mw = s.active + (d.lo >> 5);
-    const int slot = pushed % kSQ;
-    sm.q_lo[slot][lane] = (uint32_t)(d.lo >> 4);
-    sm.q_nb[slot][lane] = f_nb;
-    if (lane == 0) sm.q_grp[slot] = grp;
-    const int64_t item = (int64_t)grp * IPW + li;
-    for (int k = g; k < 9; k += L) {
-      double* dst = &sm.G[slot][li][k];
-      if (has) cp_async8(smem_u32(dst), ghat + (int64_t)k * P + item);
-      else *dst = 0.0;
-    }
-    ++pushed;
-  };
-  auto fetch_issue = [&](uint32_t st) {
-    if (!f_done && f_it == f_nit) fetch_enter();
-    if (!f_done) {
-      if (S * f_it + sg < f_nb) {
-        const float4* p1 = reinterpret_cast<const float4*>(f_x1) + 8 * (S * f_it + sg) + h;
-        const float4* p2 = reinterpret_cast<const float4*>(f_x1 + dx2) + 8 * (S * f_it + sg) + h;
-        cp_async16(ring_c + st * kStageC, p1);
-        cp_async16(ring_c + st * kStageC + kChunkB, p1 + 4);
-        cp_async16(ring_c + st * kStageC + 2 * kChunkB, p2);
-        cp_async16(ring_c + st * kStageC + 3 * kChunkB, p2 + 4);
-        cp_async4(ring_m + st * kStageM, f_mw + ((f_half0 + kBlkSlots * S * f_it) >> 5));
-      }
-      ++f_it;
-    }
-    cp_async_commit();
-  };
-
-  // ---------------------------------------------------------- compute cursor
-  int c_it = 0, c_nit = 0, c_nb = 0, c_half0 = 0, c_grp = 0, c_slot = 0, popped = 0;
-  uint32_t* c_mw = s.active;
-  double G[9];
-  HotAcc<kPrune, kL1, kMom, MOM64> acc;
-  acc.zero();
-#pragma unroll
-  for (int k = 0; k < 9; ++k) G[k] = 0.0;
-
-#pragma unroll
-  for (int t = 0; t < kSRing - 1; ++t) fetch_issue(t);
-  uint32_t st_issue = kSRing - 1, st_read = 0;
-
-  while (true) {
-    fetch_issue(st_issue);
-    st_issue = st_issue + 1 == kSRing ? 0 : st_issue + 1;
-    cp_async_wait<kSRing - 1>();
-    if (c_it == 0) {
-      if (popped == pushed) break;
-      __syncwarp();  // the group record and its ghat copies (other lanes) are visible
-      c_grp = sm.q_grp[c_slot];
-      const int64_t lo = (int64_t)sm.q_lo[c_slot][lane] << 4;
-      c_nb = sm.q_nb[c_slot][lane];
-      c_nit = max(1, (int)__reduce_max_sync(kFull, (unsigned)((c_nb + S - 1) / S)));
-#pragma unroll
-      for (int k = 0; k < 9; ++k) G[k] = sm.G[c_slot][li][k];
-      c_half0 = (int)(lo & 16) + kBlkSlots * sg;
-      c_mw = s.active + (lo >> 5);
-      acc.zero();
-    }
-    {
-      const int pos = c_half0 + kBlkSlots * S * c_it;
-      const uint32_t blk = (S * c_it + sg < c_nb) ? lds32(ring_m + st_read * kStageM) >> (pos & 31) : 0u;
-      const uint32_t bh = blk >> (2 * h);
-      uint32_t kept = 0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float4 x1 = lds128(ring_c + st_read * kStageC + j * kChunkB);
-        const float4 x2 = lds128(ring_c + st_read * kStageC + (2 + j) * kChunkB);
-        kept |= (uint32_t)acc.point(G, x1.x, x1.y, x2.x, x2.y, (bh >> (8 * j)) & 1u, thr) << (8 * j);
-        kept |= (uint32_t)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bh >> (8 * j + 1)) & 1u, thr) << (8 * j + 1);
-      }
-      acc.cnt += __popc(kept);
-      const uint32_t cleared = kPrune ? ((bh & 0x303u) & ~kept) << (2 * h) : 0u;
-      if (kPrune && cleared) atomicAnd(c_mw + (pos >> 5), ~(cleared << (pos & 31)));
-      st_read = st_read + 1 == kSRing ? 0 : st_read + 1;
-    }
-    if (++c_it < c_nit) continue;
-
-    // ---------------------------------------------------- group epilogue
-    c_it = 0;
-    ++popped;
-    c_slot = c_slot + 1 == kSQ ? 0 : c_slot + 1;
-    const int64_t n0 = (int64_t)c_grp * IPW;
-    if (kL1 && kMom && !MOM64) acc.l1 = acc.l1f;
-    const double il1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
-    double icnt;
-    if (kMom && MOM64) {
-      constexpr int N = L <= 8 ? 40 : 48;
-      double v[N];
-#pragma unroll
-      for (int k = 0; k < 36; ++k) v[k] = acc.M64[MOM64 ? k : 0];
-      v[36] = (double)acc.cnt;
-      v[37] = 0.0;
-#pragma unroll
-      for (int k = 38; k < N; ++k) v[k] = 0.0;
-      group_transpose_reduce<L>(v, lane);
-      icnt = group_sum<L>((double)acc.cnt);
-      double* stage = reinterpret_cast<double*>(sm.stage);  // 38 x IPW doubles: fits in
-      // the float staging area + the (idle at this point) ring chunk row of this lane
-      (void)stage;
-#pragma unroll
-      for (int i = 0; i < N / L; ++i) {
-        const int k = g * (N / L) + i;
-        const int64_t n = n0 + li;
-        if (n >= P) continue;
-        if (k < 36) out.mom64[(int64_t)k * P + n] = v[i];
-        else if (k == 36 && out.n_active) out.n_active[n] = (int32_t)v[i];
-      }
-      if (kL1 && out.l1 && g == 0 && n0 + li < P) out.l1[n0 + li] = il1;
-    } else if (kMom) {
-      constexpr int N = 48;
-      float v[N];
-#pragma unroll
-      for (int k = 0; k < 18; ++k) {
-        v[2 * k] = acc.Mp[MOM64 ? 0 : k].x;
-        v[2 * k + 1] = acc.Mp[MOM64 ? 0 : k].y;
-      }
-      v[36] = acc.V0.x; v[37] = acc.V0.y; v[38] = acc.V3.x;
-      v[39] = acc.V1.x; v[40] = acc.V1.y; v[41] = acc.V3.y;
-      v[42] = acc.V2.x; v[43] = acc.V2.y; v[44] = acc.v22;
-      v[45] = (float)acc.cnt;
-      v[46] = acc.s0f;
-      v[47] = 0.f;
-      group_transpose_reduce<L>(v, lane);
-      icnt = group_sum<L>((double)acc.cnt);
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < N / L; ++i) sm.stage[(g * (N / L) + i) * IPW + li] = v[i];
-      if (g == 0) sm.stage_l1[li] = il1;
-      __syncwarp();
-#pragma unroll 1
-      for (int t = lane; t < 47 * IPW; t += 32) {
-        const int vi = t / IPW;
-        const int64_t n = n0 + (t % IPW);
-        if (n >= P) continue;
-        const float val = sm.stage[t];
-        if (vi < 36) out.mom32[(int64_t)hot_mom_index(vi) * P + n] = val;
-        else if (vi < 45) { if (kLin) out.vgrad[(int64_t)(vi - 36) * P + n] = val; }
-        else if (vi == 45) { if (out.n_active) out.n_active[n] = (int32_t)val; }
-        else out.s0[n] = (double)val;
-      }
-      if (kL1 && out.l1 && lane < IPW && n0 + lane < P) out.l1[n0 + lane] = sm.stage_l1[lane];
-    } else {
-      icnt = group_sum<L>((double)acc.cnt);
-      if (g == 0 && n0 + li < P) {
-        if (out.n_active) out.n_active[n0 + li] = (int32_t)icnt;
-        if (kL1 && out.l1) out.l1[n0 + li] = il1;
-      }
-    }
-    if (sb.totals) {
-      double w3[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int q = 0; q < IPW; ++q) {
-        const double a = __shfl_sync(kFull, il1, q * L);
-        const double c = __shfl_sync(kFull, icnt, q * L);
-        if (n0 + q < P) {
-          w3[0] += a;
-          w3[1] += c;
-          w3[2] += c > 0.0 ? 1.0 : 0.0;
-        }
-      }
-      if (lane == 0) totals_add(sb.ctl, (unsigned)wid, w3[0], w3[1], w3[2]);
-    }
-    acc.zero();
-  }
-  cp_async_wait<0>();
-  // totals_finalize_kernel (launched after the pass) re-arms the counter
-}
-
 // -------------------------------------------------------------- generic kernel
 // API modes: optional z columns, fp64 moments, caller-given residual weights,
 // residual output, mask-free sweeps.  Plain scalar code; not on the hot loop.
@@ -1329,57 +999,6 @@ int launch_hot_mixed(const fm_point_store& s, double thr, const double* ghat,
   return FM_OK;
 }
 
-template <unsigned MODE, bool MOM64, int L>
-int launch_sm(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
-              const fm_pass_out& out, const PartialBufs& part, cudaStream_t stream) {
-  const size_t smem = kSmWarps * sizeof(LaneRing);
-  static bool attr = false;
-  if (!attr) {
-    FM_CUDA(cudaFuncSetAttribute(point_pass_sm<MODE, MOM64, L>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  const int64_t groups = ceil_div(s.n_items, 32 / L);
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(groups, kSmWarps)));
-  point_pass_sm<MODE, MOM64, L><<<(unsigned)blocks, kSmWarps * 32, smem, stream>>>(
-      s, ghat, thr, prev_active, out, part);
-  FM_LAUNCHED(point_pass_sm);
-  return FM_OK;
-}
-
-template <unsigned MODE, bool MOM64, int L>
-int launch_stream(const fm_point_store& s, double thr, const double* ghat, const int32_t* prev_active,
-                  const fm_pass_out& out, const StreamBufs& sb, cudaStream_t stream) {
-  const size_t smem = kGrpWarps * sizeof(StreamWarpSmem<L>);
-  static int bps = 0;
-  if (!bps) {
-    FM_CUDA(cudaFuncSetAttribute(point_pass_stream<MODE, MOM64, L>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int b = 0;
-    FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, point_pass_stream<MODE, MOM64, L>,
-                                                          kGrpWarps * 32, smem));
-    bps = b > 0 ? b : 1;
-  }
-  const int64_t NG = ceil_div(s.n_pairs, 32 / L);
-  const int64_t blocks = std::min<int64_t>((int64_t)bps * sm_count(), ceil_div(NG, kGrpWarps));
-  point_pass_stream<MODE, MOM64, L><<<(unsigned)blocks, kGrpWarps * 32, smem, stream>>>(
-      s, ghat, thr, prev_active, out, sb);
-  FM_LAUNCHED(point_pass_stream);
-  return FM_OK;
-}
-
-// Stream kernel width: L = 8 by default (FM_STREAM_L overrides; tuning).
-template <unsigned MODE, bool MOM64>
-int launch_stream_pick(const fm_point_store& s, double thr, const double* ghat,
-                       const int32_t* prev_active, const fm_pass_out& out, const StreamBufs& sb,
-                       cudaStream_t stream) {
-  int L = 8;
-  if (const char* env = getenv("FM_STREAM_L")) L = atoi(env);
-  if (L == 16) return launch_stream<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, sb, stream);
-  if (L == 4) return launch_stream<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, sb, stream);
-  return launch_stream<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, sb, stream);
-}
-
 // Lanes per item L in {4, 8, 16}: blocks are one-shot, so the last wave of
 // a launch is partially filled.  Score each L by the filled fraction of its
 // waves and a per-item reduction cost (log2(L) transpose-reduce levels plus a
@@ -1410,16 +1029,6 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     if (score > best * 1.02) {
       best = score;
       pick = L;
-    }
-  }
-  if (s.n_items == s.n_pairs) {
-    const char* env_sm = getenv("FM_SM");
-    if (env_sm && atoi(env_sm) != 0) {
-      const char* el = getenv("FM_SM_L");
-      const int sl = el ? atoi(el) : 8;
-      if (sl == 4) return launch_sm<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);
-      if (sl == 16) return launch_sm<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream);
-      return launch_sm<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream);
     }
   }
   // Whole waves of L = 4 items, the rest of the launch at L = 16 (see
@@ -1497,21 +1106,8 @@ int dispatch_generic(unsigned mode, const fm_point_store& s, double thr, const d
 
 int dispatch_hot(unsigned mode, bool f64, const fm_point_store& s, double thr, const double* ghat,
                  const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
-                 const StreamBufs* sb, cudaStream_t stream, bool* handled) {
+                 cudaStream_t stream, bool* handled) {
   *handled = true;
-  if (sb) {
-    if (f64) {
-#define FM_CASE(M) \
-  if (mode == (M)) return launch_stream_pick<(M), true>(s, thr, ghat, prev_active, out, *sb, stream);
-      FM_HOT_MODES(FM_CASE)
-#undef FM_CASE
-    } else {
-#define FM_CASE(M) \
-  if (mode == (M)) return launch_stream_pick<(M), false>(s, thr, ghat, prev_active, out, *sb, stream);
-      FM_HOT_MODES(FM_CASE)
-#undef FM_CASE
-    }
-  }
   if (f64) {
 #define FM_CASE(M) \
   if (mode == (M)) return launch_hot<(M), true>(s, thr, ghat, prev_active, out, part, stream);
@@ -1545,7 +1141,7 @@ int fm_debug_hot_trace(void* host_out) {
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store) {
   if (!store) return 0;
   const size_t ni = (size_t)store->n_items;
-  return scratch_round(sizeof(unsigned)) + scratch_round(sizeof(StreamCtl)) +
+  return scratch_round(sizeof(unsigned)) + scratch_round(sizeof(TotCtl)) +
          scratch_round(ni * kNumRed * sizeof(double)) +
          2 * scratch_round(ni * sizeof(double)) + scratch_round(ni * 4 * sizeof(int32_t)) +
          scratch_round((3 * ni + 192) * sizeof(double)) + 256;
@@ -1598,13 +1194,11 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
   size_t tot_bytes = 0;
   {
     Scratch sc(scratch, scratch_bytes);
-    // at fixed offsets always: a reserved word, then the fused-totals / stream
-    // control words, zero when the scratch is first used (the header asks for
-    // zeroed scratch) and re-armed by every launch that uses them
+    // at fixed offsets always: a reserved word, then the fused-totals
+    // accumulators -- zero when the scratch is first used (the header asks
+    // for zeroed scratch), re-armed by totals_finalize_kernel after each use
     sc.take<unsigned>(1);
-    // stream-kernel control words, also at fixed offsets (zeroed once, re-armed
-    // by every launch)
-    StreamCtl* sctl = sc.take<StreamCtl>(1);
+    TotCtl* sctl = sc.take<TotCtl>(1);
     if (out->totals) {
       tot_bytes = (3 * (size_t)s.n_items + 192) * sizeof(double);
       tot_part = sc.take<double>(3 * (size_t)s.n_items + 192);
@@ -1626,21 +1220,6 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     FM_REQUIRE((sc.used == 0 || scratch) && sc.ok(), "point-pass scratch too small (%zu < %zu)",
                scratch_bytes, sc.used);
   }
-  // the persistent stream kernel: one item per pair (FM_STREAM=1 selects it; measured
-  // slower than the one-shot launch at C2 and C4)
-  StreamBufs sbuf{nullptr, nullptr};
-  const StreamBufs* sbp = nullptr;
-  {
-    const char* env = getenv("FM_STREAM");
-    if (s.n_items == s.n_pairs && scratch && env && atoi(env) != 0 &&
-        (size_t)s.n_slots / 16 < ((size_t)1 << 32)) {
-      Scratch sc(scratch, scratch_bytes);
-      sc.take<unsigned>(1);
-      sbuf.ctl = sc.take<StreamCtl>(1);
-      sbuf.totals = out->totals;
-      sbp = &sbuf;
-    }
-  }
   int rc = FM_OK;
   bool fused = false;  // totals computed inside the hot kernel
   bool handled = false;
@@ -1651,8 +1230,8 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
     // fp64 moments are the exact default; fp32 (FFMA2 + shifted model) only for IRLS moments
     const bool hot_f64 = f64 || !(m & FM_PASS_MOMENTS);
     if (hot_f64 || (m & FM_PASS_IRLS)) {
-      rc = dispatch_hot(m, hot_f64, s2, threshold, ghat, prev_active, *out, part, sbp, st, &handled);
-      fused = handled && (sbp ? sbp->totals != nullptr : part.ctl != nullptr);
+      rc = dispatch_hot(m, hot_f64, s2, threshold, ghat, prev_active, *out, part, st, &handled);
+      fused = handled && part.ctl != nullptr;
     }
   }
   if (!handled) {
@@ -1665,13 +1244,11 @@ int fm_point_pass(const fm_point_store* store, unsigned mode, double threshold, 
       rc = f64 ? dispatch_generic<kXY32, true>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st)
                : dispatch_generic<kXY32, false>(m, s, threshold, ghat, res_in, prev_active, *out, gp, st);
   }
-  if (!rc && sbp) return launch_totals_finalize(sbp->ctl, out->totals, st);
-  if (!rc && fused && part.ctl) {
-    if (getenv("FM_HOT_NOTOT") && atoi(getenv("FM_HOT_NOTOT")) == 3) return rc;  // tuning: no finalize
-    return launch_totals_finalize(part.ctl, out->totals, st);
-  }
+  if (!rc && fused && part.ctl) return launch_totals_finalize(part.ctl, out->totals, st);
   if (rc || !out->totals || fused) return rc;
-  if (getenv("FM_HOT_NOTOT") && atoi(getenv("FM_HOT_NOTOT")) == 2) return rc;  // tuning: no totals at all
+  // tuning knob FM_HOT_NOTOT: 1 = totals by the separate fm_pass_totals
+  // kernel, 2 = no totals at all (the pass alone)
+  if (getenv("FM_HOT_NOTOT") && atoi(getenv("FM_HOT_NOTOT")) == 2) return rc;
   // generic kernels / pairs split over several items: a separate reduction
   FM_REQUIRE(out->n_active, "totals need out->n_active");
   return fm_pass_totals((m & FM_PASS_L1) ? out->l1 : nullptr, out->n_active, s.n_pairs, out->totals,

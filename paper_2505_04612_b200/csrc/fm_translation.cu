@@ -185,11 +185,6 @@ __device__ __forceinline__ double norm3(const double d[3]) {
 // np.maximum(x, 1e-8): NaN propagates
 __device__ __forceinline__ double clamp_len(double x) { return x < 1e-8 ? 1e-8 : x; }
 
-// np.sign: -1, 0, +1, NaN for NaN
-__device__ __forceinline__ double np_sign(double x) {
-  return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
-}
-
 // a / b correctly rounded (bitwise __ddiv_rn) from y = RN(1/b), for the six
 // divisions by the same edge length: q0 = RN(a y) is within 1.5 ulp, one
 // FMA-residual correction brings it within 1 ulp, and the second is exact
