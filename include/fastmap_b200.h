@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 3
+#define FM_ABI_VERSION 4
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -280,6 +280,23 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q,
                       int32_t use_graph, void* scratch, size_t scratch_bytes,
                       void* stream);
 
+/*
+ * Sharded form of fm_epi_adam_steps: `g` / `q` hold this rank's
+ * contiguous range of image pairs (global image / camera indexing); per step
+ * the local packed gradient and loss go to grad_buf [9N + C + 1], one
+ * ncclAllReduce(sum) over `nccl_comm` (an ncclComm_t from fm_nccl_comm_init;
+ * NULL = one rank) and the replicated Adam step (ref/optim.py:24-36) with
+ * the loss check of ref/epipolar.py:306-307.  Every rank passes the same
+ * params / adam_m / adam_v values and ends with the same results.  With
+ * use_graph the chunk, collective included, is one cached CUDA graph.
+ */
+int fm_epi_adam_steps_nccl(const fm_pair_graph* g, const fm_quad_model* q,
+                           double* params, double* adam_m, double* adam_v,
+                           int64_t t0, int32_t n_steps, double lr, double beta1,
+                           double beta2, double eps, double scale, int32_t* flag,
+                           void* nccl_comm, double* grad_buf, int32_t use_graph,
+                           void* scratch, size_t scratch_bytes, void* stream);
+
 /* Drop every CUDA graph cached by fm_epi_adam_steps (use_graph != 0). */
 void fm_release_cached_graphs(void);
 
@@ -496,6 +513,28 @@ int fm_cc_labels(int32_t n_nodes, int64_t n_edges, const int32_t* u, const int32
  */
 int fm_focal_votes(int32_t n_cand, int32_t n_pairs, const double* F, const double* focal,
                    const double* principal, double tau, double* votes_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* multi-GPU: NCCL communicator (SURVEY 8b "a multi-GPU variant of each takes */
+/* an ncclComm_t"; libnccl.so.2 is loaded at run time)                        */
+/* ------------------------------------------------------------------------ */
+#define FM_NCCL_UNIQUE_ID_BYTES 128
+
+/* 1 when libnccl.so.2 could be loaded, else 0. */
+int fm_nccl_available(void);
+/* ncclGetUniqueId into id_out [FM_NCCL_UNIQUE_ID_BYTES] (rank 0; the ranks
+ * exchange it out of band, e.g. a torch.distributed broadcast). */
+int fm_nccl_unique_id(void* id_out);
+/* ncclCommInitRank on the current CUDA device; *comm_out is an ncclComm_t. */
+int fm_nccl_comm_init(void** comm_out, int32_t n_ranks, const void* id, int32_t rank);
+int fm_nccl_comm_destroy(void* comm);
+/* In-place sum all-reduce of n doubles (the pass scalars of irls_refine,
+ * ref/epipolar.py:282-291); comm NULL = one rank (no-op). */
+int fm_nccl_allreduce_sum_f64(double* buf, int64_t n, void* comm, void* stream);
+/* recv [n_ranks][n] <- every rank's send [n], rank order (the multi-init
+ * translation merge, ref/translation.py:181-185). */
+int fm_nccl_allgather_f64(const double* send, double* recv, int64_t n, void* comm,
+                          void* stream);
 
 #ifdef __cplusplus
 }

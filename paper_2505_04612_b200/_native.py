@@ -44,7 +44,7 @@ FM_QUAD_MOM64 = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
-ABI_VERSION = 3
+ABI_VERSION = 4
 _F64 = ctypes.c_double
 _SZ = ctypes.c_size_t
 
@@ -106,7 +106,16 @@ SIGNATURES = {
     "fm_epi_adam_steps": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel), _P,
                                          _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64, _P,
                                          _I32, _P, _SZ, _P]),
+    "fm_epi_adam_steps_nccl": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel),
+                                              _P, _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64,
+                                              _P, _P, _P, _I32, _P, _SZ, _P]),
     "fm_release_cached_graphs": (None, []),
+    "fm_nccl_available": (ctypes.c_int, []),
+    "fm_nccl_unique_id": (ctypes.c_int, [_P]),
+    "fm_nccl_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), _I32, _P, _I32]),
+    "fm_nccl_comm_destroy": (ctypes.c_int, [_P]),
+    "fm_nccl_allreduce_sum_f64": (ctypes.c_int, [_P, _I64, _P, _P]),
+    "fm_nccl_allgather_f64": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
     "fm_rot6d_to_matrix": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "fm_rot6d_jacobian": (ctypes.c_int, [_P, _I64, _P, _P]),
     "fm_project_to_so3": (ctypes.c_int, [_P, _I64, _P, _P]),

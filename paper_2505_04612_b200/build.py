@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libfastmap_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["fm_core.cu", "fm_store.cu", "fm_point_pass.cu", "fm_epipolar.cu", "fm_translation.cu", "fm_sphere.cu",
-           "fm_fundamental.cu", "fm_rotation.cu", "fm_tracks.cu"]
+           "fm_fundamental.cu", "fm_rotation.cu", "fm_tracks.cu", "fm_dist.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

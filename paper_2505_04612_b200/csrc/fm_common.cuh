@@ -53,6 +53,10 @@ inline size_t scratch_round(size_t bytes) { return (bytes + 255) & ~size_t(255);
 
 int sm_count();
 
+// Sum all-reduce of n doubles in place over an NCCL communicator (comm NULL:
+// one rank, no-op); stream-ordered, CUDA-graph capturable (fm_dist.cu).
+int nccl_allreduce_sum_f64(double* buf, size_t n, void* comm, cudaStream_t st);
+
 // -------------------------------------------------------------- device side
 __device__ __forceinline__ void raise_flag(int32_t* flag, int code) {
   if (flag) atomicCAS(flag, 0, code);

@@ -1,0 +1,139 @@
+// Multi-GPU plumbing of the sharded hot path: the C ABI's
+// ncclComm_t entry points.  NCCL is resolved at run time with dlopen -- the
+// libnccl.so.2 torch.distributed already loaded when there is one (same
+// library, so one NCCL per process), else the system one -- so the library
+// still loads on hosts without NCCL or GPU.  The communicator is our own
+// (ncclCommInitRank over a unique id the ranks exchange through any
+// torch.distributed backend); every collective is stream-ordered on the
+// caller's stream and CUDA-graph capturable.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "fm_common.cuh"
+
+namespace fm {
+
+namespace {
+
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclCommCount) comm_count = nullptr;
+  decltype(&ncclCommUserRank) comm_user_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool loaded = false;
+};
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define FM_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    FM_SYM(get_unique_id, "ncclGetUniqueId");
+    FM_SYM(comm_init_rank, "ncclCommInitRank");
+    FM_SYM(comm_destroy, "ncclCommDestroy");
+    FM_SYM(comm_count, "ncclCommCount");
+    FM_SYM(comm_user_rank, "ncclCommUserRank");
+    FM_SYM(all_reduce, "ncclAllReduce");
+    FM_SYM(all_gather, "ncclAllGather");
+    FM_SYM(error_string, "ncclGetErrorString");
+#undef FM_SYM
+    api.loaded = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.comm_count &&
+                 api.comm_user_rank && api.all_reduce && api.all_gather && api.error_string;
+  });
+  return api.loaded ? &api : nullptr;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  const NcclApi* a = nccl_api();
+  return set_error(FM_ERR_CUDA, "%s failed: %s", what, a ? a->error_string(r) : "NCCL unavailable");
+}
+
+#define FM_NCCL(call, what)                       \
+  do {                                            \
+    ncclResult_t r__ = (call);                    \
+    if (r__ != ncclSuccess) return nccl_fail(r__, what); \
+  } while (0)
+
+}  // namespace
+
+int nccl_allreduce_sum_f64(double* buf, size_t n, void* comm, cudaStream_t st) {
+  if (!comm || n == 0) return FM_OK;  // one rank: the sum is the input
+  const NcclApi* a = nccl_api();
+  FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
+  FM_NCCL(a->all_reduce(buf, buf, n, ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm), st),
+          "ncclAllReduce");
+  return FM_OK;
+}
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+int fm_nccl_available(void) { return nccl_api() ? 1 : 0; }
+
+int fm_nccl_unique_id(void* id_out) {
+  FM_REQUIRE(id_out, "null id buffer");
+  const NcclApi* a = nccl_api();
+  FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
+  static_assert(sizeof(ncclUniqueId) == FM_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  FM_NCCL(a->get_unique_id(&id), "ncclGetUniqueId");
+  memcpy(id_out, &id, sizeof(id));
+  return FM_OK;
+}
+
+int fm_nccl_comm_init(void** comm_out, int32_t n_ranks, const void* id, int32_t rank) {
+  FM_REQUIRE(comm_out && id, "null comm / id");
+  FM_REQUIRE(n_ranks >= 1 && rank >= 0 && rank < n_ranks, "bad rank %d of %d", rank, n_ranks);
+  const NcclApi* a = nccl_api();
+  FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  FM_NCCL(a->comm_init_rank(&c, n_ranks, uid, rank), "ncclCommInitRank");
+  *comm_out = c;
+  return FM_OK;
+}
+
+int fm_nccl_comm_destroy(void* comm) {
+  if (!comm) return FM_OK;
+  const NcclApi* a = nccl_api();
+  FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
+  FM_NCCL(a->comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  return FM_OK;
+}
+
+int fm_nccl_allreduce_sum_f64(double* buf, int64_t n, void* comm, void* stream) {
+  FM_REQUIRE(n >= 0 && (buf || n == 0), "bad buffer");
+  return nccl_allreduce_sum_f64(buf, (size_t)n, comm, as_stream(stream));
+}
+
+int fm_nccl_allgather_f64(const double* send, double* recv, int64_t n, void* comm, void* stream) {
+  FM_REQUIRE(n >= 0 && ((send && recv) || n == 0), "bad buffers");
+  cudaStream_t st = as_stream(stream);
+  if (!comm) {
+    if (n && send != recv) FM_CUDA(cudaMemcpyAsync(recv, send, (size_t)n * sizeof(double),
+                                                   cudaMemcpyDeviceToDevice, st));
+    return FM_OK;
+  }
+  const NcclApi* a = nccl_api();
+  FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
+  FM_NCCL(a->all_gather(send, recv, (size_t)n, ncclFloat64, static_cast<ncclComm_t>(comm), st),
+          "ncclAllGather");
+  return FM_OK;
+}
+
+}  // extern "C"

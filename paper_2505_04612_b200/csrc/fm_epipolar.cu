@@ -458,6 +458,67 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
   if (lane < 9) R[9 * (int64_t)k + lane] = val;
 }
 
+// Replicated Adam of the sharded engine (ref/optim.py:24-36) over the
+// all-reduced packed gradient + loss `gbuf` [9N + C | loss]: blocks
+// [0, img_blocks) warp per image -- lanes 0..8 update the image's nine
+// parameters with the single-GPU expression (adam_elem), lanes 0..5 feed the
+// new rotation the next step's pairs read; the remaining blocks a thread per
+// camera (focal parameter + its scale exp(-log_focal)).  Checks follow
+// ref/epipolar.py:306-307 (loss) then ref/optim.py:28-29 (gradient).
+__global__ void __launch_bounds__(kReduceBlock)
+adam_dist_kernel(const fm_pair_graph g, double* __restrict__ params, const double* __restrict__ gbuf,
+                 double* __restrict__ R, const AdamArgs ad, int32_t* flag, const int img_blocks) {
+  if (*flag) return;
+  const int N = g.n_images;
+  const int n_cam = g.refine_focal ? g.n_cameras : 0;
+  const double loss = gbuf[(int64_t)9 * N + n_cam];
+  if (!isfinite(loss)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(flag, FM_ERR_NONFINITE_LOSS);
+    return;
+  }
+  const double lr = ad.sched[0];
+  const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+  if ((int)blockIdx.x >= img_blocks) {
+    const int c = ((int)blockIdx.x - img_blocks) * blockDim.x + threadIdx.x;
+    if (c >= n_cam) return;
+    const int64_t idx = (int64_t)9 * N + c;
+    const double gq = gbuf[idx];
+    if (!isfinite(gq)) {
+      raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+      return;
+    }
+    adam_elem(params[idx], ad.m[idx], ad.v[idx], gq, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+    R[idx] = exp(-params[idx]);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (k >= N) return;
+  const int64_t idx = lane < 6 ? 6 * (int64_t)k + lane : 6 * (int64_t)N + 3 * k + (lane - 6);
+  const double gq = lane < 9 ? gbuf[idx] : 0.0;
+  if (!__all_sync(0xffffffffu, lane >= 9 || isfinite(gq))) {
+    if (lane == 0) raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  double newp = 0.0;
+  if (lane < 9) {
+    double pv = params[idx];
+    adam_elem(pv, ad.m[idx], ad.v[idx], gq, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+    params[idx] = pv;
+    newp = pv;
+  }
+  double v6n[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) v6n[q] = __shfl_sync(0xffffffffu, newp, q);
+  double Rk[9];
+  const int code = rot6d_to_R(v6n, Rk);
+  if (lane == 0 && code) raise_flag(flag, code);
+  double val = Rk[0];
+#pragma unroll
+  for (int q = 1; q < 9; ++q) val = lane == q ? Rk[q] : val;
+  if (lane < 9) R[9 * (int64_t)k + lane] = val;
+}
+
 // Deterministic two-level sum of the per-pair loss terms.
 __global__ void loss_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
   __shared__ double red[256];
@@ -541,6 +602,47 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
       image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
           g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag);
       FM_LAUNCHED(image_reduce_kernel);
+    }
+  }
+  return FM_OK;
+}
+
+// Sharded form of enqueue_steps: per step the local pairs' packed gradient
+// and loss (the API kernels, fm_epi_loss_grad's), one all-reduce of
+// [9N + C | loss] over `comm`, then the replicated Adam step.
+int enqueue_steps_dist(const fm_pair_graph& g, const fm_quad_model& q, double* params, double* m,
+                       double* v, int n_steps, double b1, double b2, double eps, const EpiScratch& s,
+                       int32_t* flag, void* comm, double* gbuf, cudaStream_t st) {
+  const int N = g.n_images;
+  const int64_t P = g.n_pairs;
+  const int n_cam = g.refine_focal ? g.n_cameras : 0;
+  const size_t n_grad = (size_t)9 * N + n_cam;
+  const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
+  const int cam_blocks = (g.refine_focal && g.n_cameras > 0) ? g.n_cam_chunks : 0;
+  const int nb = loss_blocks(P);
+  for (int step = 0; step < n_steps; ++step) {
+    AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, step};
+    if (P > 0) {
+      if (int rc = launch_pair_grad(g, q, params, s, flag, st)) return rc;
+      if (img_blocks + cam_blocks > 0) {
+        image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
+            g, params, s.pg, gbuf, s.R, s.cpart, s.ticket, img_blocks, none, flag);
+        FM_LAUNCHED(image_reduce_kernel);
+      }
+      loss_partial_kernel<<<nb, 256, 0, st>>>(s.pg + (size_t)23 * P, P, s.lpart);
+      FM_LAUNCHED(loss_partial_kernel);
+      loss_final_kernel<<<1, 32, 0, st>>>(s.lpart, nb, gbuf + n_grad);
+      FM_LAUNCHED(loss_final_kernel);
+    } else {  // a rank without pairs contributes zeros
+      FM_CUDA(cudaMemsetAsync(gbuf, 0, (n_grad + 1) * sizeof(double), st));
+    }
+    if (int rc = nccl_allreduce_sum_f64(gbuf, n_grad + 1, comm, st)) return rc;
+    AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
+    const int cb = (int)ceil_div(n_cam, kReduceBlock);
+    if (img_blocks + cb > 0) {
+      adam_dist_kernel<<<(unsigned)(img_blocks + cb), kReduceBlock, 0, st>>>(g, params, gbuf, s.R, ad, flag,
+                                                                            img_blocks);
+      FM_LAUNCHED(adam_dist_kernel);
     }
   }
   return FM_OK;
@@ -655,10 +757,16 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   return FM_OK;
 }
 
-int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* params,
-                      double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
-                      double beta1, double beta2, double eps, double scale, int32_t* flag,
-                      int32_t use_graph, void* scratch, size_t scratch_bytes, void* stream) {
+}  // extern "C"
+
+namespace fm {
+namespace {
+// dist: the sharded step (comm may be NULL = one rank; gbuf [9N + C + 1]).
+int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* params, double* adam_m,
+                    double* adam_v, int64_t t0, int32_t n_steps, double lr, double beta1,
+                    double beta2, double eps, double scale, int32_t* flag, int32_t use_graph,
+                    void* scratch, size_t scratch_bytes, void* stream, bool dist, void* comm,
+                    double* gbuf) {
   if (int rc = check_graph(g)) return rc;
   if (int rc = check_quad(q)) return rc;
   FM_REQUIRE(flag, "fm_epi_adam_steps needs a device flag word");
@@ -683,11 +791,18 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
     }
     FM_CUDA(cudaMemcpyAsync(s.sched, sched.data(), sched.size() * sizeof(double),
                             cudaMemcpyHostToDevice, st));
+    auto enqueue = [&](cudaStream_t cs) {
+      return dist ? enqueue_steps_dist(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s,
+                                       flag, comm, gbuf, cs)
+                  : enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, cs);
+    };
     if (!use_graph) {
-      if (int rc = enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, st))
-        return rc;
+      if (int rc = enqueue(st)) return rc;
     } else {
       GraphKey key = make_key(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag);
+      key.k.push_back(dist ? 1u : 0u);
+      key.k.push_back(reinterpret_cast<uintptr_t>(comm));
+      key.k.push_back(reinterpret_cast<uintptr_t>(gbuf));
       cudaGraphExec_t exec = nullptr;
       {
         std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -698,7 +813,7 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
         cudaStream_t cs;
         FM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         FM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, cs);
+        int rc = enqueue(cs);
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(cs, &graph);
         cudaStreamDestroy(cs);
@@ -722,6 +837,28 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
     done += chunk;
   }
   return FM_OK;
+}
+}  // namespace
+}  // namespace fm
+
+extern "C" {
+
+int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* params,
+                      double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
+                      double beta1, double beta2, double eps, double scale, int32_t* flag,
+                      int32_t use_graph, void* scratch, size_t scratch_bytes, void* stream) {
+  return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, scale,
+                         flag, use_graph, scratch, scratch_bytes, stream, false, nullptr, nullptr);
+}
+
+int fm_epi_adam_steps_nccl(const fm_pair_graph* g, const fm_quad_model* q, double* params,
+                           double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
+                           double beta1, double beta2, double eps, double scale, int32_t* flag,
+                           void* nccl_comm, double* grad_buf, int32_t use_graph, void* scratch,
+                           size_t scratch_bytes, void* stream) {
+  FM_REQUIRE(grad_buf, "fm_epi_adam_steps_nccl needs grad_buf [9N + C + 1]");
+  return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, scale,
+                         flag, use_graph, scratch, scratch_bytes, stream, true, nccl_comm, grad_buf);
 }
 
 void fm_release_cached_graphs(void) {

@@ -8,7 +8,11 @@ the prune masks and the per-pair partials stay local.  The exchanges are
 * after each prune pass: one all-reduce of {Z, kept pairs, L1 sum} (3 doubles);
 * per Adam step: one all-reduce of the packed per-image gradient
   (9N + C doubles) and the loss; Adam then runs replicated on every rank
-  (identical inputs -> identical parameters, no broadcast).
+  (identical inputs -> identical parameters, no broadcast).  Over an
+  ``NcclComm`` (one shard per process) a 100-step chunk -- gradient kernels,
+  ncclAllReduce, Adam -- is one CUDA graph inside the C library
+  (fm_epi_adam_steps_nccl); over ``TorchComm`` (gloo, the CPU tests) the
+  step is driven from Python.
 
 ``ShardedIrlsEngine`` holds one or more local shards; with one shard per
 process and a ``torch.distributed`` communicator it is the multi-GPU engine,
@@ -72,8 +76,63 @@ class TorchComm:
         return out
 
 
+class NcclComm:
+    """An NCCL communicator of our own over the ranks of a torch.distributed
+    group (fm_nccl_comm_init; the unique id goes out through
+    broadcast_object_list on any backend).  Its collectives run inside our
+    library on the caller's stream, so the sharded Adam chunk -- local
+    gradient, ncclAllReduce, replicated Adam -- is one CUDA graph
+    (fm_epi_adam_steps_nccl).  Without an initialised process group it is a
+    one-rank communicator."""
+
+    native = True
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        on = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if on else 1
+        self.rank = dist.get_rank(group) if on else 0
+        lib = N.lib()
+        if not lib.fm_nccl_available():
+            raise RuntimeError("NCCL (libnccl.so.2) is not available")
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            N.check(lib.fm_nccl_unique_id(uid))
+        if self.world > 1:
+            obj = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        N.check(lib.fm_nccl_comm_init(ctypes.byref(h), self.world, uid, self.rank))
+        self.handle = h.value
+
+    def allreduce_(self, t):
+        assert t.dtype == torch.float64 and t.is_contiguous()
+        N.check(N.lib().fm_nccl_allreduce_sum_f64(N.ptr(t), t.numel(), self.handle,
+                                                  N.stream_handle()))
+        return t
+
+    def allgather(self, t):
+        """Equal-shaped float64 tensors of every rank, in rank order."""
+        src = t.contiguous().to(torch.float64)
+        out = torch.empty((self.world,) + tuple(src.shape), dtype=torch.float64, device=src.device)
+        N.check(N.lib().fm_nccl_allgather_f64(N.ptr(src), N.ptr(out), src.numel(), self.handle,
+                                              N.stream_handle()))
+        return [o.to(t.dtype) for o in out]
+
+    def close(self):
+        if self.handle:
+            N.check(N.lib().fm_nccl_comm_destroy(self.handle))
+            self.handle = None
+
+
 class NoComm:
     world, rank = 1, 0
+    native = True  # one rank: the native step chunk with a NULL communicator
+    handle = None
 
     def allreduce_(self, t):
         return t
@@ -125,17 +184,34 @@ class ShardedIrlsEngine:
               out=sh.buf.out(cur), scratch=sh.pscratch)
 
     def _scalars(self, cur, with_l1):
+        """{Z, kept pairs, L1 sum, pairs} over the shards and ranks: each
+        shard's pass left its fused totals {L1, Z, kept} in buf.tot."""
         s = torch.zeros(4, dtype=torch.float64, device=self.device)
         for sh in self.shards:
-            P = sh.graph.n_pairs
-            cnt = sh.buf.n_active[cur][:P]
-            s[0] += cnt.sum().double()
-            s[1] += (cnt > 0).sum().double()
+            s[0] += sh.buf.tot[1]
+            s[1] += sh.buf.tot[2]
             if with_l1:
-                s[2] += sh.buf.l1[:P].sum()
-            s[3] += P
+                s[2] += sh.buf.tot[0]
+            s[3] += sh.graph.n_pairs
         self.comm.allreduce_(s)
         return s.cpu().numpy()
+
+    @property
+    def native_steps(self):
+        """One shard per process over a native communicator: the Adam chunk
+        runs as fm_epi_adam_steps_nccl (collective inside the CUDA graph)."""
+        return len(self.shards) == 1 and getattr(self.comm, "native", False)
+
+    def _steps_native(self, t0, n_steps, lr, scale):
+        cfg = self.cfg
+        sh = self.shards[0]
+        if getattr(self, "gbuf", None) is None:
+            self.gbuf = torch.zeros(sh.graph.n_params + 1, dtype=torch.float64, device=self.device)
+        N.check(self.lib.fm_epi_adam_steps_nccl(
+            ctypes.byref(sh.graph.struct()), ctypes.byref(sh.buf.quad), N.ptr(self.params),
+            N.ptr(self.m), N.ptr(self.v), t0, n_steps, lr, cfg.adam_beta1, cfg.adam_beta2,
+            cfg.adam_eps, scale, N.ptr(self.aflag), self.comm.handle, N.ptr(self.gbuf), 1,
+            N.ptr(sh.gscratch), sh.gscratch.numel(), N.stream_handle()))
 
     def _check_flags(self):
         for sh in self.shards:
@@ -198,8 +274,11 @@ class ShardedIrlsEngine:
                                    0.0, 1 - cur, cur)
                         sh.buf.n_active[cur], sh.buf.n_active[1 - cur] = \
                             sh.buf.n_active[1 - cur], sh.buf.n_active[cur]
-                for k in range(steps):
-                    self._step(it * steps + k + 1, lr, 2.0 / Z)
+                if self.native_steps:
+                    self._steps_native(it * steps, steps, lr, 2.0 / Z)
+                else:
+                    for k in range(steps):
+                        self._step(it * steps + k + 1, lr, 2.0 / Z)
                 self._check_flags()
             lr /= cfg.lr_decay
         for sh in self.shards:
@@ -277,5 +356,5 @@ def gather_blocks(local, b, comm):
     return torch.cat([p[:, :int(b[r + 1] - b[r])] for r, p in enumerate(parts)], dim=1)
 
 
-__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NoComm", "make_shards",
+__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NcclComm", "NoComm", "make_shards",
            "init_blocks", "gather_blocks", "multi_init_align_sharded"]
