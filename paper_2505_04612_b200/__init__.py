@@ -11,7 +11,7 @@ from . import build  # noqa: F401
 
 __version__ = "0.1.0"
 
-__all__ = ["epipolar", "translation", "optim", "model", "config", "store", "install", "native_library"]
+__all__ = ["epipolar", "translation", "optim", "model", "config", "store", "inputs", "install", "native_library"]
 
 
 def native_library():
