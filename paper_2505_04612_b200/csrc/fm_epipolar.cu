@@ -26,15 +26,37 @@ namespace {
 
 constexpr int kPG = 24;          // per-pair gradient record: gRi 9, gRj 9, gdc 3, gphi_i, gphi_j, loss
 constexpr int kMaxSteps = 4096;  // steps per fm_epi_adam_steps call (bias-correction table)
+constexpr int kPairBlock = 64;   // pair_grad threads per block
+// Focal gradients with few cameras: pair_grad sums each block's per-camera
+// terms (a fixed tree) into cpart[c][block] and image_reduce reduces the
+// block partials with a warp per camera -- no incidence gather, no ticket.
+// More cameras: the per-camera incidence chunks (cam_chunk_*).
+constexpr int kBlockCams = 8;
+__host__ __device__ inline bool cams_by_block(const fm_pair_graph& g) {
+  return g.refine_focal && g.n_cameras > 0 && g.n_cameras <= kBlockCams;
+}
+inline int64_t pair_blocks(const fm_pair_graph& g) { return ceil_div(g.n_pairs, kPairBlock); }
+inline size_t cpart_len(const fm_pair_graph& g) {
+  size_t n = (size_t)std::max(g.n_cam_chunks, 1);
+  if (cams_by_block(g)) n = std::max(n, (size_t)g.n_cameras * (size_t)pair_blocks(g));
+  return n;
+}
 
 struct EpiScratch {
   double* R;      // [N][9] rotations, then [n_cameras] focal scales exp(-log_focal)
   double* pg;     // [kPG][P]
-  double* cpart;  // [n_cam_chunks]
+  double* cpart;  // [n_cam_chunks] or [n_cameras][pair blocks] (cams_by_block)
   double* lpart;  // [loss blocks]
   double* sched;  // [2 + 2*kMaxSteps]: lr, scale, bc1[], bc2[]
   unsigned int* ticket;  // camera-chunk completion counter (last block finalises)
 };
+
+// image_reduce blocks of the camera role: a warp per camera (cams_by_block)
+// or a block per incidence chunk.
+inline int cam_role_blocks(const fm_pair_graph& g) {
+  if (!(g.refine_focal && g.n_cameras > 0)) return 0;
+  return cams_by_block(g) ? (int)ceil_div(g.n_cameras, 2) : g.n_cam_chunks;
+}
 
 int loss_blocks(int64_t P) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(P, 1024), 1), 1024); }
 
@@ -42,7 +64,7 @@ size_t scratch_need(const fm_pair_graph& g) {
   size_t b = 0;
   b += scratch_round(((size_t)g.n_images * 9 + std::max(g.n_cameras, 1)) * sizeof(double));
   b += scratch_round((size_t)g.n_pairs * kPG * sizeof(double));
-  b += scratch_round((size_t)std::max(g.n_cam_chunks, 1) * sizeof(double));
+  b += scratch_round(cpart_len(g) * sizeof(double));
   b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
   b += scratch_round((size_t)(2 + 2 * kMaxSteps) * sizeof(double));
   b += scratch_round(sizeof(unsigned int));
@@ -53,7 +75,7 @@ bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
   Scratch sc(p, n);
   s.R = sc.take<double>((size_t)g.n_images * 9 + std::max(g.n_cameras, 1));
   s.pg = sc.take<double>((size_t)g.n_pairs * kPG);
-  s.cpart = sc.take<double>((size_t)std::max(g.n_cam_chunks, 1));
+  s.cpart = sc.take<double>(cpart_len(g));
   s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
   s.sched = sc.take<double>((size_t)(2 + 2 * kMaxSteps));
   s.ticket = sc.take<unsigned int>(1);
@@ -95,22 +117,35 @@ struct PairFwd {
 // EXACT: ghat = G / ||G|| by division, as the reference (the point passes'
 // linearisation point, whose residuals decide pruning); otherwise one
 // reciprocal and nine products (the per-step gradient path, <= 1.5 ulp).
+// Where a step reads the per-image geometry: rotation of image i at
+// R + rs * i, its centre at C + cs * i, camera c's focal scale exp(-log_focal)
+// at F[c] (geo_split: R [N][9] | F from image_rot_kernel, the packed params'
+// centres).
+struct Geo {
+  const double* R;
+  const double* C;
+  const double* F;
+  int rs, cs;
+};
+__device__ __forceinline__ Geo geo_split(const fm_pair_graph& g, const double* params, const double* R) {
+  return Geo{R, params + 6 * (int64_t)g.n_images, R + 9 * (int64_t)g.n_images, 9, 3};
+}
+
 template <bool EXACT>
-__device__ __forceinline__ void pair_forward(const fm_pair_graph& g, const double* params,
-                                             const double* R, int64_t n, PairFwd& f) {
+__device__ __forceinline__ void pair_forward(const fm_pair_graph& g, const Geo& geo, int64_t n,
+                                             PairFwd& f) {
   const int i = g.pair_i[n], j = g.pair_j[n];
-  const int N = g.n_images;
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    f.Ri[q] = R[9 * i + q];
-    f.Rj[q] = R[9 * j + q];
+    f.Ri[q] = geo.R[(int64_t)geo.rs * i + q];
+    f.Rj[q] = geo.R[(int64_t)geo.rs * j + q];
   }
-  const double* ci = params + 6 * N + 3 * i;
-  const double* cj = params + 6 * N + 3 * j;
+  const double* ci = geo.C + (int64_t)geo.cs * i;
+  const double* cj = geo.C + (int64_t)geo.cs * j;
   essential(f.Ri, f.Rj, ci, cj, f.dc, f.t, f.Rrel, f.E);
   if (g.refine_focal) {
-    f.di = R[9 * N + g.pair_ci[n]];  // exp(-log_focal), image_rot_kernel / cam_finalise
-    f.dj = R[9 * N + g.pair_cj[n]];
+    f.di = geo.F[g.pair_ci[n]];  // exp(-log_focal), image_rot_kernel / cam_update
+    f.dj = geo.F[g.pair_cj[n]];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -140,7 +175,7 @@ __global__ void pair_ghat_kernel(const fm_pair_graph g, const double* __restrict
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= g.n_pairs) return;
   PairFwd f;
-  pair_forward<true>(g, params, R, n, f);
+  pair_forward<true>(g, geo_split(g, params, R), n, f);
 #pragma unroll
   for (int q = 0; q < 9; ++q) ghat[q * g.n_pairs + n] = f.gh[q];
 }
@@ -167,18 +202,17 @@ __device__ __forceinline__ void mom_apply(const T* __restrict__ mom, int64_t P, 
 }
 
 // Loss term and full backward of one pair (ref/epipolar.py:172-232).
+struct PairGradOut {
+  double gRi[9], gRj[9], gdc[3], gphi_i, gphi_j, loss;
+};
+
 template <int KIND>
-__global__ void pair_grad_kernel(const fm_pair_graph g, const fm_quad_model q,
-                                 const double* __restrict__ params, const double* __restrict__ R,
-                                 const double* __restrict__ sched, double* __restrict__ pg,
-                                 int32_t* flag) {
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void pair_grad_one(const fm_pair_graph& g, const fm_quad_model& q,
+                                              const Geo& geo, const double scale, const int64_t n,
+                                              PairGradOut& o) {
   const int64_t P = g.n_pairs;
-  if (n >= P) return;
-  if (flag && *flag) return;
-  const double scale = sched[1];
   PairFwd f;
-  pair_forward<false>(g, params, R, n, f);
+  pair_forward<false>(g, geo, n, f);
 
   double u[9], Ln;
   if (KIND == FM_QUAD_SHIFTED32) {
@@ -269,16 +303,71 @@ __global__ void pair_grad_kernel(const fm_pair_graph g, const fm_quad_model q,
 
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    pg[k * P + n] = gRi[k];
-    pg[(9 + k) * P + n] = gRj[k];
+    o.gRi[k] = gRi[k];
+    o.gRj[k] = gRj[k];
   }
 #pragma unroll
-  for (int k = 0; k < 3; ++k) pg[(18 + k) * P + n] = gdc[k];
-  pg[21 * P + n] = gphi_i;
-  pg[22 * P + n] = gphi_j;
-  pg[23 * P + n] = loss_n;
-  if (!isfinite(loss_n)) raise_flag(flag, FM_ERR_NONFINITE_LOSS);
+  for (int k = 0; k < 3; ++k) o.gdc[k] = gdc[k];
+  o.gphi_i = gphi_i;
+  o.gphi_j = gphi_j;
+  o.loss = loss_n;
 }
+
+// Step kernel: a thread per pair (pair_grad_one) + the block's focal partials.
+template <int KIND>
+__global__ void __launch_bounds__(kPairBlock)
+pair_grad_kernel(const fm_pair_graph g, const fm_quad_model q, const double* __restrict__ params,
+                 const double* __restrict__ R, const double* __restrict__ sched,
+                 double* __restrict__ pg, double* __restrict__ cpart, int32_t* flag) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t P = g.n_pairs;
+  // the block's threads agree (the block reduction below): a flag raised by
+  // another block mid-launch stops either all or none of this block's threads
+  if (__syncthreads_or(flag != nullptr && *flag != 0)) return;
+  double gphi_i = 0, gphi_j = 0;
+  int ci = -1, cj = -1;
+  if (n < P) {
+    PairGradOut o;
+    pair_grad_one<KIND>(g, q, geo_split(g, params, R), sched[1], n, o);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      pg[k * P + n] = o.gRi[k];
+      pg[(9 + k) * P + n] = o.gRj[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pg[(18 + k) * P + n] = o.gdc[k];
+    pg[21 * P + n] = o.gphi_i;
+    pg[22 * P + n] = o.gphi_j;
+    pg[23 * P + n] = o.loss;
+    if (!isfinite(o.loss)) raise_flag(flag, FM_ERR_NONFINITE_LOSS);
+    gphi_i = o.gphi_i;
+    gphi_j = o.gphi_j;
+    if (g.refine_focal) {
+      ci = g.pair_ci[n];
+      cj = g.pair_cj[n];
+    }
+  }
+  if (cams_by_block(g)) {
+    // per-camera sums of this block's focal terms: warp butterflies, then the
+    // two warps in order (fixed order -> reproducible)
+    __shared__ double wsum[kPairBlock / 32][kBlockCams];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = 0; c < g.n_cameras; ++c) {
+      double v = (ci == c ? gphi_i : 0.0) + (cj == c ? gphi_j : 0.0);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) wsum[w][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < g.n_cameras) {
+      double v = 0;
+#pragma unroll
+      for (int k = 0; k < kPairBlock / 32; ++k) v += wsum[k][threadIdx.x];
+      cpart[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
+    }
+  }
+}
+
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {
@@ -312,6 +401,27 @@ struct AdamArgs {
 // fixed-order partial sum of focal gradients (ref/epipolar.py:194-196).
 constexpr int kReduceBlock = 64;  // 2 warps: spreads small image counts over all SMs
 
+// Camera c's focal gradient `acc` (lane 0): the packed gradient (API) or
+// Adam and the focal scale the next step's pairs read.
+template <bool ADAM>
+__device__ __forceinline__ void cam_update(const fm_pair_graph& g, double* __restrict__ params,
+                                           double* F, double* __restrict__ grad, const AdamArgs& ad,
+                                           int32_t* flag, int c, double acc) {
+  const int idx = 9 * g.n_images + c;
+  if (!ADAM) {
+    grad[idx] = acc;
+    return;
+  }
+  if (!isfinite(acc)) {
+    raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  const double lr = ad.sched[0];
+  const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
+  adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
+  F[c] = exp(-params[idx]);  // the focal scale the next step's pairs read
+}
+
 template <bool ADAM>
 __device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params, double* R,
                              const double* __restrict__ cpart, double* __restrict__ grad,
@@ -323,20 +433,7 @@ __device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params
     double acc = 0;
     for (int k = g.cam_chunk_off[c] + lane; k < g.cam_chunk_off[c + 1]; k += 32) acc += __ldcg(cpart + k);
     acc = warp_sum(acc);
-    if (lane != 0) continue;
-    const int idx = 9 * g.n_images + c;
-    if (!ADAM) {
-      grad[idx] = acc;
-      continue;
-    }
-    if (!isfinite(acc)) {
-      raise_flag(flag, FM_ERR_NONFINITE_GRAD);
-      continue;
-    }
-    const double lr = ad.sched[0];
-    const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
-    adam_elem(params[idx], ad.m[idx], ad.v[idx], acc, lr, ad.b1, ad.b2, ad.eps, bc1, bc2);
-    R[9 * g.n_images + c] = exp(-params[idx]);  // the focal scale the next step's pairs read
+    if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
   }
 }
 
@@ -357,6 +454,22 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
   __shared__ double red[kReduceBlock];
   __shared__ bool last;
   const int64_t P = g.n_pairs;
+  if ((int)blockIdx.x >= img_blocks && cams_by_block(g)) {  // ---- camera role, few cameras
+    // warp per camera: pair_grad's block partials cpart[c][0 .. nb) in a
+    // fixed lane-strided order + butterfly
+    const int c = ((int)blockIdx.x - img_blocks) * (kReduceBlock / 32) + (threadIdx.x >> 5);
+    if (c >= g.n_cameras) return;
+    if (ADAM && *flag) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (P + kPairBlock - 1) / kPairBlock;
+    const double* part = cpart + (int64_t)c * nb;
+    double acc = 0;
+#pragma unroll 4
+    for (int64_t k = lane; k < nb; k += 32) acc += part[k];
+    acc = warp_sum(acc);
+    if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
+    return;
+  }
   if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
     const int c = blockIdx.x - img_blocks;
     // a raised flag skips the work but never the ticket: every chunk block
@@ -399,16 +512,33 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0;
   const int e0 = g.img_off[k], e1 = g.img_off[k + 1];
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const int inc = g.img_inc[e];
-    const int64_t n = inc >> 1;
-    const int side = inc & 1;
-    const int base = side ? 9 : 0;
-    const double sgn = side ? 1.0 : -1.0;
+  // batches of kGather incidences per lane: all index loads, then all
+  // gradient loads in flight together, then the adds in incidence order (the
+  // per-lane accumulation order of a plain loop)
+  constexpr int kGather = 4;
+  for (int eb = e0 + lane; eb < e1; eb += 32 * kGather) {
+    int inc[kGather];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += pg[(base + q) * P + n];
+    for (int u = 0; u < kGather; ++u) inc[u] = eb + 32 * u < e1 ? g.img_inc[eb + 32 * u] : -1;
+    double v[kGather][12];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) acc[9 + q] += sgn * pg[(18 + q) * P + n];
+    for (int u = 0; u < kGather; ++u) {
+      const int64_t n = inc[u] >= 0 ? (inc[u] >> 1) : 0;
+      const int base = (inc[u] & 1) ? 9 : 0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[u][q] = inc[u] >= 0 ? pg[(base + q) * P + n] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[u][9 + q] = inc[u] >= 0 ? pg[(18 + q) * P + n] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kGather; ++u) {
+      if (inc[u] < 0) break;
+      const double sgn = (inc[u] & 1) ? 1.0 : -1.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += v[u][q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc[9 + q] += sgn * v[u][9 + q];
+    }
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = warp_sum(acc[q]);
@@ -549,16 +679,19 @@ __global__ void set_sched_kernel(double* sched, double lr, double scale, unsigne
 
 int launch_pair_grad(const fm_pair_graph& g, const fm_quad_model& q, const double* params,
                      const EpiScratch& s, int32_t* flag, cudaStream_t st) {
-  const unsigned blocks = (unsigned)ceil_div(g.n_pairs, 64);
+  const unsigned blocks = (unsigned)pair_blocks(g);
   switch (q.kind) {
     case FM_QUAD_SHIFTED32:
-      pair_grad_kernel<FM_QUAD_SHIFTED32><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_SHIFTED32><<<blocks, kPairBlock, 0, st>>>(g, q, params, s.R, s.sched, s.pg, s.cpart,
+                                                                    flag);
       break;
     case FM_QUAD_W64:
-      pair_grad_kernel<FM_QUAD_W64><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_W64><<<blocks, kPairBlock, 0, st>>>(g, q, params, s.R, s.sched, s.pg, s.cpart,
+                                                                    flag);
       break;
     case FM_QUAD_MOM64:
-      pair_grad_kernel<FM_QUAD_MOM64><<<blocks, 64, 0, st>>>(g, q, params, s.R, s.sched, s.pg, flag);
+      pair_grad_kernel<FM_QUAD_MOM64><<<blocks, kPairBlock, 0, st>>>(g, q, params, s.R, s.sched, s.pg, s.cpart,
+                                                                    flag);
       break;
     default:
       return set_error(FM_ERR_INVALID, "unknown quadratic model kind %d", q.kind);
@@ -597,7 +730,7 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
     if (rc) return rc;
     AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
     const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
-    const int cam_blocks = (g.refine_focal && g.n_cameras > 0) ? g.n_cam_chunks : 0;
+    const int cam_blocks = cam_role_blocks(g);
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
           g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag);
@@ -618,7 +751,7 @@ int enqueue_steps_dist(const fm_pair_graph& g, const fm_quad_model& q, double* p
   const int n_cam = g.refine_focal ? g.n_cameras : 0;
   const size_t n_grad = (size_t)9 * N + n_cam;
   const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
-  const int cam_blocks = (g.refine_focal && g.n_cameras > 0) ? g.n_cam_chunks : 0;
+  const int cam_blocks = cam_role_blocks(g);
   const int nb = loss_blocks(P);
   for (int step = 0; step < n_steps; ++step) {
     AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, step};
@@ -741,7 +874,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
   AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, 0};
   {
     const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
-    const int cam_blocks = (g->refine_focal && g->n_cameras > 0) ? g->n_cam_chunks : 0;
+    const int cam_blocks = cam_role_blocks(*g);
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
           *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, s.ticket, img_blocks,

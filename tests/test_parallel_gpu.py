@@ -68,8 +68,8 @@ def _c1_inputs(g):
 def test_nccl_step_chunk_bitwise_single_engine(golden_c1):
     """One shard over a real one-rank NCCL communicator: the graphed chunk
     (local gradient -> ncclAllReduce -> replicated Adam,
-    fm_epi_adam_steps_nccl) follows the single-store engine's fused
-    image_reduce Adam bit for bit."""
+    fm_epi_adam_steps_nccl) follows the single-store engine's step (pair_grad +
+    image_reduce with Adam) bit for bit."""
     from paper_2505_04612_b200 import epipolar as E
     g = golden_c1
     dev = torch.device("cuda")
@@ -168,3 +168,4 @@ def test_two_ranks_gloo_one_gpu_matches_reference():
     start = np.concatenate([[0], np.cumsum(lengths)])
     per_pair = np.array([active[start[k]:start[k + 1]].sum() for k in range(len(lengths))])
     assert np.array_equal(per_pair, g["c1_active_count"])
+
