@@ -475,14 +475,17 @@ def check_prefix(eng, store, mode, n_check=250):
             "counts": "bit-exact" if "active counts" not in bad else "differ"}
 
 
-def time_passes(eng, stream, k_steps, reduce_fn, flush=True):
+def time_passes(eng, stream, k_steps, reduce_fn, flush=True, nvtx=None):
     """k_steps passes, each bracketed by CUDA events on the launching stream
-    (the scalar reduction / all-reduce inside the window)."""
+    (the scalar reduction / all-reduce inside the window).  nvtx: name of an
+    NVTX range around the steps (ncu --nvtx-include selects the timed region)."""
     import torch
     flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=stream.device)
     flush_r = torch.ones(64 << 20, dtype=torch.float32, device=stream.device)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(k_steps)]
+    if nvtx:
+        torch.cuda.nvtx.range_push(nvtx)
     with torch.cuda.stream(stream):
         for k in range(k_steps):
             if flush:
@@ -496,6 +499,8 @@ def time_passes(eng, stream, k_steps, reduce_fn, flush=True):
             eng.point_pass(HOT_MODE(), TH, 0, 0)
             reduce_fn()
             ends[k].record(stream)
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     del flush_w, flush_r
     return [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -560,7 +565,7 @@ def run_ours(args, spec, world, rank, local):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms = time_passes(eng, stream, args.steps, reduce_scalars)
+        ms = time_passes(eng, stream, args.steps, reduce_scalars, nvtx="fm_timed")
     ms_step = max_over_ranks(np.mean(ms), device, world)
     Z_all = sum_over_ranks(Z, device, world)
     value = Z_all / (ms_step * 1e-3)
@@ -721,6 +726,8 @@ def sfm_optimize(args, spec, scene, store, graph, ids, device, stream, world, ra
             out.update(api_irls_bench(args, scene, device, stream))
     if world > 1:
         out.update(sharded_irls_bench(spec, args, device, stream, world, rank))
+    elif not args.skip_api:
+        out.update(nccl_one_rank_bench(args, scene, store, graph, ids, device, stream))
     out.update(translation_bench(device, stream, sharded=world > 1))
     return out
 
@@ -760,6 +767,40 @@ def api_irls_bench(args, scene, device, stream):
     return {"irls_refine_api_s": dt, "api_l1_history": rep["l1_history"],
             "api_note": "drop-in irls_refine on 25,000 EpipolarPair objects (fp64 host arrays): "
                         "store build + H2D upload + device schedule + mask write-back"}
+
+
+def nccl_one_rank_bench(args, scene, store, graph, ids, device, stream):
+    """The multi-GPU engine's code path at N = 1: irls_refine through
+    parallel.ShardedIrlsEngine over a real one-rank NCCL communicator (one
+    shard; each 100-step chunk = gradient kernels + ncclAllReduce + Adam in
+    one CUDA graph, fm_epi_adam_steps_nccl).  Its L1 history equals the
+    single engine's bit for bit (tests/test_parallel_gpu.py)."""
+    import torch
+
+    from paper_2505_04612_b200 import parallel as P_
+    from paper_2505_04612_b200 import scenes
+    try:
+        comm = P_.NcclComm()
+    except RuntimeError as exc:
+        return {"irls_refine_nccl1_s": None, "nccl1_note": str(exc)}
+    try:
+        with torch.cuda.stream(stream):
+            times, l1h = [], None
+            for _ in range(2):  # the first run captures the step graphs
+                store.reset_active()
+                params = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
+                eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params, args.cfg,
+                                           comm=comm)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                l1h = eng.run()
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+    finally:
+        comm.close()
+    return {"irls_refine_nccl1_s": times[-1], "irls_nccl1_l1_history": l1h,
+            "nccl1_note": "ShardedIrlsEngine, one shard, one-rank NCCL communicator: the "
+                          "multi-GPU step graph (gradient -> ncclAllReduce -> Adam)"}
 
 
 def sharded_irls_bench(spec, args, device, stream, world, rank):

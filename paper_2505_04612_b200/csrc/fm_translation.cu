@@ -288,6 +288,9 @@ __device__ __forceinline__ double flip(double x, long long sign_mask) {
 // incidence order (the reference's np.add.at order, see the file comment):
 // 3R sequential chains per warp, no redundant shuffled folds.
 // kTrAdam: Adam step cur -> nxt.  kTrGrad: write the gradient (API).
+#ifndef FM_TR_IF
+#define FM_TR_IF 4  // incidences in flight per lane (C3: 2 -> 4 took 0.61 -> 0.54 s)
+#endif
 #ifndef FM_TR_MINB
 #define FM_TR_MINB 2  // resident 256-thread blocks per SM (3: register cap 80, spills, no faster)
 #endif
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_g
                                double lr, double b1, double b2, double eps,
                                const double* const* __restrict__ bc, int step, int32_t* flag) {
   constexpr int kSlots = 32 / R;
-  constexpr int kIF = 2;               // incidences in flight per lane
+  constexpr int kIF = FM_TR_IF;        // incidences in flight per lane
   constexpr int kTile = kIF * 32 * 3;  // doubles per warp: [kIF * kSlots][R][3]
   __shared__ double tile_all[8][kTile];
   const int lane = threadIdx.x & 31;

@@ -387,11 +387,20 @@ class IrlsEngine:
     def point_pass(self, mode, threshold, cur, prev):
         if mode & N.FM_PASS_MOMENTS:
             mode |= self.buf.flags
+        torch.cuda.nvtx.range_push(f"fm/point_pass 0x{mode:x}")
         _pass(self.store, mode, threshold, ghat=self.buf.ghat0,
               prev_active=self.buf.n_active[prev] if (mode & N.FM_PASS_SKIP_DROPPED) else None,
               out=self.buf.out(cur), scratch=self.pscratch)
+        torch.cuda.nvtx.range_pop()
 
     def run(self):
+        torch.cuda.nvtx.range_push("fm/irls_refine")
+        try:
+            return self._run()
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _run(self):
         cfg = self.cfg
         P = self.graph.n_pairs
         thresholds = prune_thresholds(cfg)
@@ -429,12 +438,14 @@ class IrlsEngine:
                     # counts unchanged (no prune); keep the current buffer authoritative
                     self.buf.n_active[cur], self.buf.n_active[1 - cur] = \
                         self.buf.n_active[1 - cur], self.buf.n_active[cur]
+                torch.cuda.nvtx.range_push("fm/adam_steps")
                 N.check(self.lib.fm_epi_adam_steps(
                     ctypes.byref(self.graph.struct()), ctypes.byref(self.buf.quad),
                     N.ptr(self.params), N.ptr(self.adam_m), N.ptr(self.adam_v),
                     it * steps, steps, lr, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
                     2.0 / Z, N.ptr(self.flag), int(self.use_graph), N.ptr(self.gscratch),
                     self.gscratch.numel(), N.stream_handle()))
+                torch.cuda.nvtx.range_pop()
                 N.raise_flag(self.flag.item())
             lr /= cfg.lr_decay
         self._ghat()
