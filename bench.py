@@ -418,7 +418,12 @@ def make_engine(spec, device, args, pair_slice=None, seed_offset=0):
 
 
 def check_prefix(eng, store, mode, n_check=250):
-    """The timed pass on the first n_check image pairs vs the CPU oracle
+    """The timed pass on the first n_check image pairs vs the CPU oracle."""
+    return check_pairs(eng, store, mode, np.arange(min(n_check, store.n_pairs)))
+
+
+def check_pairs(eng, store, mode, sel):
+    """The timed pass on the image pairs `sel` (store order) vs the CPU oracle
     (ref/epipolar.py:280-301 restated, pinned to the reference's golden
     vectors): run one more pass from a snapshot of the masks and compare
     counts and masks bit-exact, L1 within 1e-5, W within 2e-5 of the pair's
@@ -427,10 +432,10 @@ def check_prefix(eng, store, mode, n_check=250):
 
     from oracle import fastmap_oracle as O
     from paper_2505_04612_b200 import epipolar as E
-    P = store.n_pairs
-    n = min(n_check, P)
-    lens = store.len_caller[:n]
-    off = store.pair_off[:n]
+    sel = np.asarray(sel, dtype=np.int64)
+    n = len(sel)
+    lens = np.asarray(store.len_caller)[sel]
+    off = np.asarray(store.pair_off)[sel]
     idx = np.concatenate([np.arange(o, o + m) for o, m in zip(off, lens)])
     bits_before = store.active_bits()[torch.as_tensor(idx, device=store.device)].cpu().numpy()
     eng.point_pass(mode, TH, 1, 0)
@@ -441,31 +446,32 @@ def check_prefix(eng, store, mode, n_check=250):
                        lens, active=bits_before)
     # pairs dropped by an earlier prune (prev == 0) are skipped by the pass:
     # all their points are inactive, so the oracle gives them zero outputs too
-    gh = eng.buf.ghat0[:, :n].cpu().numpy().T
+    seld = torch.as_tensor(sel, device=store.device)
+    gh = eng.buf.ghat0[:, seld].cpu().numpy().T
     ref = O.point_pass(flat, gh, threshold=TH)
     bits_after = store.active_bits()[torch.as_tensor(idx, device=store.device)].cpu().numpy()
     bad = []
-    if not np.array_equal(eng.buf.n_active[1][:n].cpu().numpy(), ref["n_active"]):
+    if not np.array_equal(eng.buf.n_active[1][seld].cpu().numpy(), ref["n_active"]):
         bad.append("active counts")
     if not np.array_equal(bits_after, flat.active):
         bad.append("prune masks")
-    l1 = eng.buf.l1[:n].cpu().numpy()
+    l1 = eng.buf.l1[seld].cpu().numpy()
     if np.max(np.abs(l1 - ref["l1"]) / np.maximum(np.abs(ref["l1"]), 1e-300)) > 1e-5:
         bad.append("L1")
     scale = np.abs(ref["W"]).max(axis=(1, 2), keepdims=True) + 1e-300
     if eng.buf.precision == "fp64":
-        W = E.moments_to_weights(eng.buf.mom64[:, :n].cpu().numpy())
+        W = E.moments_to_weights(eng.buf.mom64[:, seld].cpu().numpy())
         werr = float(np.max(np.abs(W - ref["W"]) / scale))
         wtol = 3e-7
     else:
-        W = E.moments_to_weights(eng.buf.mom32[:, :n].cpu().numpy())
+        W = E.moments_to_weights(eng.buf.mom32[:, seld].cpu().numpy())
         werr = float(np.max(np.abs(W - ref["W"]) / scale))
         wtol = 2e-5
-        vg = eng.buf.vgrad[:, :n].cpu().numpy().T
+        vg = eng.buf.vgrad[:, seld].cpu().numpy().T
         vscale = max(float(np.abs(O.terms_of(flat.x1, flat.x2)).sum(axis=0).max()), 1.0)
         if np.max(np.abs(vg - ref["vgrad"])) > 1e-5 * vscale:
             bad.append("linearisation terms")
-        s0 = eng.buf.s0[:n].cpu().numpy()
+        s0 = eng.buf.s0[seld].cpu().numpy()
         if np.max(np.abs(s0 - ref["s0"]) / np.maximum(np.abs(ref["s0"]), 1e-300)) > 1e-5:
             bad.append("s0")
     if werr > wtol:
@@ -689,9 +695,21 @@ def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10):
         dist.barrier()
     ms = max_over_ranks(np.mean(time_passes(eng, stream, steps, reduce_scalars)), device, world)
     total = spec.n_pairs * spec.points_per_pair
+    # parity at full size: 200 image pairs spread over this rank's range vs
+    # the CPU oracle (the same checks as the C2 prefix)
+    with torch.cuda.stream(stream):
+        sel = np.unique(np.linspace(0, store.n_pairs - 1, 200).astype(np.int64))
+        chk = check_pairs(eng, store, HOT_MODE(), sel)
+    if not chk["ok"]:
+        print(f"bench: the {cfg_name.upper()} pass does not match the CPU oracle: {chk}",
+              file=sys.stderr, flush=True)
+        sys.exit(3)
     out = {"config": f"{cfg_name.upper()}: {spec.n_pairs} image pairs / {total} point pairs split "
                      f"over {world} GPU(s)", "scaling": "strong", "value": total / (ms * 1e-3),
-           "unit": UNIT, "ms_per_step": ms, "steps": steps}
+           "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "parity_check": {k: chk[k] for k in ("pairs", "points", "ok", "masks", "counts",
+                                                 "W_max_rel_err")},
+           "parity_sample": "200 image pairs spread evenly over the (rank-0) range"}
     del eng, store, graph
     gc.collect()
     torch.cuda.empty_cache()
