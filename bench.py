@@ -535,6 +535,23 @@ def sum_over_ranks(x, device, world):
     return float(t.item())
 
 
+_SCALAR_COMM = {}
+
+
+def scalar_comm(world):
+    """The pass-scalar all-reduce of N > 1 steps: over NCCL our own
+    communicator (the collective on the pass's stream, no cross-stream
+    sync; parallel.NcclComm), over gloo torch.distributed's."""
+    import torch.distributed as dist
+
+    from paper_2505_04612_b200 import parallel as P_
+    if world == 1:
+        return P_.NoComm()
+    if "c" not in _SCALAR_COMM:
+        _SCALAR_COMM["c"] = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
+    return _SCALAR_COMM["c"]
+
+
 def run_ours(args, spec, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -547,11 +564,13 @@ def run_ours(args, spec, world, rank, local):
         scene, store, graph, ids, eng = make_engine(spec, device, args, seed_offset=rank)
         eng._ghat()
         Z, P = store.n_points, store.n_pairs
+        comm = scalar_comm(world)
+
         def reduce_scalars():
             # what irls_refine needs after a pass: {L1, Z, kept pairs}, fused
             # into the pass kernel (fixed order); over all ranks when N > 1
             if world > 1:
-                dist.all_reduce(eng.buf.tot)
+                comm.allreduce_(eng.buf.tot)
 
         # first pass: prunes and sets the counts SKIP_DROPPED uses (steady state)
         eng.buf.n_active[0].fill_(1)
@@ -616,6 +635,16 @@ def run_ours(args, spec, world, rank, local):
     strong = None
     if not args.skip_strong:
         strong = strong_bench(args, device, stream, world, rank)
+        if world > 1:
+            # the north star's C5 efficiency in this run: rank 0 also times the
+            # whole C5 on its own GPU (16 GB store; the other ranks wait)
+            t1 = None
+            if rank == 0:
+                t1 = strong_bench(args, device, stream, world, rank, single=True)["ms_per_step"]
+            dist.barrier()
+            if rank == 0:
+                strong["ms_per_step_1gpu_same_run"] = t1
+                strong["efficiency_vs_1gpu"] = t1 / (world * strong["ms_per_step"])
 
     # ---------------------------------------------------- SfM optimize time
     extra = {}
@@ -666,10 +695,15 @@ def run_ours(args, spec, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10):
+def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10, single=False):
     """C5 (1 B point pairs) split over the ranks by contiguous image-pair
     ranges (each rank generates only its range), the same pass + scalar
-    all-reduce, max over ranks.  At N=1 the whole C5 on one GPU."""
+    all-reduce, max over ranks.  At N=1 the whole C5 on one GPU.
+    single: this rank alone times the whole config on its GPU (no
+    collectives; the N = 1 reference point of the strong-scaling efficiency
+    measured inside an N > 1 run)."""
+    if single:
+        world, rank = 1, 0
     import gc
 
     import torch
@@ -683,9 +717,11 @@ def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10):
         del scene
         gc.collect()
         eng._ghat()
+        comm = scalar_comm(world)
+
         def reduce_scalars():
             if world > 1:
-                dist.all_reduce(eng.buf.tot)
+                comm.allreduce_(eng.buf.tot)
 
         eng.buf.n_active[0].fill_(1)
         eng.point_pass(HOT_MODE(), TH, 0, 0)
