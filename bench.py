@@ -481,7 +481,18 @@ def check_pairs(eng, store, mode, sel):
             "counts": "bit-exact" if "active counts" not in bad else "differ"}
 
 
-def time_passes(eng, stream, k_steps, reduce_fn, flush=True, nvtx=None):
+def pass_kernel_only(eng):
+    """One launch of the timed pass's kernel alone: the same mode and
+    buffers, without the pass-totals output (no totals reductions, no
+    finalize kernel) -- the kernel the roofline fraction is about."""
+    from paper_2505_04612_b200 import epipolar as E
+    out = {k: v for k, v in eng.buf.out(0).items() if k != "totals"}
+    mode = HOT_MODE() | eng.buf.flags
+    E._pass(eng.store, mode, TH, ghat=eng.buf.ghat0, prev_active=eng.buf.n_active[0], out=out,
+            scratch=eng.pscratch)
+
+
+def time_passes(eng, stream, k_steps, reduce_fn, flush=True, nvtx=None, step_fn=None):
     """k_steps passes, each bracketed by CUDA events on the launching stream
     (the scalar reduction / all-reduce inside the window).  nvtx: name of an
     NVTX range around the steps (ncu --nvtx-include selects the timed region)."""
@@ -502,7 +513,10 @@ def time_passes(eng, stream, k_steps, reduce_fn, flush=True, nvtx=None):
                 flush_r.sum()
             torch.cuda._sleep(400_000)  # the events bracket device work only
             starts[k].record(stream)
-            eng.point_pass(HOT_MODE(), TH, 0, 0)
+            if step_fn is None:
+                eng.point_pass(HOT_MODE(), TH, 0, 0)
+            else:
+                step_fn()
             reduce_fn()
             ends[k].record(stream)
     if nvtx:
@@ -595,10 +609,17 @@ def run_ours(args, spec, world, rank, local):
     Z_all = sum_over_ranks(Z, device, world)
     value = Z_all / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (the pass), from the same events
+    # roofline of the dominant kernel (the pass): its own launches, timed the
+    # same way (events on the launching stream, L2 flushed), without the
+    # step's totals reductions / finalize kernel; the step fraction beside it
+    with torch.cuda.stream(stream):
+        ms_k = time_passes(eng, stream, args.steps, lambda: None,
+                           step_fn=lambda: pass_kernel_only(eng))
+    ms_kernel = max_over_ranks(np.mean(ms_k), device, world)
     bytes_launch = pass_bytes(points_read, P, args.precision)
     hbm, hbm_kind = peaks()
-    achieved = bytes_launch / (ms_step * 1e-3) / 1e9
+    achieved = bytes_launch / (ms_kernel * 1e-3) / 1e9
+    achieved_step = bytes_launch / (ms_step * 1e-3) / 1e9
 
     # ------------------------------------------------------------------ e2e
     # through the C ABI with HOST buffers: pinned host store columns -> H2D,
@@ -664,9 +685,9 @@ def run_ours(args, spec, world, rank, local):
                          f"current_residuals + L1 + prune + precompute_weights "
                          f"(ref/epipolar.py:280-301) in {rp.procs} processes, best of 3: {t:.3f} s"}
 
-    # per step: the pass with its fused totals (+ the combine kernel when
-    # pairs span several work items)
-    launches = args.steps * (1 + (1 if store.n_items > store.n_pairs else 0))
+    # per step: the pass + the totals finalize kernel (+ the combine kernel
+    # when pairs span several work items)
+    launches = args.steps * (2 + (1 if store.n_items > store.n_pairs else 0))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -679,6 +700,12 @@ def run_ours(args, spec, world, rank, local):
             "config": workload_config(args, spec, world, P, Z),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(args.config, args.precision),
+                         "kernel_ms": ms_kernel,
+                         "kernel": "point_pass_hot_mixed (the pass kernel's own launches: no "
+                                   "totals output; events + L2 flush as the step)",
+                         "step_frac": achieved_step / hbm,
+                         "step_note": "the step = the pass + its fused totals (integer "
+                                      "reductions + a one-warp PDL finalize kernel)",
                          "peak_kind": hbm_kind, "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_model": "16.125 B per point read (pairs not dropped) + 292 B per "
                                         "image pair (fp32 moments; DESIGN.md 3.1)",
