@@ -385,3 +385,61 @@ def test_hot_point_pass_ragged_and_empty_pairs(precision, lanes, monkeypatch):
     mom = eng.buf.mom64 if precision == "fp64" else eng.buf.mom32
     W = E.moments_to_weights(mom.cpu().numpy()[:, :P])
     assert np.max(np.abs(W - ref["W"]) / scale) < (3e-7 if precision == "fp64" else 2e-5)
+
+
+@pytest.mark.parametrize("n_cams", [1, 3, 8, 12])
+def test_focal_gradient_paths_match_oracle(n_cams):
+    """quadratic_loss_and_grad with focal refinement (ref/epipolar.py:172-248):
+    <= 8 cameras take pair_grad's per-block camera partials, more cameras the
+    camera incidence chunks; both against the oracle (np.add.at focal sums,
+    same-camera pairs adding both terms, ref/epipolar.py:195-196)."""
+    poses, pairs = random_scene(n_images=14, n_points=300, seed=n_cams)
+    rng = np.random.default_rng(100 + n_cams)
+    cam_of = rng.integers(0, n_cams, size=14)
+    for p in pairs:
+        p.cam_i, p.cam_j = int(cam_of[p.i]), int(cam_of[p.j])
+    st = E.AdjustmentState.from_poses(poses, list(range(14)), n_cams, True)
+    st.log_focal[:] = rng.normal(scale=0.05, size=n_cams)
+    res = E.current_residuals(st, pairs)
+    W = [E.precompute_weights(p.x1[p.active], p.x2[p.active], residuals=r[p.active])
+         for p, r in zip(pairs, res)]
+    Z = int(sum(p.active.sum() for p in pairs))
+    loss, grad = E.quadratic_loss_and_grad(st, pairs, W, Z)
+    params = st.pack()
+    ij = np.array([[p.i, p.j] for p in pairs])
+    cams = np.array([[p.cam_i, p.cam_j] for p in pairs])
+    l_ref, g_ref = O.quad_loss_grad(params, 14, ij[:, 0], ij[:, 1], cams[:, 0], cams[:, 1], True,
+                                    n_cams, np.stack(W), Z)
+    np.testing.assert_allclose(loss, l_ref, rtol=1e-10)
+    np.testing.assert_allclose(grad, g_ref, rtol=1e-8, atol=1e-10 * np.abs(g_ref).max())
+    np.testing.assert_allclose(grad[-n_cams:], g_ref[-n_cams:], rtol=1e-9,
+                               atol=1e-12 * np.abs(g_ref[-n_cams:]).max())
+
+
+@pytest.mark.parametrize("n_cams", [3, 12])
+def test_irls_refine_focal_paths_match_oracle(n_cams):
+    """irls_refine with focal refinement through both camera paths of the
+    Adam step (block partials <= 8 cameras, incidence chunks above) against
+    the oracle's schedule (fp64 moments: prune decisions identical, focal
+    scales / poses / L1 history within the fp64-moment tolerances)."""
+    poses, pairs = random_scene(n_images=12, n_points=400, seed=40 + n_cams)
+    rng = np.random.default_rng(7 + n_cams)
+    cam_of = rng.integers(0, n_cams, size=12)
+    for p in pairs:
+        p.cam_i, p.cam_j = int(cam_of[p.i]), int(cam_of[p.j])
+    opairs = [SimplePair(i=p.i, j=p.j, cam_i=p.cam_i, cam_j=p.cam_j, x1=p.x1.copy(),
+                         x2=p.x2.copy(), active=p.active.copy()) for p in pairs]
+    cfg = Cfg(epipolar_lr=1e-4, epipolar_epoch_steps=30)
+    out, fs, rep = E.irls_refine(Poses(poses.rotations.copy(), poses.centers.copy()), pairs, cfg,
+                                 n_cameras=n_cams, precision="fp64")
+    flat = O.FlatPairs.from_pairs(opairs)
+    R, c, ofs, orep = O.irls_refine(poses.rotations, poses.centers,
+                                    np.array([[p.i, p.j] for p in opairs]),
+                                    np.array([[p.cam_i, p.cam_j] for p in opairs]), flat, cfg,
+                                    n_cameras=n_cams)
+    assert np.array_equal(np.concatenate([p.active for p in pairs]), flat.active)
+    assert [rep["dropped_pairs"], rep["active_pairs"]] == [orep["dropped_pairs"], orep["active_pairs"]]
+    np.testing.assert_allclose(rep["l1_history"], orep["l1_history"], rtol=1e-6)
+    np.testing.assert_allclose(fs, ofs, rtol=1e-6)
+    np.testing.assert_allclose(out.rotations, R, atol=1e-6)
+    np.testing.assert_allclose(out.centers, c, atol=1e-6)
