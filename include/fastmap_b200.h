@@ -182,13 +182,17 @@ typedef struct fm_pass_out {
   double* residual;   /* [n_slots]     or NULL; FM_PASS_RES_OUT */
   /* [3] or NULL: {sum of l1 (0 without FM_PASS_L1), Z = sum of n_active,
    * kept pairs = #(n_active > 0)} of this pass -- the scalars irls_refine
-   * needs per pass (ref/epipolar.py:282-291, :156-160).  Fused into the hot
-   * kernel (fixed order, no extra launch); needs n_active. */
+   * needs per pass (ref/epipolar.py:282-291, :156-160); needs n_active.  The
+   * hot kernel (one work item per pair) accumulates them exactly in 64-bit
+   * integer sums (L1 as fixed point: order-independent, so reproducible) and
+   * a one-warp kernel launched after it as a programmatic dependent launch
+   * converts them; other passes use one fixed-order reduction kernel. */
   double* totals;
 } fm_pass_out;
 
 /* Scratch of fm_point_pass.  It must be ZEROED before its first use (the
- * fused-totals ticket lives at offset 0; every launch leaves it zero). */
+ * fused-totals accumulators live at fixed offsets; every pass that uses them
+ * leaves them zero again).  One pass at a time per scratch (stream order). */
 size_t fm_point_pass_scratch_bytes(const fm_point_store* store);
 
 /*
