@@ -463,9 +463,21 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     const int lane = threadIdx.x & 31;
     const int64_t nb = (P + kPairBlock - 1) / kPairBlock;
     const double* part = cpart + (int64_t)c * nb;
+    // all of a lane's partials in flight at once (up to 32 x 16 per batch),
+    // then added in the lane-strided order
+    constexpr int kB = 16;
     double acc = 0;
-#pragma unroll 4
-    for (int64_t k = lane; k < nb; k += 32) acc += part[k];
+    for (int64_t k0 = 0; k0 < nb; k0 += 32 * kB) {
+      double v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t k = k0 + lane + 32 * u;
+        v[u] = k < nb ? part[k] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (k0 + lane + 32 * u < nb) acc += v[u];
+    }
     acc = warp_sum(acc);
     if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
     return;
