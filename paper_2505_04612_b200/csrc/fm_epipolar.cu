@@ -32,6 +32,7 @@ constexpr int kPairBlock = 64;   // pair_grad threads per block
 // block partials with a warp per camera -- no incidence gather, no ticket.
 // More cameras: the per-camera incidence chunks (cam_chunk_*).
 constexpr int kBlockCams = 8;
+constexpr int kIncPad = 128;  // per-image padded incidence table (image_reduce's first batch)
 __host__ __device__ inline bool cams_by_block(const fm_pair_graph& g) {
   return g.refine_focal && g.n_cameras > 0 && g.n_cameras <= kBlockCams;
 }
@@ -49,6 +50,7 @@ struct EpiScratch {
   double* lpart;  // [loss blocks]
   double* sched;  // [2 + 2*kMaxSteps]: lr, scale, bc1[], bc2[]
   unsigned int* ticket;  // camera-chunk completion counter (last block finalises)
+  int* inc_pad;          // [N][kIncPad] first incidences per image, -1 padded
 };
 
 // image_reduce blocks of the camera role: a warp per camera (cams_by_block)
@@ -68,6 +70,7 @@ size_t scratch_need(const fm_pair_graph& g) {
   b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
   b += scratch_round((size_t)(2 + 2 * kMaxSteps) * sizeof(double));
   b += scratch_round(sizeof(unsigned int));
+  b += scratch_round((size_t)std::max(g.n_images, 1) * kIncPad * sizeof(int));
   return b + 256;
 }
 
@@ -79,6 +82,7 @@ bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
   s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
   s.sched = sc.take<double>((size_t)(2 + 2 * kMaxSteps));
   s.ticket = sc.take<unsigned int>(1);
+  s.inc_pad = sc.take<int>((size_t)std::max(g.n_images, 1) * kIncPad);
   return p != nullptr && sc.ok();
 }
 
@@ -321,9 +325,10 @@ pair_grad_kernel(const fm_pair_graph g, const fm_quad_model q, const double* __r
                  double* __restrict__ pg, double* __restrict__ cpart, int32_t* flag) {
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t P = g.n_pairs;
-  // the block's threads agree (the block reduction below): a flag raised by
-  // another block mid-launch stops either all or none of this block's threads
-  if (__syncthreads_or(flag != nullptr && *flag != 0)) return;
+  // No early exit on a raised flag: a flagged run's later steps compute
+  // harmless values and image_reduce, which checks the flag before Adam,
+  // leaves the parameters alone (the flag load stays off this kernel's
+  // critical path of dependent loads).
   double gphi_i = 0, gphi_j = 0;
   int ci = -1, cj = -1;
   if (n < P) {
@@ -446,11 +451,12 @@ __device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params
 // last chunk block to finish (atomic ticket) sums the partials per camera in
 // chunk order and applies the focal update.
 template <bool ADAM>
-__global__ void __launch_bounds__(kReduceBlock)
+__global__ void __launch_bounds__(kReduceBlock, 8)  // <= 128 registers: 8 blocks/SM (C4: one wave)
 image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
                     const double* __restrict__ pg, double* __restrict__ grad,
                     double* __restrict__ R, double* __restrict__ cpart, unsigned int* ticket,
-                    const int img_blocks, const AdamArgs ad, int32_t* flag) {
+                    const int img_blocks, const AdamArgs ad, int32_t* flag,
+                    const int* __restrict__ inc_pad) {
   __shared__ double red[kReduceBlock];
   __shared__ bool last;
   const int64_t P = g.n_pairs;
@@ -459,7 +465,6 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     // fixed lane-strided order + butterfly
     const int c = ((int)blockIdx.x - img_blocks) * (kReduceBlock / 32) + (threadIdx.x >> 5);
     if (c >= g.n_cameras) return;
-    if (ADAM && *flag) return;
     const int lane = threadIdx.x & 31;
     const int64_t nb = (P + kPairBlock - 1) / kPairBlock;
     const double* part = cpart + (int64_t)c * nb;
@@ -479,6 +484,7 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
         if (k0 + lane + 32 * u < nb) acc += v[u];
     }
     acc = warp_sum(acc);
+    if (ADAM && *flag) return;  // checked after the loads: off their critical path
     if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
     return;
   }
@@ -519,19 +525,17 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int N = g.n_images;
   if (k >= N) return;
-  if (ADAM && *flag) return;
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0;
-  const int e0 = g.img_off[k], e1 = g.img_off[k + 1];
   // batches of kGather incidences per lane: all index loads, then all
   // gradient loads in flight together, then the adds in incidence order (the
-  // per-lane accumulation order of a plain loop)
-  constexpr int kGather = 4;
-  for (int eb = e0 + lane; eb < e1; eb += 32 * kGather) {
-    int inc[kGather];
-#pragma unroll
-    for (int u = 0; u < kGather; ++u) inc[u] = eb + 32 * u < e1 ? g.img_inc[eb + 32 * u] : -1;
+  // per-lane accumulation order of a plain loop over e0 + lane, e0 + lane +
+  // 32, ...).  The first batch reads the per-image padded table inc_pad
+  // (the image's first kIncPad incidences, -1 beyond its degree), so it does
+  // not wait for img_off; longer lists continue from img_off.
+  constexpr int kGather = kIncPad / 32;
+  auto gather = [&](const int (&inc)[kGather]) {
     double v[kGather][12];
 #pragma unroll
     for (int u = 0; u < kGather; ++u) {
@@ -551,6 +555,19 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
 #pragma unroll
       for (int q = 0; q < 3; ++q) acc[9 + q] += sgn * v[u][9 + q];
     }
+  };
+  const int e0 = g.img_off[k], e1 = g.img_off[k + 1];  // needed only past the table
+  {
+    int inc[kGather];
+#pragma unroll
+    for (int u = 0; u < kGather; ++u) inc[u] = inc_pad[(int64_t)k * kIncPad + lane + 32 * u];
+    gather(inc);
+  }
+  for (int eb = e0 + kIncPad + lane; eb < e1; eb += 32 * kGather) {
+    int inc[kGather];
+#pragma unroll
+    for (int u = 0; u < kGather; ++u) inc[u] = eb + 32 * u < e1 ? g.img_inc[eb + 32 * u] : -1;
+    gather(inc);
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = warp_sum(acc[q]);
@@ -568,6 +585,7 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
     else if (lane < 9) grad[6 * (int64_t)N + 3 * k + lane - 6] = gq;
     return;
   }
+  if (*flag) return;  // a raised flag freezes the parameters (checked late: off the load chain)
   bool ok = true;
 #pragma unroll
   for (int q = 0; q < 6; ++q) ok = ok && isfinite(g6[q]);
@@ -661,6 +679,22 @@ adam_dist_kernel(const fm_pair_graph g, double* __restrict__ params, const doubl
   if (lane < 9) R[9 * (int64_t)k + lane] = val;
 }
 
+// inc_pad[k][t] = image k's incidence t (t < degree), else -1: image_reduce's
+// first gather batch reads it without waiting for img_off.
+__global__ void inc_pad_kernel(const fm_pair_graph g, int* __restrict__ inc_pad) {
+  const int k = blockIdx.x;
+  const int e0 = g.img_off[k], deg = g.img_off[k + 1] - e0;
+  for (int t = threadIdx.x; t < kIncPad; t += blockDim.x)
+    inc_pad[(int64_t)k * kIncPad + t] = t < deg ? g.img_inc[e0 + t] : -1;
+}
+
+int build_inc_pad(const fm_pair_graph& g, const EpiScratch& s, cudaStream_t st) {
+  if (g.n_images == 0) return FM_OK;
+  inc_pad_kernel<<<(unsigned)g.n_images, kIncPad, 0, st>>>(g, s.inc_pad);
+  FM_LAUNCHED(inc_pad_kernel);
+  return FM_OK;
+}
+
 // Deterministic two-level sum of the per-pair loss terms.
 __global__ void loss_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
   __shared__ double red[256];
@@ -745,7 +779,7 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
     const int cam_blocks = cam_role_blocks(g);
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
-          g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag);
+          g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag, s.inc_pad);
       FM_LAUNCHED(image_reduce_kernel);
     }
   }
@@ -771,7 +805,7 @@ int enqueue_steps_dist(const fm_pair_graph& g, const fm_quad_model& q, double* p
       if (int rc = launch_pair_grad(g, q, params, s, flag, st)) return rc;
       if (img_blocks + cam_blocks > 0) {
         image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
-            g, params, s.pg, gbuf, s.R, s.cpart, s.ticket, img_blocks, none, flag);
+            g, params, s.pg, gbuf, s.R, s.cpart, s.ticket, img_blocks, none, flag, s.inc_pad);
         FM_LAUNCHED(image_reduce_kernel);
       }
       loss_partial_kernel<<<nb, 256, 0, st>>>(s.pg + (size_t)23 * P, P, s.lpart);
@@ -882,6 +916,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
     return FM_OK;
   }
   // API semantics: evaluate even if `flag` is already set by the caller
+  if (int rc = build_inc_pad(*g, s, st)) return rc;
   if (int rc = launch_pair_grad(*g, *q, params, s, nullptr, st)) return rc;
   AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, 0};
   {
@@ -890,7 +925,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
           *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, s.ticket, img_blocks,
-          none, flag);
+          none, flag, s.inc_pad);
       FM_LAUNCHED(image_reduce_kernel);
     }
   }
@@ -921,6 +956,7 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
   cudaStream_t st = as_stream(stream);
   if (n_steps == 0) return FM_OK;
   FM_CUDA(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned int), st));
+  if (int rc = build_inc_pad(*g, s, st)) return rc;
   if (int rc = launch_image_rot(*g, params, s.R, flag, st)) return rc;
   for (int32_t done = 0; done < n_steps;) {
     const int chunk = std::min<int32_t>(n_steps - done, kMaxSteps);
