@@ -287,10 +287,11 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q,
 /*
  * Sharded form of fm_epi_adam_steps: `g` / `q` hold this rank's
  * contiguous range of image pairs (global image / camera indexing); per step
- * the local packed gradient and loss go to grad_buf [9N + C + 1], one
+ * the local packed gradient goes to grad_buf [9N + C] and the finiteness of
+ * the local loss terms to grad_buf[9N + C] (0 or NaN), one
  * ncclAllReduce(sum) over `nccl_comm` (an ncclComm_t from fm_nccl_comm_init;
  * NULL = one rank) and the replicated Adam step (ref/optim.py:24-36) with
- * the loss check of ref/epipolar.py:306-307.  Every rank passes the same
+ * the loss check of ref/epipolar.py:306-307 on every rank.  Every rank passes the same
  * params / adam_m / adam_v values and ends with the same results.  With
  * use_graph the chunk, collective included, is one cached CUDA graph.
  */

@@ -456,7 +456,7 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
                     const double* __restrict__ pg, double* __restrict__ grad,
                     double* __restrict__ R, double* __restrict__ cpart, unsigned int* ticket,
                     const int img_blocks, const AdamArgs ad, int32_t* flag,
-                    const int* __restrict__ inc_pad) {
+                    const int* __restrict__ inc_pad, double* __restrict__ nonfinite_out) {
   __shared__ double red[kReduceBlock];
   __shared__ bool last;
   const int64_t P = g.n_pairs;
@@ -583,6 +583,10 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
   if (!ADAM) {
     if (lane < 6) grad[6 * (int64_t)k + lane] = gq;
     else if (lane < 9) grad[6 * (int64_t)N + 3 * k + lane - 6] = gq;
+    // sharded step: this rank's pair_grad saw a non-finite loss term -> a NaN
+    // in the all-reduced buffer makes every rank raise the loss error
+    if (nonfinite_out && k == 0 && lane == 0)
+      *nonfinite_out = *flag == FM_ERR_NONFINITE_LOSS ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
     return;
   }
   if (*flag) return;  // a raised flag freezes the parameters (checked late: off the load chain)
@@ -779,7 +783,7 @@ int enqueue_steps(const fm_pair_graph& g, const fm_quad_model& q, double* params
     const int cam_blocks = cam_role_blocks(g);
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<true><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
-          g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag, s.inc_pad);
+          g, params, s.pg, nullptr, s.R, s.cpart, s.ticket, img_blocks, ad, flag, s.inc_pad, nullptr);
       FM_LAUNCHED(image_reduce_kernel);
     }
   }
@@ -798,20 +802,18 @@ int enqueue_steps_dist(const fm_pair_graph& g, const fm_quad_model& q, double* p
   const size_t n_grad = (size_t)9 * N + n_cam;
   const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
   const int cam_blocks = cam_role_blocks(g);
-  const int nb = loss_blocks(P);
   for (int step = 0; step < n_steps; ++step) {
     AdamArgs none{nullptr, nullptr, 0, 0, 0, s.sched, step};
     if (P > 0) {
       if (int rc = launch_pair_grad(g, q, params, s, flag, st)) return rc;
+      // the loss slot gbuf[n_grad] carries only its finiteness (0 or NaN,
+      // written by image_reduce): the step needs no loss value
       if (img_blocks + cam_blocks > 0) {
         image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
-            g, params, s.pg, gbuf, s.R, s.cpart, s.ticket, img_blocks, none, flag, s.inc_pad);
+            g, params, s.pg, gbuf, s.R, s.cpart, s.ticket, img_blocks, none, flag, s.inc_pad,
+            gbuf + n_grad);
         FM_LAUNCHED(image_reduce_kernel);
       }
-      loss_partial_kernel<<<nb, 256, 0, st>>>(s.pg + (size_t)23 * P, P, s.lpart);
-      FM_LAUNCHED(loss_partial_kernel);
-      loss_final_kernel<<<1, 32, 0, st>>>(s.lpart, nb, gbuf + n_grad);
-      FM_LAUNCHED(loss_final_kernel);
     } else {  // a rank without pairs contributes zeros
       FM_CUDA(cudaMemsetAsync(gbuf, 0, (n_grad + 1) * sizeof(double), st));
     }
@@ -925,7 +927,7 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
     if (img_blocks + cam_blocks > 0) {
       image_reduce_kernel<false><<<(unsigned)(img_blocks + cam_blocks), kReduceBlock, 0, st>>>(
           *g, const_cast<double*>(params), s.pg, grad_out, s.R, s.cpart, s.ticket, img_blocks,
-          none, flag, s.inc_pad);
+          none, flag, s.inc_pad, nullptr);
       FM_LAUNCHED(image_reduce_kernel);
     }
   }
