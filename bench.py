@@ -884,9 +884,31 @@ def nccl_one_rank_bench(args, scene, store, graph, ids, device, stream):
                 times.append(time.perf_counter() - t0)
     finally:
         comm.close()
-    return {"irls_refine_nccl1_s": times[-1], "irls_nccl1_l1_history": l1h,
-            "nccl1_note": "ShardedIrlsEngine, one shard, one-rank NCCL communicator: the "
-                          "multi-GPU step graph (gradient -> ncclAllReduce -> Adam)"}
+    out = {"irls_refine_nccl1_s": times[-1], "irls_nccl1_l1_history": l1h,
+           "nccl1_note": "ShardedIrlsEngine, one shard, one-rank NCCL communicator: the "
+                         "multi-GPU step graph (gradient -> ncclAllReduce -> Adam)"}
+    # the fused peer-exchange step (reduce + exchange + Adam in one kernel)
+    # over a one-rank group
+    comm = P_.PeerComm.local_group(graph.struct(), 1, device)[0]
+    try:
+        with torch.cuda.stream(stream):
+            times, l1h = [], None
+            for _ in range(2):
+                store.reset_active()
+                params = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
+                eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params, args.cfg,
+                                           comm=comm)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                l1h = eng.run()
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+    finally:
+        comm.close()
+    out.update({"irls_refine_peer1_s": times[-1], "irls_peer1_l1_history": l1h,
+                "peer1_note": "ShardedIrlsEngine, one shard, PeerComm: pair_grad + the fused "
+                              "reduce / peer exchange / Adam kernel per step"})
+    return out
 
 
 def sharded_irls_bench(spec, args, device, stream, world, rank):
@@ -913,9 +935,33 @@ def sharded_irls_bench(spec, args, device, stream, world, rank):
         graph = PairGraph(ii[lo:hi], jj[lo:hi], zeros, zeros, len(ids), 1, True, device=device)
         del sc
         params = torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids), device=device)
-        # NCCL: our own communicator, the Adam chunk (gradient, ncclAllReduce,
-        # Adam) one CUDA graph; gloo (functional runs on one GPU): torch's
-        comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
+        # NCCL backend (one GPU per rank): the fused peer-memory exchange
+        # (PeerComm over CUDA IPC), falling back to our NCCL communicator
+        # (gradient, ncclAllReduce, Adam in one graph) if the peer exchange
+        # fails; gloo (functional runs on one GPU): torch's collectives
+        note = ""
+        comm = None
+        if dist.get_backend() == "nccl":
+            try:
+                comm = P_.PeerComm.from_process_group(graph.struct(), device)
+                eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params,
+                                           args.cfg, comm=comm)
+                eng.run()  # warm-up: graph captures of the step chunks
+            except Exception as exc:  # noqa: BLE001 - reported in the line
+                note = f"peer exchange failed ({type(exc).__name__}: {exc}); NCCL used"
+                if comm is not None:
+                    comm.close()
+                comm = None
+            ok = torch.tensor([1.0 if comm is not None else 0.0], device=device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() < 1.0 and comm is not None:
+                comm.close()
+                comm = None
+            store.reset_active()
+            params.copy_(torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids),
+                                         device=device))
+        if comm is None:
+            comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
         eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params, args.cfg,
                                    comm=comm)
         eng.run()  # warm-up: graph captures of the step chunks
@@ -931,7 +977,7 @@ def sharded_irls_bench(spec, args, device, stream, world, rank):
     out = {"irls_refine_sharded_s": max_over_ranks(dt, device, world),
            "irls_sharded_l1_history": l1h, "irls_sharded_over_ranks": world,
            "irls_sharded_pairs_rank0": hi - lo,
-           "irls_sharded_comm": type(comm).__name__}
+           "irls_sharded_comm": type(comm).__name__ + (f" ({note})" if note else "")}
     if hasattr(comm, "close"):
         comm.close()
     return out

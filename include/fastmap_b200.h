@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 4
+#define FM_ABI_VERSION 5
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -301,6 +301,53 @@ int fm_epi_adam_steps_nccl(const fm_pair_graph* g, const fm_quad_model* q,
                            double beta2, double eps, double scale, int32_t* flag,
                            void* nccl_comm, double* grad_buf, int32_t use_graph,
                            void* scratch, size_t scratch_bytes, void* stream);
+
+/*
+ * The sharded step with its all-reduce FUSED into the reduce kernel over
+ * peer memory: every rank runs it at the same time on its own
+ * shard.  Per step pair_grad, then one kernel whose blocks write their local
+ * packed-gradient components to this rank's exchange buffer, publish a step
+ * id on their ready flag, wait for the same block of every peer, sum the
+ * ranks' components in rank order (the same sum everywhere) and apply Adam
+ * (ref/optim.py:24-36) -- no separate collective, no grid barrier.  part[r]
+ * / ready[r] are device pointers to rank r's buffers (peer memory mapped
+ * with fm_ipc_open_handle, or plain device memory for ranks sharing a GPU);
+ * the two pointer arrays themselves live in device memory.  Exchange
+ * buffers hold 2 * fm_peer_part_len doubles, flag arrays fm_peer_flag_len
+ * u64 (zeroed once); epoch = steps this group completed before the call.
+ * At most 8 refined cameras.  A peer that never arrives raises FM_ERR_CUDA
+ * after ~1 s of waiting instead of hanging.
+ */
+typedef struct fm_peer_group {
+  int32_t n_ranks;
+  int32_t rank;
+  double* const* part;
+  unsigned long long* const* ready;
+  int64_t epoch;
+  int32_t max_blocks;  /* cap on the kernel's blocks (0: what is resident); ranks sharing a GPU */
+  int32_t system_scope; /* 1: peers on other GPUs (system-scope release/acquire); 0: one GPU */
+} fm_peer_group;
+
+size_t fm_peer_part_len(const fm_pair_graph* g);
+size_t fm_peer_flag_len(const fm_pair_graph* g);
+int fm_epi_adam_steps_peer(const fm_pair_graph* g, const fm_quad_model* q,
+                           double* params, double* adam_m, double* adam_v,
+                           int64_t t0, int32_t n_steps, double lr, double beta1,
+                           double beta2, double eps, double scale, int32_t* flag,
+                           const fm_peer_group* group, int32_t use_graph,
+                           void* scratch, size_t scratch_bytes, void* stream);
+
+/* This rank's exchange buffers (cudaMalloc, zeroed): *part [2][part_doubles]
+ * doubles, *ready [n_flags] u64 -- whole allocations, so they can be shared
+ * with fm_ipc_get_handle. */
+int fm_peer_buffers_alloc(size_t part_doubles, size_t n_flags, double** part,
+                          unsigned long long** ready);
+int fm_peer_buffers_free(double* part, unsigned long long* ready);
+/* CUDA IPC of exchange buffers between the ranks' processes (64-byte
+ * handles, exchanged out of band). */
+int fm_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int fm_ipc_open_handle(const void* handle, void** dev_ptr_out);
+int fm_ipc_close_handle(void* dev_ptr);
 
 /* Drop every CUDA graph cached by fm_epi_adam_steps (use_graph != 0). */
 void fm_release_cached_graphs(void);

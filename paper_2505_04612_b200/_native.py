@@ -44,7 +44,7 @@ FM_QUAD_MOM64 = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
-ABI_VERSION = 4
+ABI_VERSION = 5
 _F64 = ctypes.c_double
 _SZ = ctypes.c_size_t
 
@@ -79,6 +79,11 @@ class QuadModel(ctypes.Structure):
                 ("w81", _P), ("mom64", _P)]
 
 
+class PeerGroup(ctypes.Structure):
+    _fields_ = [("n_ranks", _I32), ("rank", _I32), ("part", _P), ("ready", _P), ("epoch", _I64),
+                ("max_blocks", _I32), ("system_scope", _I32)]
+
+
 class DirGraph(ctypes.Structure):
     _fields_ = [("n_nodes", _I32), ("n_edges", _I64), ("edge_i", _P), ("edge_j", _P),
                 ("dirs", _P), ("node_off", _P), ("node_inc", _P)]
@@ -109,6 +114,17 @@ SIGNATURES = {
     "fm_epi_adam_steps_nccl": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel),
                                               _P, _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64,
                                               _P, _P, _P, _I32, _P, _SZ, _P]),
+    "fm_peer_part_len": (_SZ, [ctypes.POINTER(PairGraph)]),
+    "fm_peer_flag_len": (_SZ, [ctypes.POINTER(PairGraph)]),
+    "fm_epi_adam_steps_peer": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel),
+                                              _P, _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64,
+                                              _P, ctypes.POINTER(PeerGroup), _I32, _P, _SZ, _P]),
+    "fm_peer_buffers_alloc": (ctypes.c_int, [_SZ, _SZ, ctypes.POINTER(ctypes.c_void_p),
+                                             ctypes.POINTER(ctypes.c_void_p)]),
+    "fm_peer_buffers_free": (ctypes.c_int, [_P, _P]),
+    "fm_ipc_get_handle": (ctypes.c_int, [_P, _P]),
+    "fm_ipc_open_handle": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
+    "fm_ipc_close_handle": (ctypes.c_int, [_P]),
     "fm_release_cached_graphs": (None, []),
     "fm_nccl_available": (ctypes.c_int, []),
     "fm_nccl_unique_id": (ctypes.c_int, [_P]),

@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -133,6 +134,45 @@ int fm_nccl_allgather_f64(const double* send, double* recv, int64_t n, void* com
   FM_REQUIRE(a, "NCCL (libnccl.so.2) could not be loaded");
   FM_NCCL(a->all_gather(send, recv, (size_t)n, ncclFloat64, static_cast<ncclComm_t>(comm), st),
           "ncclAllGather");
+  return FM_OK;
+}
+
+int fm_peer_buffers_alloc(size_t part_doubles, size_t n_flags, double** part, unsigned long long** ready) {
+  FM_REQUIRE(part && ready, "null output pointers");
+  *part = nullptr;
+  *ready = nullptr;
+  FM_CUDA(cudaMalloc(reinterpret_cast<void**>(part), std::max<size_t>(2 * part_doubles, 1) * sizeof(double)));
+  FM_CUDA(cudaMalloc(reinterpret_cast<void**>(ready), std::max<size_t>(n_flags, 1) * sizeof(unsigned long long)));
+  FM_CUDA(cudaMemset(*part, 0, std::max<size_t>(2 * part_doubles, 1) * sizeof(double)));
+  FM_CUDA(cudaMemset(*ready, 0, std::max<size_t>(n_flags, 1) * sizeof(unsigned long long)));
+  return FM_OK;
+}
+
+int fm_peer_buffers_free(double* part, unsigned long long* ready) {
+  if (part) FM_CUDA(cudaFree(part));
+  if (ready) FM_CUDA(cudaFree(ready));
+  return FM_OK;
+}
+
+int fm_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  FM_REQUIRE(dev_ptr && handle_out, "null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  FM_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  memcpy(handle_out, &h, sizeof(h));
+  return FM_OK;
+}
+
+int fm_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  FM_REQUIRE(handle && dev_ptr_out, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  FM_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return FM_OK;
+}
+
+int fm_ipc_close_handle(void* dev_ptr) {
+  if (dev_ptr) FM_CUDA(cudaIpcCloseMemHandle(dev_ptr));
   return FM_OK;
 }
 

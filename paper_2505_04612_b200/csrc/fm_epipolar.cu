@@ -48,7 +48,7 @@ struct EpiScratch {
   double* pg;     // [kPG][P]
   double* cpart;  // [n_cam_chunks] or [n_cameras][pair blocks] (cams_by_block)
   double* lpart;  // [loss blocks]
-  double* sched;  // [2 + 2*kMaxSteps]: lr, scale, bc1[], bc2[]
+  double* sched;  // [2 + 2*kMaxSteps + 1]: lr, scale, bc1[], bc2[], peer-step epoch
   unsigned int* ticket;  // camera-chunk completion counter (last block finalises)
   int* inc_pad;          // [N][kIncPad] first incidences per image, -1 padded
 };
@@ -68,7 +68,7 @@ size_t scratch_need(const fm_pair_graph& g) {
   b += scratch_round((size_t)g.n_pairs * kPG * sizeof(double));
   b += scratch_round(cpart_len(g) * sizeof(double));
   b += scratch_round((size_t)loss_blocks(g.n_pairs) * sizeof(double));
-  b += scratch_round((size_t)(2 + 2 * kMaxSteps) * sizeof(double));
+  b += scratch_round((size_t)(3 + 2 * kMaxSteps) * sizeof(double));
   b += scratch_round(sizeof(unsigned int));
   b += scratch_round((size_t)std::max(g.n_images, 1) * kIncPad * sizeof(int));
   return b + 256;
@@ -80,7 +80,7 @@ bool carve(const fm_pair_graph& g, void* p, size_t n, EpiScratch& s) {
   s.pg = sc.take<double>((size_t)g.n_pairs * kPG);
   s.cpart = sc.take<double>(cpart_len(g));
   s.lpart = sc.take<double>((size_t)loss_blocks(g.n_pairs));
-  s.sched = sc.take<double>((size_t)(2 + 2 * kMaxSteps));
+  s.sched = sc.take<double>((size_t)(3 + 2 * kMaxSteps));
   s.ticket = sc.take<unsigned int>(1);
   s.inc_pad = sc.take<int>((size_t)std::max(g.n_images, 1) * kIncPad);
   return p != nullptr && sc.ok();
@@ -442,98 +442,50 @@ __device__ void cam_finalise(const fm_pair_graph& g, double* __restrict__ params
   }
 }
 
-// One launch, two roles.  Blocks [0, img_blocks): warp per image --
-// fixed-order gather of the image's incidences, 6D VJP (every lane computes it
-// redundantly from the butterfly-reduced totals), then either the packed
-// gradient (API) or Adam with lane q updating parameter q, and the new
-// rotation.  Blocks [img_blocks, ..): one block per camera chunk --
-// fixed-order partial sum of focal gradients (ref/epipolar.py:194-196); the
-// last chunk block to finish (atomic ticket) sums the partials per camera in
-// chunk order and applies the focal update.
-template <bool ADAM>
-__global__ void __launch_bounds__(kReduceBlock, 8)  // <= 128 registers: 8 blocks/SM (C4: one wave)
-image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
-                    const double* __restrict__ pg, double* __restrict__ grad,
-                    double* __restrict__ R, double* __restrict__ cpart, unsigned int* ticket,
-                    const int img_blocks, const AdamArgs ad, int32_t* flag,
-                    const int* __restrict__ inc_pad, double* __restrict__ nonfinite_out) {
-  __shared__ double red[kReduceBlock];
-  __shared__ bool last;
+// ---- image_reduce building blocks (shared with the peer-exchange kernel)
+
+// Camera c's focal gradient from pair_grad's per-block partials cpart[c][..]:
+// a fixed lane-strided order + butterfly (every lane returns the sum).  All
+// of a lane's partials are in flight at once (up to 32 x 16 per batch).
+__device__ __forceinline__ double cam_block_sum(const fm_pair_graph& g, const double* __restrict__ cpart,
+                                                int c, int lane) {
   const int64_t P = g.n_pairs;
-  if ((int)blockIdx.x >= img_blocks && cams_by_block(g)) {  // ---- camera role, few cameras
-    // warp per camera: pair_grad's block partials cpart[c][0 .. nb) in a
-    // fixed lane-strided order + butterfly
-    const int c = ((int)blockIdx.x - img_blocks) * (kReduceBlock / 32) + (threadIdx.x >> 5);
-    if (c >= g.n_cameras) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t nb = (P + kPairBlock - 1) / kPairBlock;
-    const double* part = cpart + (int64_t)c * nb;
-    // all of a lane's partials in flight at once (up to 32 x 16 per batch),
-    // then added in the lane-strided order
-    constexpr int kB = 16;
-    double acc = 0;
-    for (int64_t k0 = 0; k0 < nb; k0 += 32 * kB) {
-      double v[kB];
+  const int64_t nb = (P + kPairBlock - 1) / kPairBlock;
+  const double* part = cpart + (int64_t)c * nb;
+  constexpr int kB = 16;
+  double acc = 0;
+  for (int64_t k0 = 0; k0 < nb; k0 += 32 * kB) {
+    double v[kB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int64_t k = k0 + lane + 32 * u;
-        v[u] = k < nb ? part[k] : 0.0;
-      }
+    for (int u = 0; u < kB; ++u) {
+      const int64_t k = k0 + lane + 32 * u;
+      v[u] = k < nb ? part[k] : 0.0;
+    }
 #pragma unroll
-      for (int u = 0; u < kB; ++u)
-        if (k0 + lane + 32 * u < nb) acc += v[u];
-    }
-    acc = warp_sum(acc);
-    if (ADAM && *flag) return;  // checked after the loads: off their critical path
-    if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
-    return;
+    for (int u = 0; u < kB; ++u)
+      if (k0 + lane + 32 * u < nb) acc += v[u];
   }
-  if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
-    const int c = blockIdx.x - img_blocks;
-    // a raised flag skips the work but never the ticket: every chunk block
-    // counts, so the last one always re-arms it (the flag can be raised by
-    // image blocks of this same launch)
-    const bool skip = ADAM && *flag;
-    double acc = 0;
-    const int lo = g.cam_chunk_lo[c], hi = skip ? lo : g.cam_chunk_lo[c + 1];
-    // unrolled: the two dependent loads of several incidences in flight
-    // together (same per-thread accumulation order)
-#pragma unroll 8
-    for (int e = lo + threadIdx.x; e < hi; e += kReduceBlock) {
-      const int inc = g.cam_inc[e];
-      acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
-    }
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int st = kReduceBlock / 2; st > 0; st >>= 1) {
-      if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      cpart[c] = red[0];
-      __threadfence();
-      last = atomicAdd(ticket, 1u) == (unsigned)(gridDim.x - img_blocks - 1);
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (!(ADAM && *(volatile int32_t*)flag)) cam_finalise<ADAM>(g, params, R, cpart, grad, ad, flag);
-    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next step
-    return;
-  }
-  const int lane = threadIdx.x & 31;
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int N = g.n_images;
-  if (k >= N) return;
+  return warp_sum(acc);
+}
+
+// Image k's packed-gradient component owned by this lane (lanes 0..5: the 6D
+// rotation parameters, 6..8: the centre) and whether the image's gradient is
+// finite (ref/optim.py:28-29).  Fixed-order gather of the image's incidences
+// (batches of kGather per lane: all index loads, then all gradient loads in
+// flight, then the adds in incidence order -- the order of a plain loop over
+// e0 + lane, e0 + lane + 32, ...; the first batch from the padded table
+// inc_pad, so it does not wait for img_off), butterfly sums, 6D VJP.
+struct ImageGrad {
+  double gq;
+  bool ok;
+};
+__device__ __forceinline__ ImageGrad image_grad(const fm_pair_graph& g, const double* __restrict__ params,
+                                                const double* __restrict__ pg,
+                                                const int* __restrict__ inc_pad, int k, int lane) {
+  const int64_t P = g.n_pairs;
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0;
-  // batches of kGather incidences per lane: all index loads, then all
-  // gradient loads in flight together, then the adds in incidence order (the
-  // per-lane accumulation order of a plain loop over e0 + lane, e0 + lane +
-  // 32, ...).  The first batch reads the per-image padded table inc_pad
-  // (the image's first kIncPad incidences, -1 beyond its degree), so it does
-  // not wait for img_off; longer lists continue from img_off.
   constexpr int kGather = kIncPad / 32;
   auto gather = [&](const int (&inc)[kGather]) {
     double v[kGather][12];
@@ -575,30 +527,26 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
 #pragma unroll
   for (int q = 0; q < 6; ++q) vcur[q] = params[6 * (int64_t)k + q];
   rot6d_vjp(vcur, acc, g6);
-  // gradient component owned by this lane (lanes 0..8 own the 9 image params)
-  double gq = acc[9];
+  ImageGrad r;
+  r.gq = acc[9];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) gq = lane == q ? g6[q] : gq;
-  gq = lane == 7 ? acc[10] : (lane == 8 ? acc[11] : gq);
-  if (!ADAM) {
-    if (lane < 6) grad[6 * (int64_t)k + lane] = gq;
-    else if (lane < 9) grad[6 * (int64_t)N + 3 * k + lane - 6] = gq;
-    // sharded step: this rank's pair_grad saw a non-finite loss term -> a NaN
-    // in the all-reduced buffer makes every rank raise the loss error
-    if (nonfinite_out && k == 0 && lane == 0)
-      *nonfinite_out = *flag == FM_ERR_NONFINITE_LOSS ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
-    return;
-  }
-  if (*flag) return;  // a raised flag freezes the parameters (checked late: off the load chain)
-  bool ok = true;
+  for (int q = 0; q < 6; ++q) r.gq = lane == q ? g6[q] : r.gq;
+  r.gq = lane == 7 ? acc[10] : (lane == 8 ? acc[11] : r.gq);
+  r.ok = true;
 #pragma unroll
-  for (int q = 0; q < 6; ++q) ok = ok && isfinite(g6[q]);
+  for (int q = 0; q < 6; ++q) r.ok = r.ok && isfinite(g6[q]);
 #pragma unroll
-  for (int q = 0; q < 3; ++q) ok = ok && isfinite(acc[9 + q]);
-  if (!ok) {
-    if (lane == 0) raise_flag(flag, FM_ERR_NONFINITE_GRAD);
-    return;
-  }
+  for (int q = 0; q < 3; ++q) r.ok = r.ok && isfinite(acc[9 + q]);
+  return r;
+}
+
+// Adam on image k's nine parameters (lane q: parameter q, the numpy
+// expression order) and its new rotation (lanes 0..5 feed rot6d_to_R).
+// Whole warp.
+__device__ __forceinline__ void image_adam(const fm_pair_graph& g, double* __restrict__ params,
+                                           double* __restrict__ R, const AdamArgs& ad, int32_t* flag,
+                                           int k, int lane, double gq) {
+  const int N = g.n_images;
   const double lr = ad.sched[0];
   const double bc1 = ad.sched[2 + ad.step], bc2 = ad.sched[2 + kMaxSteps + ad.step];
   double newp = 0.0;
@@ -620,6 +568,224 @@ image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
 #pragma unroll
   for (int q = 1; q < 9; ++q) val = lane == q ? Rk[q] : val;
   if (lane < 9) R[9 * (int64_t)k + lane] = val;
+}
+
+// One launch, two roles.  Blocks [0, img_blocks): warp per image --
+// image_grad (fixed-order gather, butterflies, 6D VJP), then either the
+// packed gradient (API) or Adam with lane q updating parameter q and the new
+// rotation (image_adam).  Blocks [img_blocks, ..): the focal gradients --
+// with few cameras a warp per camera over pair_grad's block partials
+// (cam_block_sum); otherwise a block per camera chunk, fixed-order partial
+// sums, and the last chunk block to finish (atomic ticket) sums the partials
+// per camera in chunk order and applies the focal update
+// (ref/epipolar.py:194-196).
+template <bool ADAM>
+__global__ void __launch_bounds__(kReduceBlock, 8)  // <= 128 registers: 8 blocks/SM (C4: one wave)
+image_reduce_kernel(const fm_pair_graph g, double* __restrict__ params,
+                    const double* __restrict__ pg, double* __restrict__ grad,
+                    double* __restrict__ R, double* __restrict__ cpart, unsigned int* ticket,
+                    const int img_blocks, const AdamArgs ad, int32_t* flag,
+                    const int* __restrict__ inc_pad, double* __restrict__ nonfinite_out) {
+  __shared__ double red[kReduceBlock];
+  __shared__ bool last;
+  const int64_t P = g.n_pairs;
+  if ((int)blockIdx.x >= img_blocks && cams_by_block(g)) {  // ---- camera role, few cameras
+    const int c = ((int)blockIdx.x - img_blocks) * (kReduceBlock / 32) + (threadIdx.x >> 5);
+    if (c >= g.n_cameras) return;
+    const int lane = threadIdx.x & 31;
+    const double acc = cam_block_sum(g, cpart, c, lane);
+    if (ADAM && *flag) return;  // checked after the loads: off their critical path
+    if (lane == 0) cam_update<ADAM>(g, params, R + 9 * (int64_t)g.n_images, grad, ad, flag, c, acc);
+    return;
+  }
+  if ((int)blockIdx.x >= img_blocks) {  // ---- camera chunk role
+    const int c = blockIdx.x - img_blocks;
+    // a raised flag skips the work but never the ticket: every chunk block
+    // counts, so the last one always re-arms it (the flag can be raised by
+    // image blocks of this same launch)
+    const bool skip = ADAM && *flag;
+    double acc = 0;
+    const int lo = g.cam_chunk_lo[c], hi = skip ? lo : g.cam_chunk_lo[c + 1];
+    // unrolled: the two dependent loads of several incidences in flight
+    // together (same per-thread accumulation order)
+#pragma unroll 8
+    for (int e = lo + threadIdx.x; e < hi; e += kReduceBlock) {
+      const int inc = g.cam_inc[e];
+      acc += pg[(21 + (inc & 1)) * P + (inc >> 1)];
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int st = kReduceBlock / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      cpart[c] = red[0];
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == (unsigned)(gridDim.x - img_blocks - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (!(ADAM && *(volatile int32_t*)flag)) cam_finalise<ADAM>(g, params, R, cpart, grad, ad, flag);
+    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next step
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int N = g.n_images;
+  if (k >= N) return;
+  const ImageGrad ig = image_grad(g, params, pg, inc_pad, k, lane);
+  if (!ADAM) {
+    if (lane < 6) grad[6 * (int64_t)k + lane] = ig.gq;
+    else if (lane < 9) grad[6 * (int64_t)N + 3 * k + lane - 6] = ig.gq;
+    // sharded step: this rank's pair_grad saw a non-finite loss term -> a NaN
+    // in the all-reduced buffer makes every rank raise the loss error
+    if (nonfinite_out && k == 0 && lane == 0)
+      *nonfinite_out = *flag == FM_ERR_NONFINITE_LOSS ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
+    return;
+  }
+  if (*flag) return;  // a raised flag freezes the parameters (checked late: off the load chain)
+  if (!ig.ok) {
+    if (lane == 0) raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+    return;
+  }
+  image_adam(g, params, R, ad, flag, k, lane, ig.gq);
+}
+
+// ------------------------------------------------ fused gradient exchange
+// The sharded step's reduce fused with its collective, over peer
+// memory instead of a separate all-reduce: every rank runs this kernel on
+// its own pair shard at the same time.  A logical block (2 images, or 2
+// cameras) computes its local packed-gradient components (image_grad /
+// cam_block_sum, exactly the sharded API path's values), writes them to its
+// rank's exchange buffer, publishes the step id on its own ready flag
+// (st.release.sys), waits until every peer has published the same logical
+// block (ld.acquire.sys), sums the ranks' components in rank order -- the
+// same sum on every rank, so the replicated parameters stay bitwise equal
+// -- and applies Adam.  No grid barrier and no second kernel: blocks
+// synchronise pairwise with their peers.  One physical block per resident
+// slot walks the logical blocks in order (every rank the same order), so
+// the waits cannot deadlock.  Buffers are double-buffered by step parity: a
+// rank can only reach step s+1 after every peer published step s, i.e.
+// finished reading step s-1's buffer.  A non-finite loss term on any rank
+// travels as a NaN marker per logical block; spins are bounded (a peer that
+// never arrives raises FM_ERR_CUDA instead of hanging the GPU).
+// SYS: peers on other GPUs (system scope); else ranks sharing this GPU.
+template <bool SYS>
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  if (SYS) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+template <bool SYS>
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  if (SYS) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct PeerArgs {
+  int n_ranks, rank;
+  double* const* part;             // [n_ranks] exchange buffers [2][n_pub]
+  unsigned long long* const* ready;  // [n_ranks] flag arrays [n_logical]
+  int64_t n_pub;                   // 9N + C + n_logical (components + NaN markers)
+  int sys;                         // peers on other GPUs: system-scope ordering
+};
+
+template <bool SYS>
+__global__ void __launch_bounds__(kReduceBlock, 8)
+image_reduce_peer_kernel(const fm_pair_graph g, double* __restrict__ params,
+                         const double* __restrict__ pg, double* __restrict__ R,
+                         const double* __restrict__ cpart, const int img_blocks, const int n_logical,
+                         const AdamArgs ad, int32_t* flag, const int* __restrict__ inc_pad,
+                         const PeerArgs pa) {
+  __shared__ int marker_bad;
+  const int N = g.n_images;
+  const int n_cam = g.refine_focal ? g.n_cameras : 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned long long step_id = (unsigned long long)ad.sched[2 + 2 * kMaxSteps] + ad.step + 1;
+  const int parity = (int)(step_id & 1);
+  const int local_bad = *flag == FM_ERR_NONFINITE_LOSS;  // this rank's pair terms (pair_grad done)
+  double* mine = pa.part[pa.rank] + parity * pa.n_pub;
+  const int64_t marker0 = (int64_t)9 * N + n_cam;
+  for (int b = blockIdx.x; b < n_logical; b += gridDim.x) {
+    // ---- local components and their slots
+    int64_t slot = -1;  // this lane's published slot (-1: none)
+    double val = 0.0;
+    if (b < img_blocks) {
+      const int k = b * (kReduceBlock / 32) + w;
+      if (k < N) {
+        const ImageGrad ig = image_grad(g, params, pg, inc_pad, k, lane);
+        if (lane < 6) slot = 6 * (int64_t)k + lane;
+        else if (lane < 9) slot = 6 * (int64_t)N + 3 * k + lane - 6;
+        val = ig.gq;
+      }
+    } else {
+      const int c = (b - img_blocks) * (kReduceBlock / 32) + w;
+      if (c < n_cam) {
+        const double acc = cam_block_sum(g, cpart, c, lane);
+        if (lane == 0) {
+          slot = 9 * (int64_t)N + c;
+          val = acc;
+        }
+      }
+    }
+    if (slot >= 0) mine[slot] = val;
+    if (threadIdx.x == 0) mine[marker0 + b] = local_bad ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
+    __syncthreads();
+    // ---- publish, then wait for every peer's same logical block
+    // the release store orders the whole block's writes (cumulative through
+    // the barrier above): no separate system-scope fence
+    if (threadIdx.x == 0) st_release<SYS>(pa.ready[pa.rank] + b, step_id);
+    if ((int)threadIdx.x < pa.n_ranks) {
+      const unsigned long long* f = pa.ready[threadIdx.x] + b;
+      long long spins = 0;
+      while (ld_acquire<SYS>(f) < step_id) {
+        __nanosleep(64);
+        // a peer that never arrives (~1 s) raises FM_ERR_CUDA once; after
+        // that nobody waits any more, so the launch drains instead of hanging
+        if ((++spins & 1023) == 0 &&
+            (*(volatile int32_t*)flag == FM_ERR_CUDA || spins > (1ll << 24))) {
+          atomicCAS(flag, 0, FM_ERR_CUDA);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- rank-order sums (identical on every rank)
+    double tot = 0.0, bad = 0.0;
+    for (int r = 0; r < pa.n_ranks; ++r) {
+      const double* pr = pa.part[r] + parity * pa.n_pub;
+      if (slot >= 0) tot += __ldcv(pr + slot);
+      bad += __ldcv(pr + marker0 + b);
+    }
+    if (threadIdx.x == 0) marker_bad = !(bad == bad) ? 1 : 0;  // NaN marker from some rank
+    __syncthreads();
+    const bool loss_bad = marker_bad != 0;
+    __syncthreads();  // marker_bad is rewritten by the next logical block
+    if (loss_bad) {
+      if (threadIdx.x == 0) raise_flag(flag, FM_ERR_NONFINITE_LOSS);
+      continue;
+    }
+    if (*(volatile int32_t*)flag) continue;  // frozen (every rank alike)
+    if (b < img_blocks) {
+      const int k = b * (kReduceBlock / 32) + w;
+      if (k >= N) continue;
+      // the summed gradient's finiteness decides (ref/optim.py:28-29), as
+      // after the all-reduce of the other sharded paths
+      bool fin = (lane >= 9) || isfinite(tot);
+      fin = __all_sync(0xffffffffu, fin);
+      if (!fin) {
+        if (lane == 0) raise_flag(flag, FM_ERR_NONFINITE_GRAD);
+        continue;
+      }
+      image_adam(g, params, R, ad, flag, k, lane, tot);
+    } else {
+      const int c = (b - img_blocks) * (kReduceBlock / 32) + w;
+      if (c < n_cam && lane == 0) cam_update<true>(g, params, R + 9 * (int64_t)N, nullptr, ad, flag, c, tot);
+    }
+  }
 }
 
 // Replicated Adam of the sharded engine (ref/optim.py:24-36) over the
@@ -829,6 +995,28 @@ int enqueue_steps_dist(const fm_pair_graph& g, const fm_quad_model& q, double* p
   return FM_OK;
 }
 
+// The peer-exchange step: pair_grad, then the fused reduce + exchange + Adam.
+int enqueue_steps_peer(const fm_pair_graph& g, const fm_quad_model& q, double* params, double* m,
+                       double* v, int n_steps, double b1, double b2, double eps, const EpiScratch& s,
+                       int32_t* flag, const PeerArgs& pa, int grid, cudaStream_t st) {
+  const int N = g.n_images;
+  const int img_blocks = (int)ceil_div((int64_t)N * 32, kReduceBlock);
+  const int n_logical = img_blocks + (cams_by_block(g) ? (int)ceil_div(g.n_cameras, 2) : 0);
+  for (int step = 0; step < n_steps; ++step) {
+    if (g.n_pairs > 0)
+      if (int rc = launch_pair_grad(g, q, params, s, flag, st)) return rc;
+    AdamArgs ad{m, v, b1, b2, eps, s.sched, step};
+    if (pa.sys)
+      image_reduce_peer_kernel<true><<<(unsigned)grid, kReduceBlock, 0, st>>>(
+          g, params, s.pg, s.R, s.cpart, img_blocks, n_logical, ad, flag, s.inc_pad, pa);
+    else
+      image_reduce_peer_kernel<false><<<(unsigned)grid, kReduceBlock, 0, st>>>(
+          g, params, s.pg, s.R, s.cpart, img_blocks, n_logical, ad, flag, s.inc_pad, pa);
+    FM_LAUNCHED(image_reduce_peer_kernel);
+  }
+  return FM_OK;
+}
+
 // --------------------------------------------------------------- graph cache
 struct GraphKey {
   std::vector<uintptr_t> k;
@@ -941,14 +1129,33 @@ int fm_epi_loss_grad(const fm_pair_graph* g, const fm_quad_model* q, const doubl
 
 }  // extern "C"
 
+extern "C" size_t fm_peer_part_len(const fm_pair_graph* g);
+
 namespace fm {
 namespace {
+// Physical blocks of the peer kernel: every logical block, capped by what
+// is resident at once (the waits need every block of every rank resident)
+// and by the caller's max_blocks (ranks sharing one GPU in tests).
+int peer_grid(const fm_pair_graph& g, const fm_peer_group* peer) {
+  const int img_blocks = (int)ceil_div((int64_t)g.n_images * 32, kReduceBlock);
+  const int n_logical = img_blocks + (cams_by_block(g) ? (int)ceil_div(g.n_cameras, 2) : 0);
+  static int per_sm = 0;
+  if (!per_sm) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, image_reduce_peer_kernel<true>, kReduceBlock, 0);
+    per_sm = b > 0 ? b : 1;
+  }
+  int grid = std::min(n_logical, per_sm * sm_count());
+  if (peer->max_blocks > 0) grid = std::min(grid, (int)peer->max_blocks);
+  return std::max(grid, 1);
+}
+
 // dist: the sharded step (comm may be NULL = one rank; gbuf [9N + C + 1]).
 int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* params, double* adam_m,
                     double* adam_v, int64_t t0, int32_t n_steps, double lr, double beta1,
                     double beta2, double eps, double scale, int32_t* flag, int32_t use_graph,
                     void* scratch, size_t scratch_bytes, void* stream, bool dist, void* comm,
-                    double* gbuf) {
+                    double* gbuf, const fm_peer_group* peer = nullptr) {
   if (int rc = check_graph(g)) return rc;
   if (int rc = check_quad(q)) return rc;
   FM_REQUIRE(flag, "fm_epi_adam_steps needs a device flag word");
@@ -964,9 +1171,10 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
     const int chunk = std::min<int32_t>(n_steps - done, kMaxSteps);
     // schedule: lr, 2/Z, and the bias corrections 1 - beta^t computed with the
     // host pow() exactly as ref/optim.py:34-35 does
-    std::vector<double> sched(2 + 2 * kMaxSteps, 1.0);
+    std::vector<double> sched(3 + 2 * kMaxSteps, 1.0);
     sched[0] = lr;
     sched[1] = scale;
+    sched[2 + 2 * kMaxSteps] = peer ? (double)(peer->epoch + done) : 0.0;  // peer step ids
     for (int k = 0; k < chunk; ++k) {
       const double t = (double)(t0 + done + k + 1);
       sched[2 + k] = 1.0 - pow(beta1, t);
@@ -975,6 +1183,12 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
     FM_CUDA(cudaMemcpyAsync(s.sched, sched.data(), sched.size() * sizeof(double),
                             cudaMemcpyHostToDevice, st));
     auto enqueue = [&](cudaStream_t cs) {
+      if (peer) {
+        PeerArgs pa{peer->n_ranks, peer->rank, peer->part, peer->ready,
+                    (int64_t)fm_peer_part_len(g), peer->system_scope != 0};
+        return enqueue_steps_peer(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag,
+                                  pa, peer_grid(*g, peer), cs);
+      }
       return dist ? enqueue_steps_dist(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s,
                                        flag, comm, gbuf, cs)
                   : enqueue_steps(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag, cs);
@@ -983,7 +1197,15 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
       if (int rc = enqueue(st)) return rc;
     } else {
       GraphKey key = make_key(*g, *q, params, adam_m, adam_v, chunk, beta1, beta2, eps, s, flag);
-      key.k.push_back(dist ? 1u : 0u);
+      key.k.push_back(dist ? 1u : (peer ? 2u : 0u));
+      if (peer) {
+        key.k.push_back(reinterpret_cast<uintptr_t>(peer->part));
+        key.k.push_back(reinterpret_cast<uintptr_t>(peer->ready));
+        key.k.push_back((uintptr_t)peer->n_ranks);
+        key.k.push_back((uintptr_t)peer->rank);
+        key.k.push_back((uintptr_t)peer->max_blocks);
+        key.k.push_back((uintptr_t)peer->system_scope);
+      }
       key.k.push_back(reinterpret_cast<uintptr_t>(comm));
       key.k.push_back(reinterpret_cast<uintptr_t>(gbuf));
       cudaGraphExec_t exec = nullptr;
@@ -1042,6 +1264,33 @@ int fm_epi_adam_steps_nccl(const fm_pair_graph* g, const fm_quad_model* q, doubl
   FM_REQUIRE(grad_buf, "fm_epi_adam_steps_nccl needs grad_buf [9N + C + 1]");
   return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, scale,
                          flag, use_graph, scratch, scratch_bytes, stream, true, nccl_comm, grad_buf);
+}
+
+size_t fm_peer_part_len(const fm_pair_graph* g) {
+  if (!g) return 0;
+  const int img_blocks = (int)ceil_div((int64_t)g->n_images * 32, kReduceBlock);
+  const int n_logical = img_blocks + (cams_by_block(*g) ? (int)ceil_div(g->n_cameras, 2) : 0);
+  return (size_t)9 * g->n_images + (g->refine_focal ? g->n_cameras : 0) + (size_t)n_logical;
+}
+
+size_t fm_peer_flag_len(const fm_pair_graph* g) {
+  if (!g) return 0;
+  const int img_blocks = (int)ceil_div((int64_t)g->n_images * 32, kReduceBlock);
+  return (size_t)img_blocks + (cams_by_block(*g) ? (size_t)ceil_div(g->n_cameras, 2) : 0);
+}
+
+int fm_epi_adam_steps_peer(const fm_pair_graph* g, const fm_quad_model* q, double* params,
+                           double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
+                           double beta1, double beta2, double eps, double scale, int32_t* flag,
+                           const fm_peer_group* group, int32_t use_graph, void* scratch,
+                           size_t scratch_bytes, void* stream) {
+  FM_REQUIRE(group && group->part && group->ready && group->n_ranks >= 1 &&
+                 group->rank >= 0 && group->rank < group->n_ranks && group->epoch >= 0,
+             "bad peer group");
+  FM_REQUIRE(g && (!g->refine_focal || cams_by_block(*g)),
+             "the peer-exchange step handles at most %d refined cameras", kBlockCams);
+  return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, scale,
+                         flag, use_graph, scratch, scratch_bytes, stream, false, nullptr, nullptr, group);
 }
 
 void fm_release_cached_graphs(void) {

@@ -129,6 +129,126 @@ class NcclComm:
             self.handle = None
 
 
+class PeerComm:
+    """The sharded step's all-reduce fused into its reduce kernel over peer
+    memory (fm_epi_adam_steps_peer): rank r's blocks publish their packed
+    gradient components into r's exchange buffer, wait for the same block of
+    every peer and sum the ranks' components in rank order inside the kernel
+    (no separate collective).  Buffers are whole cudaMalloc allocations
+    (fm_peer_buffers_alloc); across processes their CUDA IPC handles go out
+    through torch.distributed (fm_ipc_get_handle / fm_ipc_open_handle; the
+    peers' memory is then read over NVLink).  ``local_group`` builds several
+    ranks inside one process (tests: ranks sharing one GPU, each driven on
+    its own stream).  The pass scalars still go through ``allreduce_``
+    (torch.distributed), once per prune pass."""
+
+    native = True
+    peer = True
+
+    class _LocalReducer:
+        """Host rendezvous of in-process ranks (one thread each): sum in rank
+        order, the same result for every rank."""
+
+        def __init__(self, world):
+            import threading
+            self.slots = [None] * world
+            self.barrier = threading.Barrier(world, timeout=300)
+
+        def allreduce_(self, rank, t):
+            self.slots[rank] = t.cpu()
+            self.barrier.wait()
+            total = self.slots[0].clone()
+            for x in self.slots[1:]:
+                total += x
+            self.barrier.wait()
+            t.copy_(total)
+            return t
+
+    def __init__(self, graph_struct, rank, world, part_ptrs, ready_ptrs, owned, max_blocks=0,
+                 opened=(), dist_group=None, reducer=None, system_scope=False):
+        self.rank, self.world = rank, world
+        self.part_ptrs = part_ptrs      # int64 device tensor [world]
+        self.ready_ptrs = ready_ptrs    # int64 device tensor [world]
+        self.owned = owned              # (part, ready) pointers this object frees
+        self.opened = list(opened)      # IPC-mapped peer pointers to close
+        self.epoch = 0
+        self.max_blocks = max_blocks
+        self.dist_group = dist_group
+        self.reducer = reducer
+        self.system_scope = system_scope
+        self.handle = None
+
+    @staticmethod
+    def _alloc(gs):
+        lib = N.lib()
+        part, ready = ctypes.c_void_p(), ctypes.c_void_p()
+        N.check(lib.fm_peer_buffers_alloc(lib.fm_peer_part_len(ctypes.byref(gs)),
+                                          lib.fm_peer_flag_len(ctypes.byref(gs)),
+                                          ctypes.byref(part), ctypes.byref(ready)))
+        return part.value, ready.value
+
+    @classmethod
+    def local_group(cls, graph_struct, world, device, max_blocks=0):
+        """`world` ranks in this process (one exchange buffer each)."""
+        bufs = [cls._alloc(graph_struct) for _ in range(world)]
+        parts = torch.tensor([b[0] for b in bufs], dtype=torch.int64, device=device)
+        readies = torch.tensor([b[1] for b in bufs], dtype=torch.int64, device=device)
+        red = cls._LocalReducer(world)
+        return [cls(graph_struct, r, world, parts, readies, bufs[r], max_blocks, reducer=red)
+                for r in range(world)]
+
+    @classmethod
+    def from_process_group(cls, graph_struct, device, group=None):
+        """One rank per process: exchange the buffers' IPC handles."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        lib = N.lib()
+        mine = cls._alloc(graph_struct)
+        hp, hr = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
+        N.check(lib.fm_ipc_get_handle(mine[0], hp))
+        N.check(lib.fm_ipc_get_handle(mine[1], hr))
+        allh = [None] * world
+        dist.all_gather_object(allh, (bytes(hp), bytes(hr)), group=group)
+        parts, readies, opened = [], [], []
+        for r, (a, b) in enumerate(allh):
+            if r == rank:
+                parts.append(mine[0])
+                readies.append(mine[1])
+                continue
+            pa, pb = ctypes.c_void_p(), ctypes.c_void_p()
+            N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(a), ctypes.byref(pa)))
+            N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(b), ctypes.byref(pb)))
+            parts.append(pa.value)
+            readies.append(pb.value)
+            opened += [pa.value, pb.value]
+        return cls(graph_struct, rank, world,
+                   torch.tensor(parts, dtype=torch.int64, device=device),
+                   torch.tensor(readies, dtype=torch.int64, device=device), mine,
+                   opened=opened, dist_group=group, system_scope=True)
+
+    def struct(self):
+        return N.PeerGroup(n_ranks=self.world, rank=self.rank, part=self.part_ptrs.data_ptr(),
+                           ready=self.ready_ptrs.data_ptr(), epoch=self.epoch,
+                           max_blocks=self.max_blocks, system_scope=int(self.system_scope))
+
+    def allreduce_(self, t):
+        import torch.distributed as dist
+        if self.reducer is not None:
+            return self.reducer.allreduce_(self.rank, t)
+        if self.world > 1 and dist.is_initialized():
+            dist.all_reduce(t, group=self.dist_group)
+        return t
+
+    def close(self):
+        lib = N.lib()
+        for ptr in self.opened:
+            N.check(lib.fm_ipc_close_handle(ptr))
+        self.opened = []
+        if self.owned:
+            N.check(lib.fm_peer_buffers_free(*self.owned))
+            self.owned = None
+
+
 class NoComm:
     world, rank = 1, 0
     native = True  # one rank: the native step chunk with a NULL communicator
@@ -205,6 +325,15 @@ class ShardedIrlsEngine:
     def _steps_native(self, t0, n_steps, lr, scale):
         cfg = self.cfg
         sh = self.shards[0]
+        if getattr(self.comm, "peer", False):
+            grp = self.comm.struct()
+            N.check(self.lib.fm_epi_adam_steps_peer(
+                ctypes.byref(sh.graph.struct()), ctypes.byref(sh.buf.quad), N.ptr(self.params),
+                N.ptr(self.m), N.ptr(self.v), t0, n_steps, lr, cfg.adam_beta1, cfg.adam_beta2,
+                cfg.adam_eps, scale, N.ptr(self.aflag), ctypes.byref(grp), 1, N.ptr(sh.gscratch),
+                sh.gscratch.numel(), N.stream_handle()))
+            self.comm.epoch += n_steps
+            return
         if getattr(self, "gbuf", None) is None:
             self.gbuf = torch.zeros(sh.graph.n_params + 1, dtype=torch.float64, device=self.device)
         N.check(self.lib.fm_epi_adam_steps_nccl(
@@ -356,5 +485,6 @@ def gather_blocks(local, b, comm):
     return torch.cat([p[:, :int(b[r + 1] - b[r])] for r, p in enumerate(parts)], dim=1)
 
 
-__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NcclComm", "NoComm", "make_shards",
+__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NcclComm", "PeerComm", "NoComm",
+           "make_shards",
            "init_blocks", "gather_blocks", "multi_init_align_sharded"]

@@ -169,3 +169,68 @@ def test_two_ranks_gloo_one_gpu_matches_reference():
     per_pair = np.array([active[start[k]:start[k + 1]].sum() for k in range(len(lengths))])
     assert np.array_equal(per_pair, g["c1_active_count"])
 
+
+
+def test_peer_exchange_two_ranks_one_gpu_bitwise_sharded_reference(golden_c1):
+    """The fused reduce + exchange + Adam over peer memory
+    (fm_epi_adam_steps_peer): two ranks in this process, each driven by its
+    own thread on its own stream, exchange their blocks' gradient components
+    through each other's buffers inside the kernel.  Both ranks end with the
+    same parameters, bit for bit the two-shard engine that sums the shards'
+    packed gradients in rank order (parallel.ShardedIrlsEngine, two shards,
+    one process), and the reference's decisions / RRA / RTA."""
+    import threading
+    g = golden_c1
+    dev = torch.device("cuda")
+    lengths, ij, x1, x2, p0 = _c1_inputs(g)
+    n = int(ij.max()) + 1
+    cams = np.zeros_like(ij)
+    bounds = P_.partition_pairs(lengths, 2)
+    ref_shards = P_.make_shards(x1, x2, lengths, ij, cams, n, 1, True, bounds, dev)
+    p_ref = torch.as_tensor(p0.copy(), device=dev)
+    ref = P_.ShardedIrlsEngine(ref_shards, p_ref, Cfg())
+    l1_ref = ref.run()
+    shards = P_.make_shards(x1, x2, lengths, ij, cams, n, 1, True, bounds, dev)
+    comms = P_.PeerComm.local_group(shards[0].graph.struct(), 2, dev, max_blocks=64)
+    out = [None, None]
+
+    def worker(r):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            p = torch.as_tensor(p0.copy(), device=dev)
+            eng = P_.ShardedIrlsEngine([shards[r]], p, Cfg(), comm=comms[r])
+            assert eng.native_steps
+            l1 = eng.run()
+            torch.cuda.synchronize()
+            out[r] = (l1, p.cpu().numpy(), eng.dropped, eng.kept)
+
+    errors = []
+
+    def guarded(r):
+        try:
+            worker(r)
+        except BaseException as exc:  # noqa: BLE001 - reported below
+            errors.append(exc)
+            comms[r].reducer.barrier.abort()
+
+    threads = [threading.Thread(target=guarded, args=(r,)) for r in range(2)]
+    try:
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=600)
+    finally:
+        for c in comms:
+            c.close()
+    assert not errors, errors
+    (la, pa, da, ka), (lb, pb, db, kb) = out
+    assert np.array_equal(pa, pb) and la == lb and (da, ka) == (db, kb)
+    assert la == l1_ref
+    assert np.array_equal(pa, p_ref.cpu().numpy())
+    assert [da, ka] == list(g["c1_counts"])
+    rot = O.project_to_so3(O.rot6d_to_matrix(pa[:6 * n].reshape(n, 6)))
+    cen = pa[6 * n:9 * n].reshape(n, 3)
+    ours = O.pose_metrics(rot, cen, g["c1_R_gt"], g["c1_c_gt"])
+    refm = O.pose_metrics(g["c1_R_out"], g["c1_c_out"], g["c1_R_gt"], g["c1_c_gt"])
+    for key in ("RRA@1", "RRA@3", "RTA@1", "RTA@3"):
+        assert ours[key] == refm[key]
