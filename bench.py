@@ -553,16 +553,37 @@ _SCALAR_COMM = {}
 
 
 def scalar_comm(world):
-    """The pass-scalar all-reduce of N > 1 steps: over NCCL our own
-    communicator (the collective on the pass's stream, no cross-stream
-    sync; parallel.NcclComm), over gloo torch.distributed's."""
+    """The pass-scalar all-reduce of N > 1 steps: with the NCCL backend
+    (one GPU per rank) over peer memory (parallel.PeerSum, CUDA IPC), else
+    our NCCL communicator; over gloo torch.distributed's."""
+    import torch
     import torch.distributed as dist
 
     from paper_2505_04612_b200 import parallel as P_
     if world == 1:
         return P_.NoComm()
     if "c" not in _SCALAR_COMM:
-        _SCALAR_COMM["c"] = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
+        comm = None
+        if dist.get_backend() == "nccl":
+            # the scalars over peer memory (one warp: publish, wait, rank-order
+            # sum), NCCL if the peer buffers cannot be shared
+            try:
+                comm = P_.PeerSum.from_process_group(3)
+                probe = torch.zeros(3, dtype=torch.float64, device="cuda")
+                comm.allreduce_(probe)
+                torch.cuda.synchronize()
+                comm.check()
+            except Exception:  # noqa: BLE001 - NCCL below
+                comm = None
+            ok = torch.tensor([1.0 if comm is not None else 0.0], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() < 1.0:
+                comm = None
+            if comm is None:
+                comm = P_.NcclComm()
+        else:
+            comm = P_.TorchComm()
+        _SCALAR_COMM["c"] = comm
     return _SCALAR_COMM["c"]
 
 

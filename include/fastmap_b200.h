@@ -343,6 +343,14 @@ int fm_epi_adam_steps_peer(const fm_pair_graph* g, const fm_quad_model* q,
 int fm_peer_buffers_alloc(size_t part_doubles, size_t n_flags, double** part,
                           unsigned long long** ready);
 int fm_peer_buffers_free(double* part, unsigned long long* ready);
+/* In-place sum of n <= 32 doubles over the ranks of a peer group (the pass
+ * scalars of irls_refine, ref/epipolar.py:282-291, in the sharded step):
+ * one warp publishes vals into this rank's exchange buffer (2 x n doubles,
+ * flag array of 1), waits for every peer and sums in rank order (the same
+ * result everywhere).  group->epoch = exchanges completed before this one;
+ * *err gets FM_ERR_CUDA if a peer never arrives (bounded wait). */
+int fm_peer_sum_f64(double* vals, int32_t n, const fm_peer_group* group, int32_t* err,
+                    void* stream);
 /* CUDA IPC of exchange buffers between the ranks' processes (64-byte
  * handles, exchanged out of band). */
 int fm_ipc_get_handle(const void* dev_ptr, void* handle_out);

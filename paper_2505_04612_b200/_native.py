@@ -122,6 +122,7 @@ SIGNATURES = {
     "fm_peer_buffers_alloc": (ctypes.c_int, [_SZ, _SZ, ctypes.POINTER(ctypes.c_void_p),
                                              ctypes.POINTER(ctypes.c_void_p)]),
     "fm_peer_buffers_free": (ctypes.c_int, [_P, _P]),
+    "fm_peer_sum_f64": (ctypes.c_int, [_P, _I32, ctypes.POINTER(PeerGroup), _P, _P]),
     "fm_ipc_get_handle": (ctypes.c_int, [_P, _P]),
     "fm_ipc_open_handle": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
     "fm_ipc_close_handle": (ctypes.c_int, [_P]),

@@ -77,11 +77,69 @@ int nccl_allreduce_sum_f64(double* buf, size_t n, void* comm, cudaStream_t st) {
   return FM_OK;
 }
 
+// Small all-reduce over peer memory (the pass scalars): one warp per rank
+// writes its n values into its exchange buffer (step parity), publishes the
+// exchange id, waits for every peer's id and sums the ranks' values in rank
+// order -- the same result on every rank.  Bounded spins: a missing peer
+// sets *err instead of hanging.
+template <bool SYS>
+__global__ void peer_sum_kernel(double* vals, int n, double* const* part,
+                                unsigned long long* const* ready, int n_ranks, int rank,
+                                unsigned long long id, int32_t* err) {
+  const int lane = threadIdx.x;
+  const int parity = (int)(id & 1);
+  double* mine = part[rank] + parity * n;
+  if (lane < n) mine[lane] = vals[lane];
+  __syncwarp();
+  if (lane == 0) {
+    if (SYS) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ready[rank]), "l"(id) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ready[rank]), "l"(id) : "memory");
+  }
+  if (lane < n_ranks) {
+    long long spins = 0;
+    for (;;) {
+      unsigned long long v;
+      if (SYS) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ready[lane]) : "memory");
+      else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ready[lane]) : "memory");
+      if (v >= id) break;
+      __nanosleep(64);
+      if (++spins > (1ll << 24)) {
+        atomicCAS(err, 0, FM_ERR_CUDA);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < n) {
+    double t = 0.0;
+    for (int r = 0; r < n_ranks; ++r) t += __ldcv(part[r] + parity * n + lane);
+    vals[lane] = t;
+  }
+}
+
 }  // namespace fm
 
 using namespace fm;
 
 extern "C" {
+
+int fm_peer_sum_f64(double* vals, int32_t n, const fm_peer_group* group, int32_t* err, void* stream) {
+  FM_REQUIRE(vals && group && group->part && group->ready && err && n >= 1 && n <= 32,
+             "bad peer sum arguments");
+  FM_REQUIRE(group->n_ranks >= 1 && group->n_ranks <= 32 && group->rank >= 0 &&
+                 group->rank < group->n_ranks && group->epoch >= 0,
+             "bad peer group");
+  const unsigned long long id = (unsigned long long)group->epoch + 1;
+  cudaStream_t st = as_stream(stream);
+  if (group->system_scope)
+    peer_sum_kernel<true><<<1, 32, 0, st>>>(vals, n, group->part, group->ready, group->n_ranks,
+                                            group->rank, id, err);
+  else
+    peer_sum_kernel<false><<<1, 32, 0, st>>>(vals, n, group->part, group->ready, group->n_ranks,
+                                             group->rank, id, err);
+  FM_LAUNCHED(peer_sum_kernel);
+  return FM_OK;
+}
 
 int fm_nccl_available(void) { return nccl_api() ? 1 : 0; }
 

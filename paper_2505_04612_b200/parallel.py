@@ -129,6 +129,95 @@ class NcclComm:
             self.handle = None
 
 
+def _peer_alloc(part_doubles, n_flags):
+    """One rank's exchange buffers (whole cudaMalloc allocations, zeroed)."""
+    part, ready = ctypes.c_void_p(), ctypes.c_void_p()
+    N.check(N.lib().fm_peer_buffers_alloc(part_doubles, n_flags, ctypes.byref(part), ctypes.byref(ready)))
+    return part.value, ready.value
+
+
+def _peer_share(mine, group=None):
+    """Exchange the ranks' buffers through CUDA IPC: returns (parts, readies,
+    opened) in rank order (own pointers for this rank, mapped peer memory
+    for the others)."""
+    import torch.distributed as dist
+    lib = N.lib()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    hp, hr = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
+    N.check(lib.fm_ipc_get_handle(mine[0], hp))
+    N.check(lib.fm_ipc_get_handle(mine[1], hr))
+    allh = [None] * world
+    dist.all_gather_object(allh, (bytes(hp), bytes(hr)), group=group)
+    parts, readies, opened = [], [], []
+    for r, (a, b) in enumerate(allh):
+        if r == rank:
+            parts.append(mine[0])
+            readies.append(mine[1])
+            continue
+        pa, pb = ctypes.c_void_p(), ctypes.c_void_p()
+        N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(a), ctypes.byref(pa)))
+        N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(b), ctypes.byref(pb)))
+        parts.append(pa.value)
+        readies.append(pb.value)
+        opened += [pa.value, pb.value]
+    return parts, readies, opened
+
+
+class PeerSum:
+    """In-place sums of up to 32 doubles over the ranks through peer memory
+    (fm_peer_sum_f64: one warp publishes, waits for every peer, sums in rank
+    order) -- the pass scalars of the sharded step without a separate
+    collective library call."""
+
+    native = True
+
+    def __init__(self, n, rank, world, parts, readies, owned, opened=(), system_scope=False):
+        self.n, self.rank, self.world = n, rank, world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.part_ptrs = torch.tensor(parts, dtype=torch.int64, device=dev)
+        self.ready_ptrs = torch.tensor(readies, dtype=torch.int64, device=dev)
+        self.owned, self.opened = owned, list(opened)
+        self.system_scope = system_scope
+        self.epoch = 0
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    @classmethod
+    def local_group(cls, n, world):
+        bufs = [_peer_alloc(n, 1) for _ in range(world)]
+        return [cls(n, r, world, [b[0] for b in bufs], [b[1] for b in bufs], bufs[r])
+                for r in range(world)]
+
+    @classmethod
+    def from_process_group(cls, n, group=None):
+        import torch.distributed as dist
+        mine = _peer_alloc(n, 1)
+        parts, readies, opened = _peer_share(mine, group)
+        return cls(n, dist.get_rank(group), dist.get_world_size(group), parts, readies, mine,
+                   opened, system_scope=True)
+
+    def allreduce_(self, t):
+        assert t.dtype == torch.float64 and t.is_contiguous() and t.numel() <= self.n
+        grp = N.PeerGroup(n_ranks=self.world, rank=self.rank, part=self.part_ptrs.data_ptr(),
+                          ready=self.ready_ptrs.data_ptr(), epoch=self.epoch, max_blocks=0,
+                          system_scope=int(self.system_scope))
+        N.check(N.lib().fm_peer_sum_f64(N.ptr(t), t.numel(), ctypes.byref(grp), N.ptr(self.err),
+                                        N.stream_handle()))
+        self.epoch += 1
+        return t
+
+    def check(self):
+        N.raise_flag(self.err.item())
+
+    def close(self):
+        lib = N.lib()
+        for ptr in self.opened:
+            N.check(lib.fm_ipc_close_handle(ptr))
+        self.opened = []
+        if self.owned:
+            N.check(lib.fm_peer_buffers_free(*self.owned))
+            self.owned = None
+
+
 class PeerComm:
     """The sharded step's all-reduce fused into its reduce kernel over peer
     memory (fm_epi_adam_steps_peer): rank r's blocks publish their packed
@@ -181,11 +270,7 @@ class PeerComm:
     @staticmethod
     def _alloc(gs):
         lib = N.lib()
-        part, ready = ctypes.c_void_p(), ctypes.c_void_p()
-        N.check(lib.fm_peer_buffers_alloc(lib.fm_peer_part_len(ctypes.byref(gs)),
-                                          lib.fm_peer_flag_len(ctypes.byref(gs)),
-                                          ctypes.byref(part), ctypes.byref(ready)))
-        return part.value, ready.value
+        return _peer_alloc(lib.fm_peer_part_len(ctypes.byref(gs)), lib.fm_peer_flag_len(ctypes.byref(gs)))
 
     @classmethod
     def local_group(cls, graph_struct, world, device, max_blocks=0):
@@ -202,25 +287,8 @@ class PeerComm:
         """One rank per process: exchange the buffers' IPC handles."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        lib = N.lib()
         mine = cls._alloc(graph_struct)
-        hp, hr = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
-        N.check(lib.fm_ipc_get_handle(mine[0], hp))
-        N.check(lib.fm_ipc_get_handle(mine[1], hr))
-        allh = [None] * world
-        dist.all_gather_object(allh, (bytes(hp), bytes(hr)), group=group)
-        parts, readies, opened = [], [], []
-        for r, (a, b) in enumerate(allh):
-            if r == rank:
-                parts.append(mine[0])
-                readies.append(mine[1])
-                continue
-            pa, pb = ctypes.c_void_p(), ctypes.c_void_p()
-            N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(a), ctypes.byref(pa)))
-            N.check(lib.fm_ipc_open_handle((ctypes.c_char * 64).from_buffer_copy(b), ctypes.byref(pb)))
-            parts.append(pa.value)
-            readies.append(pb.value)
-            opened += [pa.value, pb.value]
+        parts, readies, opened = _peer_share(mine, group)
         return cls(graph_struct, rank, world,
                    torch.tensor(parts, dtype=torch.int64, device=device),
                    torch.tensor(readies, dtype=torch.int64, device=device), mine,
@@ -485,6 +553,7 @@ def gather_blocks(local, b, comm):
     return torch.cat([p[:, :int(b[r + 1] - b[r])] for r, p in enumerate(parts)], dim=1)
 
 
-__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NcclComm", "PeerComm", "NoComm",
+__all__ = ["partition_pairs", "ShardedIrlsEngine", "Shard", "TorchComm", "NcclComm", "PeerComm", "PeerSum",
+           "NoComm",
            "make_shards",
            "init_blocks", "gather_blocks", "multi_init_align_sharded"]

@@ -234,3 +234,33 @@ def test_peer_exchange_two_ranks_one_gpu_bitwise_sharded_reference(golden_c1):
     refm = O.pose_metrics(g["c1_R_out"], g["c1_c_out"], g["c1_R_gt"], g["c1_c_gt"])
     for key in ("RRA@1", "RRA@3", "RTA@1", "RTA@3"):
         assert ours[key] == refm[key]
+
+
+def test_peer_sum_two_ranks_one_gpu():
+    """fm_peer_sum_f64 with two ranks sharing the GPU (one thread + stream
+    each): every exchange returns the rank-order sum on both ranks."""
+    import threading
+    comms = P_.PeerSum.local_group(3, 2)
+    vals = [np.random.default_rng(r).normal(size=(50, 3)) for r in range(2)]
+    out = [[], []]
+
+    def worker(r):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            for k in range(50):
+                t = torch.as_tensor(vals[r][k], device="cuda").contiguous()
+                comms[r].allreduce_(t)
+                out[r].append(t.cpu().numpy())
+            comms[r].check()
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    try:
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+    finally:
+        for c in comms:
+            c.close()
+    want = vals[0] + vals[1]
+    assert np.array_equal(np.stack(out[0]), want) and np.array_equal(np.stack(out[1]), want)
