@@ -564,9 +564,9 @@ def scalar_comm(world):
         return P_.NoComm()
     if "c" not in _SCALAR_COMM:
         comm = None
-        if dist.get_backend() == "nccl":
+        if True:
             # the scalars over peer memory (one warp: publish, wait, rank-order
-            # sum), NCCL if the peer buffers cannot be shared
+            # sum; buffers shared by CUDA IPC), else NCCL / gloo
             try:
                 comm = P_.PeerSum.from_process_group(3)
                 probe = torch.zeros(3, dtype=torch.float64, device="cuda")
@@ -580,9 +580,7 @@ def scalar_comm(world):
             if ok.item() < 1.0:
                 comm = None
             if comm is None:
-                comm = P_.NcclComm()
-        else:
-            comm = P_.TorchComm()
+                comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
         _SCALAR_COMM["c"] = comm
     return _SCALAR_COMM["c"]
 
@@ -956,13 +954,12 @@ def sharded_irls_bench(spec, args, device, stream, world, rank):
         graph = PairGraph(ii[lo:hi], jj[lo:hi], zeros, zeros, len(ids), 1, True, device=device)
         del sc
         params = torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids), device=device)
-        # NCCL backend (one GPU per rank): the fused peer-memory exchange
-        # (PeerComm over CUDA IPC), falling back to our NCCL communicator
-        # (gradient, ncclAllReduce, Adam in one graph) if the peer exchange
-        # fails; gloo (functional runs on one GPU): torch's collectives
+        # the fused peer-memory exchange (PeerComm over CUDA IPC), falling
+        # back to our NCCL communicator (gradient, ncclAllReduce, Adam in one
+        # graph) or, over gloo, torch's collectives if it cannot be set up
         note = ""
         comm = None
-        if dist.get_backend() == "nccl":
+        if True:  # every backend: the ranks' buffers shared by CUDA IPC
             try:
                 comm = P_.PeerComm.from_process_group(graph.struct(), device)
                 eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params,

@@ -264,3 +264,65 @@ def test_peer_sum_two_ranks_one_gpu():
             c.close()
     want = vals[0] + vals[1]
     assert np.array_equal(np.stack(out[0]), want) and np.array_equal(np.stack(out[1]), want)
+
+
+def _ipc_worker(rank, world, port, path, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        g = dict(np.load(path))
+        lengths, ij, x1, x2, p0 = _c1_inputs(g)
+        n = int(ij.max()) + 1
+        bounds = P_.partition_pairs(lengths, world)
+        sh = P_.make_shards(x1, x2, lengths, ij, np.zeros_like(ij), n, 1, True, bounds,
+                            torch.device("cuda"), ranks=[rank])
+        comm = P_.PeerComm.from_process_group(sh[0].graph.struct(), torch.device("cuda"))
+        try:
+            params = torch.as_tensor(p0, device="cuda")
+            eng = P_.ShardedIrlsEngine(sh, params, Cfg(), comm=comm)
+            l1 = eng.run()
+        finally:
+            comm.close()
+        q.put((rank, l1, params.cpu().numpy(), eng.dropped, eng.kept))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_two_processes_cuda_ipc(golden_c1):
+    """The multi-process form of the fused exchange: two processes (gloo
+    only for the 64-byte CUDA IPC handles and the pass scalars), each
+    mapping the other's exchange buffers (fm_ipc_open_handle) and running
+    fm_epi_adam_steps_peer with system-scope release/acquire.  Both end bitwise
+    equal to the two-shard engine in one process."""
+    import os
+    import socket
+    import torch.multiprocessing as mp
+    g = golden_c1
+    path = os.path.join(os.path.dirname(__file__), "golden", "golden_config1.npz")
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, la, pa, da, ka), (_, lb, pb, db, kb) = res
+    assert np.array_equal(pa, pb) and la == lb and (da, ka) == (db, kb)
+    lengths, ij, x1, x2, p0 = _c1_inputs(g)
+    n = int(ij.max()) + 1
+    bounds = P_.partition_pairs(lengths, 2)
+    ref_sh = P_.make_shards(x1, x2, lengths, ij, np.zeros_like(ij), n, 1, True, bounds,
+                            torch.device("cuda"))
+    pr = torch.as_tensor(p0.copy(), device="cuda")
+    l1_ref = P_.ShardedIrlsEngine(ref_sh, pr, Cfg()).run()
+    assert la == l1_ref and np.array_equal(pa, pr.cpu().numpy())
+    assert [da, ka] == list(g["c1_counts"])
