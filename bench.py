@@ -673,6 +673,12 @@ def run_ours(args, spec, world, rank, local):
     e2e_steps(2)
     e2e_ms = max_over_ranks(e2e_steps(max(3, min(args.steps, 10))), device, world)
 
+    # ---------------------------------------------------- SfM optimize time
+    extra = {}
+    if not args.skip_optimize:
+        extra["sfm_optimize"] = sfm_optimize(args, spec, scene, store, graph, ids, device, stream,
+                                             world, rank)
+
     # --------------------------------------------- strong scaling (secondary)
     strong = None
     if not args.skip_strong:
@@ -687,12 +693,6 @@ def run_ours(args, spec, world, rank, local):
             if rank == 0:
                 strong["ms_per_step_1gpu_same_run"] = t1
                 strong["efficiency_vs_1gpu"] = t1 / (world * strong["ms_per_step"])
-
-    # ---------------------------------------------------- SfM optimize time
-    extra = {}
-    if not args.skip_optimize:
-        extra["sfm_optimize"] = sfm_optimize(args, spec, scene, store, graph, ids, device, stream,
-                                             world, rank)
 
     # ---------------------------------------------------------- CPU baseline
     cpu = None
