@@ -553,9 +553,10 @@ _SCALAR_COMM = {}
 
 
 def scalar_comm(world):
-    """The pass-scalar all-reduce of N > 1 steps: with the NCCL backend
-    (one GPU per rank) over peer memory (parallel.PeerSum, CUDA IPC), else
-    our NCCL communicator; over gloo torch.distributed's."""
+    """The pass-scalar all-reduce of N > 1 steps: over peer memory
+    (parallel.PeerSum: one warp publishes, waits for the peers, sums in rank
+    order; buffers shared by CUDA IPC) when every rank can set it up, else
+    our NCCL communicator (NCCL backend) or torch's collectives (gloo)."""
     import torch
     import torch.distributed as dist
 
@@ -564,23 +565,20 @@ def scalar_comm(world):
         return P_.NoComm()
     if "c" not in _SCALAR_COMM:
         comm = None
-        if True:
-            # the scalars over peer memory (one warp: publish, wait, rank-order
-            # sum; buffers shared by CUDA IPC), else NCCL / gloo
-            try:
-                comm = P_.PeerSum.from_process_group(3)
-                probe = torch.zeros(3, dtype=torch.float64, device="cuda")
-                comm.allreduce_(probe)
-                torch.cuda.synchronize()
-                comm.check()
-            except Exception:  # noqa: BLE001 - NCCL below
-                comm = None
-            ok = torch.tensor([1.0 if comm is not None else 0.0], device="cuda")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if ok.item() < 1.0:
-                comm = None
-            if comm is None:
-                comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
+        try:
+            comm = P_.PeerSum.from_process_group(3)
+            probe = torch.zeros(3, dtype=torch.float64, device="cuda")
+            comm.allreduce_(probe)
+            torch.cuda.synchronize()
+            comm.check()
+        except Exception:  # noqa: BLE001 - the fallback below
+            comm = None
+        ok = torch.tensor([1.0 if comm is not None else 0.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1.0:
+            comm = None
+        if comm is None:
+            comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
         _SCALAR_COMM["c"] = comm
     return _SCALAR_COMM["c"]
 
@@ -959,25 +957,24 @@ def sharded_irls_bench(spec, args, device, stream, world, rank):
         # graph) or, over gloo, torch's collectives if it cannot be set up
         note = ""
         comm = None
-        if True:  # every backend: the ranks' buffers shared by CUDA IPC
-            try:
-                comm = P_.PeerComm.from_process_group(graph.struct(), device)
-                eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params,
-                                           args.cfg, comm=comm)
-                eng.run()  # warm-up: graph captures of the step chunks
-            except Exception as exc:  # noqa: BLE001 - reported in the line
-                note = f"peer exchange failed ({type(exc).__name__}: {exc}); NCCL used"
-                if comm is not None:
-                    comm.close()
-                comm = None
-            ok = torch.tensor([1.0 if comm is not None else 0.0], device=device)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if ok.item() < 1.0 and comm is not None:
+        try:
+            comm = P_.PeerComm.from_process_group(graph.struct(), device)
+            eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params,
+                                       args.cfg, comm=comm)
+            eng.run()  # warm-up: graph captures of the step chunks
+        except Exception as exc:  # noqa: BLE001 - reported in the line
+            note = f"peer exchange failed ({type(exc).__name__}: {exc}); fallback used"
+            if comm is not None:
                 comm.close()
-                comm = None
-            store.reset_active()
-            params.copy_(torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids),
-                                         device=device))
+            comm = None
+        ok = torch.tensor([1.0 if comm is not None else 0.0], device=device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1.0 and comm is not None:
+            comm.close()
+            comm = None
+        store.reset_active()
+        params.copy_(torch.as_tensor(scenes.initial_params(scenes.generate_poses(spec), ids),
+                                     device=device))
         if comm is None:
             comm = P_.NcclComm() if dist.get_backend() == "nccl" else P_.TorchComm()
         eng = P_.ShardedIrlsEngine([P_.Shard(store, graph, args.precision)], params, args.cfg,
