@@ -312,6 +312,62 @@ def reference_steps(spec, steps, warmup, n_pairs=None, procs=None):
     return times, rp
 
 
+C1_FIXTURE = os.path.join(ROOT, "tests", "golden", "golden_config1.npz")
+
+
+class Poses:  # the reference's PoseState fields (ref/model.py:129-135)
+    def __init__(self, rotations, centers, registered=None):
+        self.rotations, self.centers = rotations, centers
+        self.registered = np.ones(len(rotations), dtype=bool) if registered is None else registered
+
+
+def c1_problem(pair_cls, graph_cls):
+    """BASELINE config 1 as the pipeline hands it to the two stages (SURVEY
+    8d: "C1: everything in full"): 1,225 EpipolarPair (223,241 point pairs,
+    fp64 homogeneous, from the committed fixture tests/golden/golden_config1.npz
+    that tests/golden/make_golden.py built with the reference's synth +
+    calibration), the perturbed poses, and the 1,225-edge DirectionGraph.
+    pair_cls / graph_cls: the reference's or our classes."""
+    g = dict(np.load(C1_FIXTURE))
+    lens = g["c1_len"].astype(np.int64)
+    start = np.concatenate([[0], np.cumsum(lens)])
+    pairs = []
+    for k, (i, j) in enumerate(g["c1_ij"]):
+        a, b = start[k], start[k + 1]
+        pairs.append(pair_cls(i=int(i), j=int(j), cam_i=0, cam_j=0,
+                              x1=np.column_stack([g["c1_x1"][a:b].astype(np.float64), np.ones(b - a)]),
+                              x2=np.column_stack([g["c1_x2"][a:b].astype(np.float64), np.ones(b - a)])))
+    graph = graph_cls(n=len(g["c1_R_in"]), edges_i=g["c1_ij"][:, 0].astype(np.int64),
+                      edges_j=g["c1_ij"][:, 1].astype(np.int64), directions=g["c1_dirs"])
+    return g, pairs, graph
+
+
+def c1_sfm_optimize(E, T, cfg, poses_cls, reps, sync=lambda: None):
+    """irls_refine + multi_init_align on C1 through the given modules (the
+    reference's or ours), wall time per call; returns the timings and the
+    results' fingerprints (the two arms must agree)."""
+    out = {"irls_s": [], "translation_s": []}
+    for _ in range(reps):
+        g, pairs, graph = c1_problem(E.EpipolarPair, T.DirectionGraph)
+        poses = poses_cls(g["c1_R_in"].copy(), g["c1_c_in"].copy())
+        sync()
+        t0 = time.perf_counter()
+        res, fs, rep = E.irls_refine(poses, pairs, cfg, n_cameras=1)
+        sync()
+        t1 = time.perf_counter()
+        centers, loss = T.multi_init_align(graph, cfg, seed=0)
+        sync()
+        t2 = time.perf_counter()
+        out["irls_s"].append(t1 - t0)
+        out["translation_s"].append(t2 - t1)
+    out["l1_history"] = [float(x) for x in rep["l1_history"]]
+    out["kept_pairs"] = int(rep["active_pairs"])
+    out["translation_loss"] = float(loss)
+    out["irls_max_abs_dR_vs_fixture"] = float(np.abs(res.rotations - g["c1_R_out"]).max())
+    out["translation_loss_equals_fixture"] = bool(float(loss) == float(g["c1_tr_loss"][0]))
+    return out
+
+
 def reference_sfm_optimize(spec):
     """The reference's own per-step costs of the two gradient stages on one
     core (numpy; it is single-threaded code), stated as extrapolations:
@@ -364,6 +420,22 @@ def reference_sfm_optimize(spec):
         out["multi_init_align_c3_extrapolated_s"] = 17 * 6000 * min(t)
     out["how"] = ("reference (baseline/_ref) on one host core, best of 3 per call; "
                   "irls_refine x 900 Adam steps, multi_init_align x 17 x 6000 steps")
+    # measured in full on BASELINE config 1 (the same inputs as our arm's
+    # sfm_optimize.c1): the reference's own irls_refine + multi_init_align
+    from fastmap import epipolar as RE
+    from fastmap.config import PipelineConfig
+    cores = host_cores()
+    with threadpool_limits(cores):  # numpy/BLAS on every host core
+        c1 = c1_sfm_optimize(RE, RT, PipelineConfig(),
+                             lambda R, c: PoseState(rotations=R, centers=c,
+                                                    registered=np.ones(len(R), dtype=bool)), reps=1)
+    c1["sfm_optimize_s"] = c1["irls_s"][0] + c1["translation_s"][0]
+    c1["how"] = ("config 1 (50 images, 1,225 image pairs, 223,241 point pairs; "
+                 "tests/golden/golden_config1.npz): the reference's irls_refine then "
+                 "multi_init_align (3 inits x 6000 steps + final), numpy/BLAS "
+                 f"on {cores} host threads, one call")
+    c1["cores"] = cores
+    out["c1"] = c1
     return out
 
 
@@ -813,18 +885,24 @@ def sfm_optimize(args, spec, scene, store, graph, ids, device, stream, world, ra
     from paper_2505_04612_b200 import scenes
     out = {}
     if rank == 0:
-        params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
-        store.reset_active()
+        times = []
         with torch.cuda.stream(stream):
-            eng2 = E.IrlsEngine(store, graph, params0, args.cfg, precision=args.precision)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            l1h = eng2.run()
-            torch.cuda.synchronize()
-            t_irls = time.perf_counter() - t0
-        out.update({"irls_refine_engine_s": t_irls, "l1_history": l1h,
+            for _ in range(4):  # the first call captures the step graphs
+                params0 = torch.as_tensor(scenes.initial_params(scene, ids), device=device)
+                store.reset_active()
+                eng2 = E.IrlsEngine(store, graph, params0, args.cfg, precision=args.precision)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                l1h = eng2.run()
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+        out.update({"irls_refine_engine_s": float(np.median(times[1:])),
+                    "irls_refine_engine_first_s": times[0],
+                    "irls_refine_engine_samples_s": times[1:], "l1_history": l1h,
                     "dropped_pairs": eng2.dropped, "active_pairs": eng2.kept,
-                    "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps"})
+                    "schedule": "3 prune rounds x 3 IRLS x 100 Adam steps",
+                    "engine_note": "median of 3 calls after a first call (which also captures "
+                                   "the 100-step CUDA graphs)"})
         if not args.skip_api:
             out.update(api_irls_bench(args, scene, device, stream))
     if world > 1:
@@ -832,7 +910,38 @@ def sfm_optimize(args, spec, scene, store, graph, ids, device, stream, world, ra
     elif not args.skip_api:
         out.update(nccl_one_rank_bench(args, scene, store, graph, ids, device, stream))
     out.update(translation_bench(device, stream, sharded=world > 1))
+    if rank == 0:
+        if out.get("irls_refine_engine_s") is not None:
+            # GPU "SfM optimize time" = multi_init_align + irls_refine,
+            # with and without the store upload (C2 epipolar, C3 translation)
+            out["sfm_optimize_s_without_upload"] = out["irls_refine_engine_s"] + out["multi_init_align_s"]
+            if out.get("irls_refine_api_s") is not None:
+                out["sfm_optimize_s_with_upload"] = out["irls_refine_api_s"] + out["multi_init_align_s"]
+        out["c1"] = our_c1_sfm_optimize(device, stream)
     return out
+
+
+def our_c1_sfm_optimize(device, stream):
+    """BASELINE config 1 in full through our drop-in API (the functions
+    install() puts at ref/pipeline.py:233/:248): irls_refine from the 1,225
+    host EpipolarPair objects (store build + upload + write-back included)
+    then multi_init_align -- the same inputs and calls the reference arm
+    times (its sfm_optimize.c1).  Median of 3 calls after a first call."""
+    import torch
+
+    from paper_2505_04612_b200 import epipolar as E
+    from paper_2505_04612_b200 import translation as T
+    from paper_2505_04612_b200.config import HotPathConfig
+    with torch.cuda.stream(stream):
+        first = c1_sfm_optimize(E, T, HotPathConfig(), Poses, 1, torch.cuda.synchronize)
+        c1 = c1_sfm_optimize(E, T, HotPathConfig(), Poses, 3, torch.cuda.synchronize)
+    irls, tr = float(np.median(c1["irls_s"])), float(np.median(c1["translation_s"]))
+    c1.update({"irls_s": irls, "translation_s": tr, "sfm_optimize_s": irls + tr,
+               "first_call_sfm_optimize_s": first["irls_s"][0] + first["translation_s"][0],
+               "how": "config 1 (tests/golden/golden_config1.npz): irls_refine (API, host "
+                      "EpipolarPair objects) then multi_init_align (3 inits x 6000 steps + final); "
+                      "median of 3 calls after a first call"})
+    return c1
 
 
 def api_irls_bench(args, scene, device, stream):
@@ -846,11 +955,6 @@ def api_irls_bench(args, scene, device, stream):
 
     from paper_2505_04612_b200 import epipolar as E
 
-    class Poses:  # the reference's PoseState fields (ref/model.py:129-135)
-        def __init__(self, rotations, centers, registered=None):
-            self.rotations, self.centers = rotations, centers
-            self.registered = np.ones(len(rotations), dtype=bool) if registered is None else registered
-
     x1 = scene["x1"].double().cpu().numpy()
     x2 = scene["x2"].double().cpu().numpy()
     lens = scene["lengths"]
@@ -860,16 +964,22 @@ def api_irls_bench(args, scene, device, stream):
                             x1=np.hstack([x1[start[q]:start[q + 1]], ones[:lens[q]]]),
                             x2=np.hstack([x2[start[q]:start[q + 1]], ones[:lens[q]]]))
              for q, (i, j) in enumerate(scene["ij"])]
-    poses = Poses(scene["R_in"].copy(), scene["c_in"].copy())
+    times = []
     with torch.cuda.stream(stream):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, _, rep = E.irls_refine(poses, pairs, args.cfg, n_cameras=1)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-    return {"irls_refine_api_s": dt, "api_l1_history": rep["l1_history"],
+        for _ in range(3):
+            poses = Poses(scene["R_in"].copy(), scene["c_in"].copy())
+            for p in pairs:
+                p.active[:] = True  # irls_refine prunes the masks in place
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, _, rep = E.irls_refine(poses, pairs, args.cfg, n_cameras=1)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    return {"irls_refine_api_s": float(np.median(times)), "irls_refine_api_samples_s": times,
+            "api_l1_history": rep["l1_history"],
             "api_note": "drop-in irls_refine on 25,000 EpipolarPair objects (fp64 host arrays): "
-                        "store build + H2D upload + device schedule + mask write-back"}
+                        "store build + H2D upload + device schedule + mask write-back; median "
+                        "of 3 calls"}
 
 
 def nccl_one_rank_bench(args, scene, store, graph, ids, device, stream):
@@ -1028,16 +1138,23 @@ def translation_bench(device, stream, sharded=False):
         if sharded:
             import torch.distributed as dist
             dist.barrier()
-        t0 = time.perf_counter()
-        centers, loss = run(g, C, seed=0)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        times = []
+        for _ in range(3):
+            if sharded:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            centers, loss = run(g, C, seed=0)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
     if sharded:
-        dt = max_over_ranks(dt, device, int(os.environ.get("WORLD_SIZE", "1")))
+        times = [max_over_ranks(t, device, int(os.environ.get("WORLD_SIZE", "1"))) for t in times]
+    dt = float(np.median(times))
     evals = (16 + 1) * 6000 * m
-    return {"multi_init_align_s": dt, "translation_loss": loss,
+    return {"multi_init_align_s": dt, "multi_init_align_samples_s": times, "translation_loss": loss,
             "translation_config": "C3: 2000 nodes, 200000 edges, 16 inits x 6000 steps + final "
-                                  "(after one 200-step warm-up call); bitwise the reference",
+                                  "(after one 200-step warm-up call; median of 3 calls); bitwise "
+                                  "the reference",
             "translation_edge_evals_per_s": evals / dt}
 
 

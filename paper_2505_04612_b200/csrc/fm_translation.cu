@@ -295,23 +295,29 @@ __device__ __forceinline__ double flip(double x, long long sign_mask) {
 #define FM_TR_MINB 2  // resident 256-thread blocks per SM (3: register cap 80, spills, no faster)
 #endif
 
-template <int MODE, int R>
-__global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
-                               const double* __restrict__ cur,
-                               double* __restrict__ nxt, double* __restrict__ am,
-                               double* __restrict__ av, double* __restrict__ lpart, int B,
-                               double lr, double b1, double b2, double eps,
-                               const double* const* __restrict__ bc, int step, int32_t* flag) {
+// Loads of centres written in the same launch by other blocks (the
+// cluster-persistent descent) must come from L2; across launches the
+// read-only path is fine.
+template <bool COHERENT>
+__device__ __forceinline__ double ld_c(const double* p) {
+  return COHERENT ? __ldcg(p) : __ldg(p);
+}
+
+// One optimizer step of warp work item w = (node, group of R runs): the
+// body of tr_step_kernel, shared with the cluster-persistent descent.
+template <int MODE, int R, bool COHERENT>
+__device__ __forceinline__ void tr_node_step(const fm_dir_graph& g, const double4* __restrict__ rec,
+                                             const double* cur, double* nxt, double* __restrict__ am,
+                                             double* __restrict__ av, double* __restrict__ lpart, int B,
+                                             double lr, double b1, double b2, double eps,
+                                             const double* bc1, const double* bc2, int step,
+                                             int32_t* flag, int64_t w, double* tile) {
   constexpr int kSlots = 32 / R;
-  constexpr int kIF = FM_TR_IF;        // incidences in flight per lane
-  constexpr int kTile = kIF * 32 * 3;  // doubles per warp: [kIF * kSlots][R][3]
-  __shared__ double tile_all[8][kTile];
+  constexpr int kIF = FM_TR_IF;  // incidences in flight per lane
   const int lane = threadIdx.x & 31;
-  double* tile = tile_all[threadIdx.x >> 5];
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int groups = (B + R - 1) / R;
   if (w >= (int64_t)g.n_nodes * groups) return;
-  if (MODE == kTrAdam && *flag) return;
+  if (MODE == kTrAdam && (COHERENT ? *(volatile int32_t*)flag : *flag)) return;
   const int v = (int)(w / groups);
   const int rb = lane % R, slot = lane / R;
   const int b = (int)(w % groups) * R + rb;  // this lane's run
@@ -324,7 +330,8 @@ __global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_g
 
   double cv[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) cv[k] = cur[((int64_t)v * B + bl) * 3 + k];
+  for (int k = 0; k < 3; ++k) cv[k] = COHERENT ? __ldcg(cur + ((int64_t)v * B + bl) * 3 + k)
+                                               : cur[((int64_t)v * B + bl) * 3 + k];
   double acc = 0.0, lacc = 0.0;
   const int e0 = g.node_off[v], e1 = g.node_off[v + 1];
   for (int base = e0; base < e1; base += kIF * kSlots) {
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_g
     for (int f = 0; f < kIF; ++f) {
       const double* p = cur + ((int64_t)(__double_as_longlong(r[f].w) & 0x7fffffff) * B + bl) * 3;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) c[f][k] = __ldg(p + k);
+      for (int k = 0; k < 3; ++k) c[f][k] = ld_c<COHERENT>(p + k);
     }
 #pragma unroll
     for (int f = 0; f < kIF; ++f) {
@@ -385,14 +392,67 @@ __global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_g
     atomicMax(flag, FM_ERR_NONFINITE_GRAD);
     return;
   }
-  const double c1 = bc[0][step], c2 = bc[1][step];
-  const double ck = cur[base + fk];
+  const double c1 = bc1[step], c2 = bc2[step];
+  const double ck = COHERENT ? __ldcg(cur + base + fk) : cur[base + fk];
   const double mk = __dadd_rn(__dmul_rn(b1, am[base + fk]), __dmul_rn(1.0 - b1, acc));
   const double vk = __dadd_rn(__dmul_rn(b2, av[base + fk]), __dmul_rn(1.0 - b2, __dmul_rn(acc, acc)));
   am[base + fk] = mk;
   av[base + fk] = vk;
   nxt[base + fk] = __dsub_rn(ck, __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, c1)),
                                            __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, c2)), eps)));
+}
+
+constexpr int kTrTile = FM_TR_IF * 32 * 3;  // doubles per warp: [kIF * kSlots][R][3]
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(256, FM_TR_MINB) tr_step_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
+                               const double* __restrict__ cur,
+                               double* __restrict__ nxt, double* __restrict__ am,
+                               double* __restrict__ av, double* __restrict__ lpart, int B,
+                               double lr, double b1, double b2, double eps,
+                               const double* const* __restrict__ bc, int step, int32_t* flag) {
+  __shared__ double tile_all[8][kTrTile];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  tr_node_step<MODE, R, false>(g, rec, cur, nxt, am, av, lpart, B, lr, b1, b2, eps,
+                               MODE == kTrAdam ? bc[0] : nullptr, MODE == kTrAdam ? bc[1] : nullptr,
+                               step, flag, w, tile_all[threadIdx.x >> 5]);
+}
+
+// Small graphs (<= 2 warp work items per warp of one cluster: config 1, the acceptance
+// scenes): the whole descent in ONE launch of one thread-block cluster --
+// every step the warps run their work items (tr_node_step, the same
+// arithmetic as the per-step kernel), then the cluster barrier (release /
+// acquire at cluster scope) publishes the new centres to the other blocks;
+// centres written in the launch are read from L2 (ld.cg).  Replaces one
+// graph-replayed launch per step (launch + drain latency dominated at these
+// sizes).  Every thread runs every step and every barrier: a raised flag
+// turns the remaining steps into no-ops instead of an early exit.
+constexpr int kClusterMax = 8;  // blocks per cluster (portable size; 16 is tried first)
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) tr_steps_cluster_kernel(const fm_dir_graph g, const double4* __restrict__ rec,
+                                                           double* c0, double* c1, double* __restrict__ am,
+                                                           double* __restrict__ av, double* __restrict__ lpart,
+                                                           int B, double lr, double b1, double b2, double eps,
+                                                           const double* bc1, const double* bc2, int steps,
+                                                           int32_t* flag) {
+  __shared__ double tile_all[8][kTrTile];
+  const int groups = (B + R - 1) / R;
+  const int64_t n_work = (int64_t)g.n_nodes * groups;
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  double* tile = tile_all[threadIdx.x >> 5];
+  for (int k = 0; k < steps; ++k) {
+    const double* cur = (k & 1) ? c1 : c0;
+    double* nxt = (k & 1) ? c0 : c1;
+    for (int64_t w = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); w < n_work; w += stride)
+      tr_node_step<kTrAdam, R, true>(g, rec, cur, nxt, am, av, lpart, B, lr, b1, b2, eps, bc1, bc2, k,
+                                     flag, w, tile);
+    cluster_sync_all();
+  }
 }
 
 // |r| of flattened element q of the (m, 3) residual array of run b
@@ -600,6 +660,59 @@ int enqueue_exact_loss(const fm_dir_graph& g, const double* c, int B, const TrSc
   return FM_OK;
 }
 
+template <int R>
+cudaError_t launch_tr_cluster_r(const fm_dir_graph& g, const TrScratch& s, int B, int steps, double lr,
+                                double b1, double b2, double eps, const double* table, int32_t* flag,
+                                int nblk, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nblk);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)nblk;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (nblk > kClusterMax) {
+    cudaError_t e = cudaFuncSetAttribute(tr_steps_cluster_kernel<R>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchKernelEx(&cfg, tr_steps_cluster_kernel<R>, g, (const double4*)s.rec, s.cA, s.buf, s.m,
+                            s.v, s.lpart, B, lr, b1, b2, eps, table, table + steps, steps, flag);
+}
+
+// The whole descent as one cluster launch (small graphs); false: not taken
+// (too many work items, disabled, or the launch was refused -- the caller
+// then replays the per-step graphs).  Measured at config 1 (50 nodes, 3
+// runs, 6000 steps; tools/c1_tr_probe.py): per-step graphs 39-45 ms; one
+// cluster of 8 blocks, R = 4: 37 ms; 16 blocks (non-portable size), R = 2:
+// 29 ms -- twice the warps, so each SM sub-partition hides more latency.
+bool launch_tr_cluster(const fm_dir_graph& g, const TrScratch& s, int B, int steps, double lr, double b1,
+                       double b2, double eps, const double* table, int32_t* flag, cudaStream_t st) {
+  if (getenv("FM_TR_NOCLUSTER")) return false;
+  const char* env_r = getenv("FM_TRC_R");  // tuning overrides
+  const char* env_c = getenv("FM_TRC_CLUSTER");
+  const int R = env_r ? atoi(env_r) : (B >= 2 ? 2 : 1);
+  const int64_t n_work = (int64_t)g.n_nodes * ((B + R - 1) / R);
+  for (int cmax : {env_c ? atoi(env_c) : 2 * kClusterMax, kClusterMax}) {
+    if (n_work > 2 * 8 * (int64_t)cmax) continue;
+    const int nblk = (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n_work, 8), 1), cmax);
+    cudaError_t e;
+    switch (R) {
+      case 1: e = launch_tr_cluster_r<1>(g, s, B, steps, lr, b1, b2, eps, table, flag, nblk, st); break;
+      case 4: e = launch_tr_cluster_r<4>(g, s, B, steps, lr, b1, b2, eps, table, flag, nblk, st); break;
+      case 8: e = launch_tr_cluster_r<8>(g, s, B, steps, lr, b1, b2, eps, table, flag, nblk, st); break;
+      default: e = launch_tr_cluster_r<2>(g, s, B, steps, lr, b1, b2, eps, table, flag, nblk, st); break;
+    }
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();  // clear; try the portable size, then fall back
+  }
+  return false;
+}
+
 struct TrKey {
   std::vector<uintptr_t> k;
   bool operator<(const TrKey& o) const { return k < o.k; }
@@ -670,7 +783,7 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
   // graphs depend only on the scratch / graph pointers and are reused
   // across calls
   FM_CUDA(cudaMemcpyAsync(s.cA, centers, nb3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  int done = 0;
+  int done = launch_tr_cluster(*g, s, B, steps, lr, beta1, beta2, eps, table, flag, st) ? steps : 0;
   while (done < steps) {
     const int chunk = std::min(kGraphSteps, steps - done);
     tr_set_ctrl_kernel<<<1, 1, 0, st>>>(s.ctrl, table + done, table + steps + done);
@@ -726,9 +839,10 @@ int fm_tr_align(const fm_dir_graph* g, double* centers, int32_t B, int32_t steps
     }
     done += chunk;
   }
-  // full chunks (even) end in cA; an odd tail ends in buf.  The reference
-  // returns the loss evaluated at the last step, i.e. before its update.
-  const bool odd = (steps % kGraphSteps) & 1;
+  // step k reads cA (k even) or buf: an odd step count ends in buf (full
+  // graph chunks are even).  The reference returns the loss evaluated at the
+  // last step, i.e. before its update.
+  const bool odd = steps & 1;
   const double* fin = odd ? s.buf : s.cA;
   const double* pre = odd ? s.cA : s.buf;
   if (int rc = enqueue_exact_loss(*g, pre, B, s, loss_out, st)) return rc;

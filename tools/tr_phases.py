@@ -12,7 +12,7 @@ class C:
     translation_lr, translation_steps, translation_inits = 1e-3, 6000, 16
     adam_beta1, adam_beta2, adam_eps = 0.9, 0.999, 1e-8
 dg = T.device_graph(g)
-for rep in range(2):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     runs = T.init_runs(g, C, 0, range(16), dg)
     torch.cuda.synchronize(); t1 = time.perf_counter()
