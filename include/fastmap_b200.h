@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 5
+#define FM_ABI_VERSION 6
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -188,6 +188,12 @@ typedef struct fm_pass_out {
    * a one-warp kernel launched after it as a programmatic dependent launch
    * converts them; other passes use one fixed-order reduction kernel. */
   double* totals;
+  /* NULL, or a device error word (ABI 6): when it is non-zero at launch the
+   * pass does nothing -- in particular a prune leaves the masks alone.
+   * irls_refine enqueues its schedule without host round trips; this keeps
+   * the caller's masks at the state of the first error, as the reference
+   * stops there (ref/epipolar.py:283-308). */
+  const int32_t* stop;
 } fm_pass_out;
 
 /* Scratch of fm_point_pass.  It must be ZEROED before its first use (the
@@ -283,6 +289,20 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q,
                       double beta2, double eps, double scale, int32_t* flag,
                       int32_t use_graph, void* scratch, size_t scratch_bytes,
                       void* stream);
+
+/*
+ * fm_epi_adam_steps with scale = 2/Z read on the device from `totals`, the
+ * fused {L1, Z, kept} of the round's prune pass (fm_pass_out.totals), so
+ * irls_refine enqueues its whole schedule without a host round trip
+ * (ref/epipolar.py:291-308).  Z == 0 (every pair pruned) gives an infinite
+ * scale and a non-finite flag; the caller checks kept first.
+ */
+int fm_epi_adam_steps_z(const fm_pair_graph* g, const fm_quad_model* q,
+                        double* params, double* adam_m, double* adam_v,
+                        int64_t t0, int32_t n_steps, double lr, double beta1,
+                        double beta2, double eps, const double* totals,
+                        int32_t* flag, int32_t use_graph, void* scratch,
+                        size_t scratch_bytes, void* stream);
 
 /*
  * Sharded form of fm_epi_adam_steps: `g` / `q` hold this rank's

@@ -44,7 +44,7 @@ FM_QUAD_MOM64 = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
-ABI_VERSION = 5
+ABI_VERSION = 6
 _F64 = ctypes.c_double
 _SZ = ctypes.c_size_t
 
@@ -58,7 +58,7 @@ class PointStore(ctypes.Structure):
 
 class PassOut(ctypes.Structure):
     _fields_ = [("mom32", _P), ("mom64", _P), ("vgrad", _P), ("s0", _P), ("l1", _P),
-                ("n_active", _P), ("residual", _P), ("totals", _P)]
+                ("n_active", _P), ("residual", _P), ("totals", _P), ("stop", _P)]
 
 
 class PairGraph(ctypes.Structure):
@@ -111,6 +111,9 @@ SIGNATURES = {
     "fm_epi_adam_steps": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel), _P,
                                          _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64, _P,
                                          _I32, _P, _SZ, _P]),
+    "fm_epi_adam_steps_z": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel), _P,
+                                           _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _P, _P,
+                                           _I32, _P, _SZ, _P]),
     "fm_epi_adam_steps_nccl": (ctypes.c_int, [ctypes.POINTER(PairGraph), ctypes.POINTER(QuadModel),
                                               _P, _P, _P, _I64, _I32, _F64, _F64, _F64, _F64, _F64,
                                               _P, _P, _P, _I32, _P, _SZ, _P]),

@@ -17,6 +17,7 @@
 #include <tuple>
 #include <vector>
 #include <cmath>
+#include <cstring>
 
 #include "fm_common.cuh"
 
@@ -887,6 +888,40 @@ __global__ void loss_final_kernel(const double* __restrict__ part, int nb, doubl
   }
 }
 
+// scale = 2/Z from a pass's fused totals {L1, Z, kept} (device), so the host
+// need not read Z back between the pass and the epoch (ref/epipolar.py:291,
+// `2.0 / Z` with Z an integer count: the same IEEE division)
+__global__ void sched_scale_kernel(double* sched, const double* totals) { sched[1] = 2.0 / totals[1]; }
+
+// Pinned staging for the per-call schedule upload: a pageable
+// cudaMemcpyAsync may wait for the stream, which would serialise the host
+// with the device between epochs.  A small ring of pinned buffers, each
+// reused only after its previous copy completed (event).
+constexpr int kSchedLen = 3 + 2 * kMaxSteps;
+struct PinnedSched {
+  double* host = nullptr;
+  cudaEvent_t done = nullptr;
+};
+std::mutex g_pin_mu;
+PinnedSched g_pin[8];
+int g_pin_next = 0;
+
+int upload_sched(const std::vector<double>& sched, double* dst, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  PinnedSched& slot = g_pin[g_pin_next];
+  g_pin_next = (g_pin_next + 1) % 8;
+  if (!slot.host) {
+    FM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&slot.host), kSchedLen * sizeof(double)));
+    FM_CUDA(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming));
+  } else {
+    FM_CUDA(cudaEventSynchronize(slot.done));  // its previous copy has been consumed
+  }
+  memcpy(slot.host, sched.data(), kSchedLen * sizeof(double));
+  FM_CUDA(cudaMemcpyAsync(dst, slot.host, kSchedLen * sizeof(double), cudaMemcpyHostToDevice, st));
+  FM_CUDA(cudaEventRecord(slot.done, st));
+  return FM_OK;
+}
+
 __global__ void set_sched_kernel(double* sched, double lr, double scale, unsigned int* ticket) {
   sched[0] = lr;
   sched[1] = scale;
@@ -1155,7 +1190,8 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
                     double* adam_v, int64_t t0, int32_t n_steps, double lr, double beta1,
                     double beta2, double eps, double scale, int32_t* flag, int32_t use_graph,
                     void* scratch, size_t scratch_bytes, void* stream, bool dist, void* comm,
-                    double* gbuf, const fm_peer_group* peer = nullptr) {
+                    double* gbuf, const fm_peer_group* peer = nullptr,
+                    const double* totals = nullptr) {
   if (int rc = check_graph(g)) return rc;
   if (int rc = check_quad(q)) return rc;
   FM_REQUIRE(flag, "fm_epi_adam_steps needs a device flag word");
@@ -1171,7 +1207,7 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
     const int chunk = std::min<int32_t>(n_steps - done, kMaxSteps);
     // schedule: lr, 2/Z, and the bias corrections 1 - beta^t computed with the
     // host pow() exactly as ref/optim.py:34-35 does
-    std::vector<double> sched(3 + 2 * kMaxSteps, 1.0);
+    std::vector<double> sched(kSchedLen, 1.0);
     sched[0] = lr;
     sched[1] = scale;
     sched[2 + 2 * kMaxSteps] = peer ? (double)(peer->epoch + done) : 0.0;  // peer step ids
@@ -1180,8 +1216,11 @@ int adam_steps_impl(const fm_pair_graph* g, const fm_quad_model* q, double* para
       sched[2 + k] = 1.0 - pow(beta1, t);
       sched[2 + kMaxSteps + k] = 1.0 - pow(beta2, t);
     }
-    FM_CUDA(cudaMemcpyAsync(s.sched, sched.data(), sched.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, st));
+    if (int rc = upload_sched(sched, s.sched, st)) return rc;
+    if (totals) {
+      sched_scale_kernel<<<1, 1, 0, st>>>(s.sched, totals);
+      FM_LAUNCHED(sched_scale_kernel);
+    }
     auto enqueue = [&](cudaStream_t cs) {
       if (peer) {
         PeerArgs pa{peer->n_ranks, peer->rank, peer->part, peer->ready,
@@ -1254,6 +1293,16 @@ int fm_epi_adam_steps(const fm_pair_graph* g, const fm_quad_model* q, double* pa
                       int32_t use_graph, void* scratch, size_t scratch_bytes, void* stream) {
   return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, scale,
                          flag, use_graph, scratch, scratch_bytes, stream, false, nullptr, nullptr);
+}
+
+int fm_epi_adam_steps_z(const fm_pair_graph* g, const fm_quad_model* q, double* params,
+                        double* adam_m, double* adam_v, int64_t t0, int32_t n_steps, double lr,
+                        double beta1, double beta2, double eps, const double* totals, int32_t* flag,
+                        int32_t use_graph, void* scratch, size_t scratch_bytes, void* stream) {
+  FM_REQUIRE(totals, "fm_epi_adam_steps_z needs the pass totals {L1, Z, kept}");
+  return adam_steps_impl(g, q, params, adam_m, adam_v, t0, n_steps, lr, beta1, beta2, eps, 0.0,
+                         flag, use_graph, scratch, scratch_bytes, stream, false, nullptr, nullptr,
+                         nullptr, totals);
 }
 
 int fm_epi_adam_steps_nccl(const fm_pair_graph* g, const fm_quad_model* q, double* params,

@@ -452,6 +452,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   constexpr int S = L / 4;     // blocks per iteration
   static_assert(L == 4 || L == 8 || L == 16, "L in {4, 8, 16}");
 
+  if (out.stop && *out.stop) return;  // an earlier stage failed: leave everything alone
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -769,6 +770,7 @@ point_pass_generic(const fm_point_store s, const double* __restrict__ ghat,
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (item >= s.n_items) return;
+  if (out.stop && *out.stop) return;  // an earlier stage failed: leave everything alone
   const int n = s.item_pair[item];
   const int first = s.pair_item_off[n];
   const bool single = (s.pair_item_off[n + 1] - first) == 1;

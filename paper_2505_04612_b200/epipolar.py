@@ -384,13 +384,21 @@ class IrlsEngine:
                                      N.ptr(self.buf.ghat0), N.ptr(self.flag), N.ptr(self.gscratch),
                                      self.gscratch.numel(), N.stream_handle()))
 
-    def point_pass(self, mode, threshold, cur, prev):
+    def point_pass(self, mode, threshold, cur, prev, totals=None, stop=None):
+        """One fused pass into buffer `cur`; its {L1, Z, kept} go to `totals`
+        (default buf.tot).  stop: a device error word that, when raised,
+        makes the pass a no-op (the asynchronous schedule in _run)."""
         if mode & N.FM_PASS_MOMENTS:
             mode |= self.buf.flags
         torch.cuda.nvtx.range_push(f"fm/point_pass 0x{mode:x}")
+        out = self.buf.out(cur)
+        if totals is not None:
+            out["totals"] = totals
+        if stop is not None:
+            out["stop"] = stop
         _pass(self.store, mode, threshold, ghat=self.buf.ghat0,
               prev_active=self.buf.n_active[prev] if (mode & N.FM_PASS_SKIP_DROPPED) else None,
-              out=self.buf.out(cur), scratch=self.pscratch)
+              out=out, scratch=self.pscratch)
         torch.cuda.nvtx.range_pop()
 
     def run(self):
@@ -401,15 +409,24 @@ class IrlsEngine:
             torch.cuda.nvtx.range_pop()
 
     def _run(self):
+        """The schedule of ref/epipolar.py:278-319, enqueued without a host
+        round trip: every pass writes its {L1, Z, kept} into its own row of
+        a device history, each epoch reads its round's 2/Z on the device
+        (fm_epi_adam_steps_z), the error word is snapshotted after every
+        stage, and a raised word turns the later passes into no-ops (masks
+        stay as at the first error).  One synchronisation at the end then
+        replays the reference's checks in its order."""
         cfg = self.cfg
         P = self.graph.n_pairs
         thresholds = prune_thresholds(cfg)
-        l1_history = []
+        iters = cfg.irls_iters_between_prunes
+        steps = cfg.epipolar_epoch_steps
+        n_pass = len(thresholds) * iters + 1
+        hist = torch.zeros((n_pass, 3), dtype=torch.float64, device=self.device)
+        flags = torch.zeros(2 * n_pass, dtype=torch.int32, device=self.device)
+        k = f = 0
         lr = cfg.epipolar_lr
         cur = 0
-        Z = None
-        dropped = 0
-        kept = P
         for rnd, th in enumerate(thresholds):
             self._ghat()
             mode = N.FM_PASS_PRUNE | N.FM_PASS_MOMENTS | N.FM_PASS_IRLS
@@ -417,46 +434,70 @@ class IrlsEngine:
                 mode |= N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED
             prev = cur
             cur = 1 - cur
-            self.point_pass(mode, th, cur, prev)
-            l1_sum, z, kept = self.buf.tot.cpu().numpy()
-            if rnd > 0:
-                l1_history.append(float(l1_sum) / Z)
-            Z, kept = int(z), int(kept)
-            N.raise_flag(self.flag.item())
-            dropped = P - kept
-            if kept == 0:
-                self.dropped = dropped
-                raise ValueError("all pairs pruned away")
+            round_tot = hist[k]
+            self.point_pass(mode, th, cur, prev, totals=round_tot, stop=self.flag)
+            k += 1
+            flags[f].copy_(self.flag[0])
+            f += 1
             self.adam_m.zero_()
             self.adam_v.zero_()
-            steps = cfg.epipolar_epoch_steps
-            for it in range(cfg.irls_iters_between_prunes):
+            for it in range(iters):
                 if it > 0:
                     self._ghat()
                     self.point_pass(N.FM_PASS_MOMENTS | N.FM_PASS_IRLS | N.FM_PASS_SKIP_DROPPED,
-                                    0.0, 1 - cur, cur)
+                                    0.0, 1 - cur, cur, totals=hist[k], stop=self.flag)
+                    k += 1
                     # counts unchanged (no prune); keep the current buffer authoritative
                     self.buf.n_active[cur], self.buf.n_active[1 - cur] = \
                         self.buf.n_active[1 - cur], self.buf.n_active[cur]
+                    flags[f].copy_(self.flag[0])
+                    f += 1
                 torch.cuda.nvtx.range_push("fm/adam_steps")
-                N.check(self.lib.fm_epi_adam_steps(
+                N.check(self.lib.fm_epi_adam_steps_z(
                     ctypes.byref(self.graph.struct()), ctypes.byref(self.buf.quad),
                     N.ptr(self.params), N.ptr(self.adam_m), N.ptr(self.adam_v),
                     it * steps, steps, lr, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
-                    2.0 / Z, N.ptr(self.flag), int(self.use_graph), N.ptr(self.gscratch),
+                    N.ptr(round_tot), N.ptr(self.flag), int(self.use_graph), N.ptr(self.gscratch),
                     self.gscratch.numel(), N.stream_handle()))
                 torch.cuda.nvtx.range_pop()
-                N.raise_flag(self.flag.item())
+                flags[f].copy_(self.flag[0])
+                f += 1
             lr /= cfg.lr_decay
         self._ghat()
-        prev = cur
-        self.point_pass(N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED, 0.0, 1 - cur, cur)
+        self.point_pass(N.FM_PASS_L1 | N.FM_PASS_SKIP_DROPPED, 0.0, 1 - cur, cur, totals=hist[k],
+                        stop=self.flag)
         self.buf.n_active[cur], self.buf.n_active[1 - cur] = \
             self.buf.n_active[1 - cur], self.buf.n_active[cur]
-        l1_sum = float(self.buf.tot.cpu().numpy()[0])
-        N.raise_flag(self.flag.item())
-        l1_history.append(l1_sum / Z)
-        self.dropped = dropped
+        flags[f].copy_(self.flag[0])
+        self.buf.tot.copy_(hist[k])
+        # the one synchronisation; the reference's checks in its order
+        H = hist.cpu().numpy()
+        F = flags.cpu().numpy()
+        l1_history = []
+        k = f = 0
+        Z = None
+        kept = P
+        for rnd in range(len(thresholds)):
+            l1_sum, z, kept_r = H[k]
+            k += 1
+            if rnd > 0:
+                l1_history.append(float(l1_sum) / Z)
+            Z, kept = int(z), int(kept_r)
+            N.raise_flag(int(F[f]))
+            f += 1
+            if kept == 0:
+                self.dropped = P
+                raise ValueError("all pairs pruned away")
+            for it in range(iters):
+                if it > 0:
+                    k += 1
+                    N.raise_flag(int(F[f]))
+                    f += 1
+                N.raise_flag(int(F[f]))
+                f += 1
+        N.raise_flag(int(F[f]))
+        l1_history.append(float(H[k][0]) / Z)
+        self.dropped = P - kept
         self.kept = kept
         return l1_history
 

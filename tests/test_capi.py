@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_device_count():
     from paper_2505_04612_b200 import _native
     lib = _native.lib()
-    assert lib.fm_abi_version() == 5
+    assert lib.fm_abi_version() == 6
     n = lib.fm_device_count()
     assert n == torch.cuda.device_count() or (n == 0 and not torch.cuda.is_available())
 

@@ -257,6 +257,28 @@ def test_errors_match_reference(golden_small):
     assert np.array_equal(E.precompute_weights(np.zeros((0, 3)), np.zeros((0, 3))), np.zeros((9, 9)))
 
 
+def test_error_mid_schedule_leaves_masks_at_the_error(golden_small):
+    """irls_refine enqueues its whole schedule and checks errors at the end;
+    a failure in round 1's epoch must still leave the caller's masks as the
+    reference leaves them -- pruned by round 1 only (ref/epipolar.py:283,
+    :306-307), not by the later rounds' passes (the stop word makes them
+    no-ops).  lr = inf blows the first Adam step up."""
+    g = golden_small
+    th = dict(prune_threshold_start=2e-3, prune_threshold_end=5e-4)  # rounds prune 432 -> 208 -> .. 96
+    ref_pairs = pairs_from(g, "irls_", E.EpipolarPair)
+    E.irls_refine(Poses(g["irls_R_in"].copy(), g["irls_c_in"].copy()), ref_pairs,
+                  Cfg(prune_rounds=1, **th), n_cameras=1)
+    want = np.concatenate([p.active for p in ref_pairs])
+    pairs = pairs_from(g, "irls_", E.EpipolarPair)
+    # the reference raises FloatingPointError('non-finite epipolar loss') here
+    with pytest.raises(FloatingPointError, match="non-finite epipolar loss"):
+        E.irls_refine(Poses(g["irls_R_in"].copy(), g["irls_c_in"].copy()), pairs,
+                      Cfg(epipolar_lr=float("inf"), **th), n_cameras=1)
+    got = np.concatenate([p.active for p in pairs])
+    assert 0 < int(want.sum()) < len(want)  # the reference: 208 of 432
+    assert np.array_equal(got, want)
+
+
 def test_nonfinite_pose_is_pruned_like_reference(golden_small):
     """NaN centres give NaN residuals; `NaN <= th` is False, so the reference
     prunes everything and raises 'all pairs pruned away'."""
