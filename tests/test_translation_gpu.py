@@ -206,3 +206,55 @@ def test_bitwise_over_wide_dynamic_range():
     assert loss == l_ref
     np.testing.assert_array_equal(grad, g_ref)
     np.testing.assert_array_equal(T.per_node_residuals(c, gr), O.per_node_residuals(c, ei, ej, d))
+
+
+def _descent(graph, init, steps, cluster):
+    """translation._align with the cluster-persistent path on or off."""
+    old = os.environ.pop("FM_TR_NOCLUSTER", None)
+    if not cluster:
+        os.environ["FM_TR_NOCLUSTER"] = "1"
+    try:
+        c, loss = T._align(T.device_graph(graph), init, Cfg(), steps)
+        return c.cpu().numpy(), loss
+    finally:
+        os.environ.pop("FM_TR_NOCLUSTER", None)
+        if old is not None:
+            os.environ["FM_TR_NOCLUSTER"] = old
+
+
+@pytest.mark.parametrize("B,steps", [(1, 1), (1, 250), (2, 7), (3, 250), (5, 33)])
+def test_cluster_descent_equals_per_step_launches(B, steps):
+    """Small graphs run the whole descent as one thread-block-cluster launch
+    (fm_translation.cu tr_steps_cluster_kernel); it must give the per-step
+    launches' results bit for bit: odd and even step counts (the ping-pong
+    parity), runs per warp 1 and 2 with idle run lanes (B = 3, 5), a hub
+    node of degree 300 (several incidence batches), duplicate edges and a
+    self-loop."""
+    rng = np.random.default_rng(B * 1000 + steps)
+    n, m = 48, 900
+    ei = rng.integers(0, n, size=m)
+    ej = rng.integers(0, n, size=m)
+    ei[:300] = 0                     # hub
+    ei[300:310], ej[300:310] = 4, 5  # duplicates
+    ei[310], ej[310] = 6, 6          # self-loop
+    d = rng.normal(size=(m, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    gr = T.DirectionGraph(n=n, edges_i=ei, edges_j=ej, directions=d)
+    init = rng.normal(size=(n, B, 3))
+    c1, l1 = _descent(gr, init, steps, cluster=True)
+    c2, l2 = _descent(gr, init, steps, cluster=False)
+    np.testing.assert_array_equal(c1, c2)
+    np.testing.assert_array_equal(l1, l2)
+    if B == 1 and steps == 1:  # and the numpy restatement of the reference
+        c_ref, l_ref = O.align_centers(n, ei, ej, d, Cfg(), init=init[:, 0], steps=steps)
+        np.testing.assert_array_equal(c1[:, 0], c_ref)
+        assert l1[0] == l_ref
+
+
+def test_cluster_descent_nonfinite_raises():
+    """A NaN direction makes the loss non-finite at the first step: the
+    cluster path raises the reference's error (ref/translation.py:150)."""
+    gr = T.DirectionGraph(n=4, edges_i=np.array([0, 1, 2]), edges_j=np.array([1, 2, 3]),
+                          directions=np.array([[1.0, 0, 0], [np.nan, 1.0, 0], [0, 0, 1.0]]))
+    with pytest.raises(FloatingPointError, match="non-finite translation loss"):
+        T.align_centers(gr, Cfg(translation_steps=20), seed=0)
