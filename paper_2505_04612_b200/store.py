@@ -289,20 +289,32 @@ class PointPairStore:
     def from_pairs(cls, pairs, device=None, chunk=CHUNK, all_active=False, sanitize=False,
                    fp64=False):
         """Build from EpipolarPair-like objects (reference or ours)."""
-        lengths = np.array([len(p.x1) for p in pairs], dtype=np.int64)
+        lengths = np.fromiter((len(p.x1) for p in pairs), dtype=np.int64, count=len(pairs))
         if len(pairs):
-            x1 = np.concatenate([np.asarray(p.x1, dtype=np.float64).reshape(-1, 3) for p in pairs])
-            x2 = np.concatenate([np.asarray(p.x2, dtype=np.float64).reshape(-1, 3) for p in pairs])
-            act = None if all_active else np.concatenate(
-                [np.asarray(p.active, dtype=bool).reshape(-1) for p in pairs])
+            x1 = _stack_rows([p.x1 for p in pairs], np.float64, 3)
+            x2 = _stack_rows([p.x2 for p in pairs], np.float64, 3)
+            act = None if all_active else _stack_rows([p.active for p in pairs], bool, None)
         else:
             x1 = np.zeros((0, 3))
             x2 = np.zeros((0, 3))
             act = None
-        i = np.array([p.i for p in pairs], dtype=np.int64)
-        j = np.array([p.j for p in pairs], dtype=np.int64)
+        i = np.fromiter((p.i for p in pairs), dtype=np.int64, count=len(pairs))
+        j = np.fromiter((p.j for p in pairs), dtype=np.int64, count=len(pairs))
         return cls(x1, x2, lengths, i, j, active=act, device=device, chunk=chunk, sanitize=sanitize,
                    fp64=fp64)
+
+
+def _stack_rows(arrays, dtype, width):
+    """np.concatenate of per-pair arrays as (-1, width) (or flat) `dtype`
+    rows: one concatenate when every array already has that dtype and shape
+    (the pipeline's EpipolarPair), else a per-array conversion."""
+    def ok(a):
+        return (isinstance(a, np.ndarray) and a.dtype == dtype
+                and (a.ndim == 1 if width is None else (a.ndim == 2 and a.shape[1] == width)))
+    if all(ok(a) for a in arrays):
+        return np.concatenate(arrays)
+    shape = (-1,) if width is None else (-1, width)
+    return np.concatenate([np.asarray(a, dtype=dtype).reshape(shape) for a in arrays])
 
 
 def csr(keys, n_keys, payload):
