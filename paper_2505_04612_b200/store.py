@@ -291,9 +291,9 @@ class PointPairStore:
         """Build from EpipolarPair-like objects (reference or ours)."""
         lengths = np.fromiter((len(p.x1) for p in pairs), dtype=np.int64, count=len(pairs))
         if len(pairs):
-            x1 = _stack_rows([p.x1 for p in pairs], np.float64, 3)
-            x2 = _stack_rows([p.x2 for p in pairs], np.float64, 3)
-            act = None if all_active else _stack_rows([p.active for p in pairs], bool, None)
+            x1 = _stack_rows([p.x1 for p in pairs], np.float64, 3, "x1")
+            x2 = _stack_rows([p.x2 for p in pairs], np.float64, 3, "x2")
+            act = None if all_active else _stack_rows([p.active for p in pairs], bool, None, "act")
         else:
             x1 = np.zeros((0, 3))
             x2 = np.zeros((0, 3))
@@ -304,17 +304,49 @@ class PointPairStore:
                    fp64=fp64)
 
 
-def _stack_rows(arrays, dtype, width):
+# Host staging of the API store build: page-locked, reused across calls
+# (grow-only, per column), so the concatenation writes warm pages and the
+# upload is a DMA at full PCIe speed instead of a staged pageable copy.
+# Calls are stream-ordered and synchronised at their end (irls_refine and
+# the API functions read results back), so a buffer is free again when the
+# next call fills it.  Columns above the cap use ordinary memory.
+_STAGE = {}
+_STAGE_CAP = 1 << 30  # bytes per column
+
+
+def _staging(name, n, dtype):
+    """A page-locked numpy array of n `dtype` values (a view of a cached
+    pinned buffer), or None when it would exceed the cap or pinning fails."""
+    nbytes = int(n) * np.dtype(dtype).itemsize
+    if nbytes == 0 or nbytes > _STAGE_CAP or not torch.cuda.is_available():
+        return None
+    buf = _STAGE.get(name)
+    if buf is None or buf.numel() < nbytes:
+        try:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        except RuntimeError:
+            return None
+        _STAGE[name] = buf
+    return buf.numpy()[:nbytes].view(dtype)
+
+
+def _stack_rows(arrays, dtype, width, stage=None):
     """np.concatenate of per-pair arrays as (-1, width) (or flat) `dtype`
     rows: one concatenate when every array already has that dtype and shape
-    (the pipeline's EpipolarPair), else a per-array conversion."""
+    (the pipeline's EpipolarPair), else a per-array conversion.  stage: name
+    of a pinned staging buffer to concatenate into."""
     def ok(a):
         return (isinstance(a, np.ndarray) and a.dtype == dtype
                 and (a.ndim == 1 if width is None else (a.ndim == 2 and a.shape[1] == width)))
-    if all(ok(a) for a in arrays):
+    if not all(ok(a) for a in arrays):
+        shape = (-1,) if width is None else (-1, width)
+        arrays = [np.asarray(a, dtype=dtype).reshape(shape) for a in arrays]
+    rows = sum(len(a) for a in arrays)
+    out = _staging(stage, rows * (width or 1), dtype) if stage else None
+    if out is None:
         return np.concatenate(arrays)
-    shape = (-1,) if width is None else (-1, width)
-    return np.concatenate([np.asarray(a, dtype=dtype).reshape(shape) for a in arrays])
+    out = out.reshape((rows,) if width is None else (rows, width))
+    return np.concatenate(arrays, out=out)
 
 
 def csr(keys, n_keys, payload):
