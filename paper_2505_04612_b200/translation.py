@@ -18,6 +18,7 @@ and so do the cheirality counts (``fm_depth_counts``).
 """
 
 import ctypes
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -36,29 +37,61 @@ class PairRejected(ValueError):
     ``except translation.PairRejected`` catches ours."""
 
 
-def fibonacci_sphere(n):
-    """The reference's deterministic unit-sphere lattice of n points
-    (ref/translation.py:23-29)."""
+@functools.lru_cache(maxsize=8)
+def _fibonacci_sphere(n):
     k = np.arange(n, dtype=np.float64) + 0.5
     z = 1.0 - 2.0 * k / n
     r = np.sqrt(np.maximum(1.0 - z * z, 0.0))
     phi = _GOLDEN_ANGLE * k
-    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+    out = np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+    out.setflags(write=False)
+    return out
+
+
+def fibonacci_sphere(n):
+    """The reference's deterministic unit-sphere lattice of n points
+    (ref/translation.py:23-29); computed once per n."""
+    return _fibonacci_sphere(int(n)).copy()
+
+
+_LATTICE_DEV = {}
+
+
+def _lattice_on(device, n):
+    """fibonacci_sphere(n) resident on the device (uploaded once)."""
+    key = (str(device), int(n))
+    t = _LATTICE_DEV.get(key)
+    if t is None:
+        t = _LATTICE_DEV[key] = torch.as_tensor(_fibonacci_sphere(int(n)).copy(), device=device)
+    return t
+
+
+@functools.lru_cache(maxsize=32)
+def _cap_local(radius, n):
+    """The axis-independent spiral of _cap_samples (cached per radius / n)."""
+    k = np.arange(n, dtype=np.float64) + 0.5
+    theta = radius * np.sqrt(k / n)
+    phi = _GOLDEN_ANGLE * k
+    out = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)],
+                   axis=1)
+    out.setflags(write=False)
+    return out
+
+
+def _cross(a, b):
+    # np.cross of two 3-vectors: the same products and differences
+    return np.array([a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]])
 
 
 def _cap_samples(axis, radius, n):
     """Spiral of n directions within angle `radius` of `axis`
     (ref/translation.py:32-49)."""
-    k = np.arange(n, dtype=np.float64) + 0.5
-    theta = radius * np.sqrt(k / n)
-    phi = _GOLDEN_ANGLE * k
-    local = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)],
-                     axis=1)
+    local = _cap_local(float(radius), int(n))
     axis = axis / np.linalg.norm(axis)
     ref = np.array([1.0, 0.0, 0.0]) if abs(axis[2]) > 0.9 else np.array([0.0, 0.0, 1.0])
-    u = np.cross(ref, axis)
+    u = _cross(ref, axis)
     u /= np.linalg.norm(u)
-    v = np.cross(axis, u)
+    v = _cross(axis, u)
     return local @ np.stack([u, v, axis], axis=1).T
 
 
@@ -98,29 +131,33 @@ def reestimate_relative_batch(x1s, x2s, rel_rotations, cfg):
         ks = live[lo:lo + 65535]
         lens = np.array([len(x1s[k]) for k in ks], dtype=np.int64)
         off = torch.as_tensor(np.concatenate([[0], np.cumsum(lens)]), device=device)
-        X1 = torch.as_tensor(np.concatenate([x1s[k] for k in ks]), device=device)
-        X2 = torch.as_tensor(np.concatenate([x2s[k] for k in ks]), device=device)
-        R = torch.as_tensor(np.ascontiguousarray(np.stack([rel_rotations[k] for k in ks]),
-                                                 dtype=np.float64), device=device)
-        B = len(ks)
+        Z, B = int(lens.sum()), len(ks)
+        # points of both sides and the rotations in one upload
+        host = np.concatenate([np.concatenate([x1s[k] for k in ks]).ravel(),
+                               np.concatenate([x2s[k] for k in ks]).ravel(),
+                               np.ascontiguousarray(np.stack([rel_rotations[k] for k in ks]),
+                                                    dtype=np.float64).ravel()])
+        dev = torch.as_tensor(host, device=device)
+        X1, X2, R = dev[:3 * Z], dev[3 * Z:6 * Z], dev[6 * Z:]
+        e = torch.empty((B, n), dtype=torch.float64, device=device)
 
-        def errors(cands, stride):
-            d = torch.as_tensor(np.ascontiguousarray(cands), device=device)
-            e = torch.empty((B, n), dtype=torch.float64, device=device)
+        def errors(d, stride):
+            if not isinstance(d, torch.Tensor):
+                d = torch.as_tensor(np.ascontiguousarray(d), device=device)
             N.check(lib.fm_sphere_errors_batch(N.ptr(X1), N.ptr(X2), N.ptr(off), B, N.ptr(R),
                                                N.ptr(d), stride, n, N.ptr(e), N.stream_handle()))
             return e.cpu().numpy()
 
-        lattice = fibonacci_sphere(n)
-        err = errors(lattice, 0)
+        lattice = _fibonacci_sphere(n)
+        err = errors(_lattice_on(device, n), 0)
         med = np.median(err, axis=1)
         flat = (med < 1e-15) | (np.min(err, axis=1) > 0.9 * med)
         best = lattice[np.argmin(err, axis=1)]
         radius = 2.0 * np.sqrt(4.0 * np.pi / n)
         for _ in range(int(cfg.sphere_refine_levels)):
             cands = np.stack([_cap_samples(best[q], radius, n) for q in range(B)])
-            e = errors(cands, 3 * n)
-            best = cands[np.arange(B), np.argmin(e, axis=1)]
+            err_l = errors(cands, 3 * n)
+            best = cands[np.arange(B), np.argmin(err_l, axis=1)]
             radius *= 2.0 * np.sqrt(np.pi / n)
         t = torch.as_tensor(np.ascontiguousarray(best), device=device)
         counts = torch.empty((B, 2), dtype=torch.int32, device=device)
