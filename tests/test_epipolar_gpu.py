@@ -465,3 +465,26 @@ def test_irls_refine_focal_paths_match_oracle(n_cams):
     np.testing.assert_allclose(fs, ofs, rtol=1e-6)
     np.testing.assert_allclose(out.rotations, R, atol=1e-6)
     np.testing.assert_allclose(out.centers, c, atol=1e-6)
+
+
+def test_repeated_calls_reuse_staging(golden_small, golden_c1):
+    """The API store build concatenates into reused page-locked staging
+    buffers (store._STAGE): a small call, a larger one (the buffers grow)
+    and the small one again give identical results and masks."""
+    g = golden_small
+
+    def small():
+        pairs = pairs_from(g, "irls_", E.EpipolarPair)
+        out, fs, rep = E.irls_refine(Poses(g["irls_R_in"].copy(), g["irls_c_in"].copy()), pairs,
+                                     Cfg(epipolar_lr=1e-3), n_cameras=1)
+        return out, rep, np.concatenate([p.active for p in pairs])
+
+    a = small()
+    pairs = c1_pairs(golden_c1, E.EpipolarPair)
+    E.irls_refine(Poses(golden_c1["c1_R_in"].copy(), golden_c1["c1_c_in"].copy()), pairs, Cfg(),
+                  n_cameras=1)
+    b = small()
+    np.testing.assert_array_equal(a[0].rotations, b[0].rotations)
+    np.testing.assert_array_equal(a[0].centers, b[0].centers)
+    assert a[1]["l1_history"] == b[1]["l1_history"]
+    np.testing.assert_array_equal(a[2], b[2])
