@@ -390,7 +390,7 @@ class IrlsEngine:
         makes the pass a no-op (the asynchronous schedule in _run)."""
         if mode & N.FM_PASS_MOMENTS:
             mode |= self.buf.flags
-        torch.cuda.nvtx.range_push(f"fm/point_pass 0x{mode:x}")
+        torch.cuda.nvtx.range_push(f"fm.point_pass 0x{mode:x}")
         out = self.buf.out(cur)
         if totals is not None:
             out["totals"] = totals
@@ -402,7 +402,7 @@ class IrlsEngine:
         torch.cuda.nvtx.range_pop()
 
     def run(self):
-        torch.cuda.nvtx.range_push("fm/irls_refine")
+        torch.cuda.nvtx.range_push("fm.irls_refine")
         try:
             return self._run()
         finally:
@@ -452,7 +452,7 @@ class IrlsEngine:
                         self.buf.n_active[1 - cur], self.buf.n_active[cur]
                     flags[f].copy_(self.flag[0])
                     f += 1
-                torch.cuda.nvtx.range_push("fm/adam_steps")
+                torch.cuda.nvtx.range_push("fm.adam_steps")
                 N.check(self.lib.fm_epi_adam_steps_z(
                     ctypes.byref(self.graph.struct()), ctypes.byref(self.buf.quad),
                     N.ptr(self.params), N.ptr(self.adam_m), N.ptr(self.adam_v),
