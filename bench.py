@@ -919,6 +919,25 @@ def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10, sin
            "parity_check": {k: chk[k] for k in ("pairs", "points", "ok", "masks", "counts",
                                                  "W_max_rel_err")},
            "parity_sample": "200 image pairs spread evenly over the (rank-0) range"}
+    if world == 1:
+        # the whole irls_refine schedule on the full config (one GPU): the
+        # point passes dominate here, the Adam steps at C2
+        with torch.cuda.stream(stream):
+            store.reset_active()
+            times = []
+            for _ in range(2):  # the first call captures the step graphs
+                store.reset_active()
+                p0 = eng.params.clone()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                l1h = eng.run()
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+                eng.params.copy_(p0)
+        out.update({"irls_refine_s": times[-1], "irls_refine_first_s": times[0],
+                    "irls_l1_history": l1h,
+                    "irls_note": "irls_refine (3 prune rounds x 3 IRLS x 100 Adam steps) on the "
+                                 "whole config, store on the device; second call"})
     del eng, store, graph
     gc.collect()
     torch.cuda.empty_cache()
