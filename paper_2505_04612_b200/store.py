@@ -314,6 +314,12 @@ _STAGE = {}
 _STAGE_CAP = 1 << 30  # bytes per column
 
 
+def release_staging():
+    """Free the page-locked staging buffers of the API store build (they
+    are kept between calls; the next call allocates them again)."""
+    _STAGE.clear()
+
+
 def _staging(name, n, dtype):
     """A page-locked numpy array of n `dtype` values (a view of a cached
     pinned buffer), or None when it would exceed the cap or pinning fails."""
