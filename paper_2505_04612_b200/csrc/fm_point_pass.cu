@@ -427,9 +427,16 @@ __device__ __forceinline__ void group_transpose_reduce(T (&v)[N], int lane) {
 // Per-lane ring: stage d holds the lane's two chunks of x1 then of x2
 // (chunk-major: a warp's LDS.128 of one chunk row touches 32 consecutive
 // 16-byte words) and the mask word of the lane's block.
+// Stage-major: a lane's mask slot sits at a fixed (per-lane) distance from its
+// chunk slots in the same stage, so one running stage address serves the
+// copies, the chunk reads and the mask read (no per-iteration stage index
+// arithmetic).
+struct LaneStage {
+  float4 c[4][32];
+  uint32_t m[32];
+};
 struct LaneRing {
-  float4 c[kRing][4][32];
-  uint32_t m[kRing][32];
+  LaneStage s[kRing];
 };
 
 // L = 4 S lanes per work item: S sub-groups of 4 lanes; iteration `it`
@@ -489,19 +496,20 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   uint32_t* mwb_w = reinterpret_cast<uint32_t*>(s.active) + (d.lo >> 5);
 
   constexpr uint32_t kChunkB = 32 * 16;  // one chunk row of the warp
-  constexpr uint32_t kStageC = 4 * kChunkB;
-  constexpr uint32_t kStageM = 32 * 4;
-  const uint32_t ring_c = smem_u32(&ring.c[0][0][lane]);
-  const uint32_t ring_m = smem_u32(&ring.m[0][lane]);
-  auto issue = [&](int it, uint32_t st) {
+  constexpr uint32_t kStageB = sizeof(LaneStage);
+  // this lane's chunk-0 slot of stage 0; its mask slot of a stage is mdelta on
+  const uint32_t ring0 = smem_u32(&ring.s[0].c[0][lane]);
+  const uint32_t ring_last = ring0 + (kRing - 1) * kStageB;
+  const uint32_t mdelta = 4 * kChunkB - 12 * lane;
+  auto issue = [&](int it, uint32_t dst) {
     if (!FM_HOT_NOLOAD && S * it + sg < nblk) {
       const float4* p1 = x1b + 8 * S * it;
       const float4* p2 = x2b + 8 * S * it;
-      cp_async16(ring_c + st * kStageC, p1);
-      cp_async16(ring_c + st * kStageC + kChunkB, p1 + 4);
-      cp_async16(ring_c + st * kStageC + 2 * kChunkB, p2);
-      cp_async16(ring_c + st * kStageC + 3 * kChunkB, p2 + 4);
-      cp_async4(ring_m + st * kStageM, mwb + ((half0 + kBlkSlots * S * it) >> 5));
+      cp_async16(dst, p1);
+      cp_async16(dst + kChunkB, p1 + 4);
+      cp_async16(dst + 2 * kChunkB, p2);
+      cp_async16(dst + 3 * kChunkB, p2 + 4);
+      cp_async4(dst + mdelta, mwb + ((half0 + kBlkSlots * S * it) >> 5));
     }
     cp_async_commit();
   };
@@ -509,39 +517,42 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
 #pragma unroll
     for (int st = 0; st < kRing; ++st)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) ring.c[st][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < 4; ++c) ring.s[st].c[c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncwarp();
 #pragma unroll
-  for (int it = 0; it < kRing - 1; ++it) issue(it, it);
+  for (int it = 0; it < kRing - 1; ++it) issue(it, ring0 + it * kStageB);
 
   HotAcc<kPrune, kL1, kMom, MOM64> acc;
   acc.zero();
-  uint32_t st_issue = kRing - 1, st_read = 0;
+  // cur: the stage read this iteration; prv: the one read last iteration,
+  // refilled now (kRing - 1 iterations ahead)
+  uint32_t cur = ring0, prv = ring_last;
 #pragma unroll kUnroll
   for (int it = 0; it < warp_it; ++it) {
-    issue(it + kRing - 1, st_issue);
-    st_issue = st_issue + 1 == kRing ? 0 : st_issue + 1;
+    issue(it + kRing - 1, prv);
     cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
     // a block past the item end reads mask 0: nothing counts, nothing is
     // pruned, weights are +0 (its stale ring bytes are finite)
     const int pos = half0 + kBlkSlots * S * it;  // block's first bit, relative to word lo/32
-    const uint32_t blk = (S * it + sg < nblk) ? (FM_HOT_NOLOAD ? 0xffffu : lds32(ring_m + st_read * kStageM) >> (pos & 31)) : 0u;
     // this lane's points: slots 2h, 2h+1 (chunk 0) and 2h+8, 2h+9 (chunk 1),
-    // i.e. bits 0, 1, 8, 9 of bh
-    const uint32_t bh = blk >> (2 * h);
+    // i.e. bits 0, 1, 8, 9 of bh (pos is a multiple of 16, so pos % 32 + 2h < 32)
+    const uint32_t bh = (S * it + sg < nblk)
+                            ? (FM_HOT_NOLOAD ? 0xffffu : lds32(cur + mdelta) >> ((pos & 31) + 2 * h))
+                            : 0u;
     uint32_t kept = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const float4 x1 = lds128(ring_c + st_read * kStageC + j * kChunkB);
-      const float4 x2 = lds128(ring_c + st_read * kStageC + (2 + j) * kChunkB);
-      kept |= (uint32_t)acc.point(G, x1.x, x1.y, x2.x, x2.y, (bh >> (8 * j)) & 1u, thr) << (8 * j);
-      kept |= (uint32_t)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bh >> (8 * j + 1)) & 1u, thr) << (8 * j + 1);
+      const float4 x1 = lds128(cur + j * kChunkB);
+      const float4 x2 = lds128(cur + (2 + j) * kChunkB);
+      kept |= (uint32_t)acc.point(G, x1.x, x1.y, x2.x, x2.y, (bh & (1u << (8 * j))) != 0u, thr) << (8 * j);
+      kept |= (uint32_t)acc.point(G, x1.z, x1.w, x2.z, x2.w, (bh & (2u << (8 * j))) != 0u, thr) << (8 * j + 1);
     }
     acc.cnt += __popc(kept);
     const uint32_t cleared = kPrune ? ((bh & 0x303u) & ~kept) << (2 * h) : 0u;
     if (kPrune && cleared) atomicAnd(mwb_w + (pos >> 5), ~(cleared << (pos & 31)));
-    st_read = st_read + 1 == kRing ? 0 : st_read + 1;
+    prv = cur;
+    cur = cur == ring_last ? ring0 : cur + kStageB;
   }
   cp_async_wait<0>();
   if (kL1 && kMom && !MOM64) acc.l1 = acc.l1f;
@@ -571,7 +582,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
     for (int k = 38; k < N; ++k) v[k] = 0.0;
     group_transpose_reduce<L>(v, lane);
     if (NI == P) {  // staged, row-coalesced stores (see the fp32 path)
-      double* stage = reinterpret_cast<double*>(&ring.c[0][0][0]);
+      double* stage = reinterpret_cast<double*>(&ring.s[0].c[0][0]);
       const int q = lane / L;
       __syncwarp();
 #pragma unroll
@@ -626,7 +637,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
       // every item is a whole pair (item == pair): stage the warp's sums in
       // its idle ring and write each output row as IPW consecutive pairs --
       // a handful of sectors per store instead of one per lane
-      float* stage = reinterpret_cast<float*>(&ring.c[0][0][0]);
+      float* stage = reinterpret_cast<float*>(&ring.s[0].c[0][0]);
       double* stage_l1 = reinterpret_cast<double*>(stage + N * IPW);
       const int q = lane / L;
       __syncwarp();

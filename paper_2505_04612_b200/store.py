@@ -121,8 +121,17 @@ class PointPairStore:
         x1 = np.asarray(x1, dtype=np.float64)
         x2 = np.asarray(x2, dtype=np.float64)
         dim = x1.shape[1] if x1.ndim == 2 and len(x1) else 2
-        homog = (not fp64 and dim == 3 and len(x1) > 0
-                 and not (np.all(x1[:, 2] == 1.0) and np.all(x2[:, 2] == 1.0)))
+        if self.n_points:
+            x1d = _dev(np.ascontiguousarray(x1), device)
+            x2d = _dev(np.ascontiguousarray(x2), device)
+            act = None if active is None else _dev(np.asarray(active, dtype=np.uint8), device)
+        else:  # pairs without points: nothing is read
+            x1d = x2d = torch.zeros((1, dim), dtype=torch.float64, device=device)
+            act = None
+        # z != 1 anywhere needs the homogeneous columns; decided on the device
+        # (a strided host scan of the z column cost ~30 ms per side at C2)
+        homog = (not fp64 and dim == 3 and self.n_points > 0
+                 and not bool(((x1d[:, 2] == 1.0).all() & (x2d[:, 2] == 1.0).all()).item()))
         self.homogeneous = bool(homog)
         self.x1d = self.x2d = self.x1 = self.x2 = self.x1z = self.x2z = None
         if fp64:
@@ -142,13 +151,6 @@ class PointPairStore:
         self.caller_start_d = _dev(self.caller_start, device)
         self.rank_d = _dev(self.rank, device)
         self._struct = None
-        if self.n_points:
-            x1d = _dev(np.ascontiguousarray(x1), device)
-            x2d = _dev(np.ascontiguousarray(x2), device)
-            act = None if active is None else _dev(np.asarray(active, dtype=np.uint8), device)
-        else:  # pairs without points: nothing is read
-            x1d = x2d = torch.zeros((1, dim), dtype=torch.float64, device=device)
-            act = None
         N.check(N.lib().fm_store_build(ctypes.byref(self.struct()), N.ptr(x1d), N.ptr(x2d), dim,
                                        N.ptr(act), N.ptr(self.caller_start_d), N.ptr(self.rank_d),
                                        int(sanitize), N.stream_handle()))
@@ -291,9 +293,10 @@ class PointPairStore:
         """Build from EpipolarPair-like objects (reference or ours)."""
         lengths = np.fromiter((len(p.x1) for p in pairs), dtype=np.int64, count=len(pairs))
         if len(pairs):
-            x1 = _stack_rows([p.x1 for p in pairs], np.float64, 3, "x1")
-            x2 = _stack_rows([p.x2 for p in pairs], np.float64, 3, "x2")
-            act = None if all_active else _stack_rows([p.active for p in pairs], bool, None, "act")
+            rows = int(lengths.sum())
+            x1 = _stack_rows([p.x1 for p in pairs], np.float64, 3, "x1", rows)
+            x2 = _stack_rows([p.x2 for p in pairs], np.float64, 3, "x2", rows)
+            act = None if all_active else _stack_rows([p.active for p in pairs], bool, None, "act", rows)
         else:
             x1 = np.zeros((0, 3))
             x2 = np.zeros((0, 3))
@@ -336,11 +339,22 @@ def _staging(name, n, dtype):
     return buf.numpy()[:nbytes].view(dtype)
 
 
-def _stack_rows(arrays, dtype, width, stage=None):
+def _stack_rows(arrays, dtype, width, stage=None, rows=None):
     """np.concatenate of per-pair arrays as (-1, width) (or flat) `dtype`
     rows: one concatenate when every array already has that dtype and shape
     (the pipeline's EpipolarPair), else a per-array conversion.  stage: name
-    of a pinned staging buffer to concatenate into."""
+    of a pinned staging buffer to concatenate into; rows: the row count when
+    the caller knows it (then the common case concatenates straight into the
+    staging buffer, numpy checking shapes and casts, with no per-array scan)."""
+    if rows is not None and stage:
+        out = _staging(stage, rows * (width or 1), dtype)
+        if out is not None:
+            out = out.reshape((rows,) if width is None else (rows, width))
+            try:
+                return np.concatenate(arrays, out=out, casting="safe")
+            except (ValueError, TypeError):
+                pass  # ragged widths / unsafe casts: the checked path below
+
     def ok(a):
         return (isinstance(a, np.ndarray) and a.dtype == dtype
                 and (a.ndim == 1 if width is None else (a.ndim == 2 and a.shape[1] == width)))
