@@ -100,3 +100,40 @@ def test_empty_and_all_active():
     st = S.PointPairStore(x1, x2, lens, ij[:, 0], ij[:, 1], device=dev)
     assert st.caller_masks().all()
     assert int(st.active_bits().sum().item()) == int(lens.sum())
+
+
+def test_from_pairs_input_forms_build_the_same_store():
+    """from_pairs concatenates straight into the pinned staging when every
+    pair holds (n, 3) arrays numpy can cast safely; other forms (fp32 arrays,
+    nested lists, integer masks) take the checked path.
+    All give the same device store, bit for bit."""
+    from types import SimpleNamespace as NS
+    dev = torch.device("cuda")
+    lens, ij, x1, x2, act = ragged(7, nan=False)
+    x1 = x1.astype(np.float32).astype(np.float64)  # exact in fp32 for the fp32 form
+    x2 = x2.astype(np.float32).astype(np.float64)
+    start = np.concatenate([[0], np.cumsum(lens)])
+
+    def pairs(f1, f2, fa):
+        return [NS(i=int(ij[k, 0]), j=int(ij[k, 1]), x1=f1(x1[start[k]:start[k + 1]]),
+                   x2=f2(x2[start[k]:start[k + 1]]), active=fa(act[start[k]:start[k + 1]]))
+                for k in range(len(lens))]
+
+    ident = lambda a: a.copy()  # noqa: E731
+    # the reference's EpipolarPair holds (M, 3) homogeneous x1 / x2 (ref/epipolar.py:26-27)
+    forms = {
+        "fp64": pairs(ident, ident, ident),
+        "fp32": pairs(lambda a: a.astype(np.float32), ident, ident),
+        "lists": pairs(lambda a: a.tolist(), ident, lambda a: a.tolist()),
+        "int_mask": pairs(ident, ident, lambda a: a.astype(np.int64)),
+    }
+    ref = None
+    for name, ps in forms.items():
+        st = S.PointPairStore.from_pairs(ps, device=dev)
+        got = (st.x1.cpu().numpy(), st.x2.cpu().numpy(), st.active.cpu().numpy(), st.homogeneous)
+        if ref is None:
+            ref = got
+            continue
+        for a, b in zip(ref[:3], got[:3]):
+            assert np.array_equal(a, b), name
+        assert got[3] is False, name
