@@ -457,7 +457,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   constexpr bool kSkip = MODE & FM_PASS_SKIP_DROPPED;
   constexpr int IPW = 32 / L;  // items per warp
   constexpr int S = L / 4;     // blocks per iteration
-  static_assert(L == 4 || L == 8 || L == 16, "L in {4, 8, 16}");
+  static_assert(L == 4 || L == 8 || L == 16 || L == 32, "L in {4, 8, 16, 32}");
 
   if (out.stop && *out.stop) return;  // an earlier stage failed: leave everything alone
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -572,7 +572,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   // outputs (consecutive items -> neighbouring SoA stores)
   const bool single = d.single;
   if (kMom && MOM64) {
-    constexpr int N = L <= 8 ? 40 : 48;  // 36 moments, count, l1, padding
+    constexpr int N = L <= 8 ? 40 : (L == 16 ? 48 : 64);  // 36 moments, count, l1, padding
     double v[N];
 #pragma unroll
     for (int k = 0; k < 36; ++k) v[k] = acc.M64[MOM64 ? k : 0];
@@ -617,7 +617,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
       }
     }
   } else if (kMom) {
-    constexpr int N = 48;  // 36 moments (hot order), 9 vgrad, count, s0, padding
+    constexpr int N = L == 32 ? 64 : 48;  // 36 moments (hot order), 9 vgrad, count, s0, padding
     float v[N];
 #pragma unroll
     for (int k = 0; k < 18; ++k) {
@@ -630,7 +630,8 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
     v[42] = acc.V2.x; v[43] = acc.V2.y; v[44] = acc.v22;
     v[45] = (float)acc.cnt;
     v[46] = acc.s0f;
-    v[47] = 0.f;
+#pragma unroll
+    for (int k = 47; k < N; ++k) v[k] = 0.f;
     group_transpose_reduce<L>(v, lane);
     const double l1 = kL1 ? group_sum<L>(acc.l1) : 0.0;
     if (NI == P) {
@@ -1058,6 +1059,7 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
       return launch_hot_mixed<MODE, MOM64, 4, 16>(s, thr, ghat, prev_active, out, part, stream, n1);
   }
   if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
+  if (pick == 32) return launch_hot_l<MODE, MOM64, 32>(s, thr, ghat, prev_active, out, part, stream);
   if (pick == 16) return launch_hot_l<MODE, MOM64, 16>(s, thr, ghat, prev_active, out, part, stream);
   if (pick == 8) return launch_hot_l<MODE, MOM64, 8>(s, thr, ghat, prev_active, out, part, stream);
   return launch_hot_l<MODE, MOM64, 4>(s, thr, ghat, prev_active, out, part, stream);

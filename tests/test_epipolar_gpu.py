@@ -90,12 +90,12 @@ def random_scene(n_images=8, n_points=700, seed=0, noise=2e-3):
     return Poses(rots, centers), [pairs[q] for q in perm]
 
 
-@pytest.mark.parametrize("lanes", ["4", "8", "16"])
+@pytest.mark.parametrize("lanes", ["4", "8", "16", "32"])
 @pytest.mark.parametrize("chunk,precision", [(8192, "fp64"), (128, "fp64"), (8192, "fp32"),
                                              (128, "fp32")])
 def test_hot_point_pass_matches_oracle(chunk, precision, lanes, monkeypatch):
     """Fused prune + IRLS moments + L1 (hot kernel) vs the fp64 oracle, for
-    every lane-group width L (FM_HOT_L: 1, 2 or 4 sub-groups per item, so
+    every lane-group width L (FM_HOT_L: 1, 2, 4 or 8 sub-groups per item, so
     items whose block count is not a multiple of the sub-groups exercise the
     idle-block path); chunk=128 splits pairs over several work items (combine
     path).  fp64 moments: W within 3e-7 (the IRLS weight uses a rounded
@@ -367,7 +367,7 @@ def test_l1_loss_with_nonfinite_active_point_is_nan(golden_small):
     assert np.isnan(loss)
 
 
-@pytest.mark.parametrize("lanes", ["4", "8", "16"])
+@pytest.mark.parametrize("lanes", ["4", "8", "16", "32"])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_hot_point_pass_ragged_and_empty_pairs(precision, lanes, monkeypatch):
     """Pair lengths around the 16-slot block (0, 1, 2, 15, 16, 17, 33, ...),
