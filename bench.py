@@ -888,7 +888,15 @@ def run_ours(args, spec, world, rank, local):
                          "peak_kind": hbm_kind, "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_model": "16.125 B per point read (pairs not dropped) + 292 B per "
                                         "image pair (fp32 moments; DESIGN.md 3.1)",
-                         "dropped_pairs_skipped": dropped},
+                         "dropped_pairs_skipped": dropped,
+                         # SURVEY 8(d)'s contract figure: 24.125 B per point pair (the
+                         # north-star store's 16 B coordinates + 8 B per-point image
+                         # columns + mask bit); this store keeps the image indices per
+                         # image pair, so `frac` above (the bytes this kernel moves) is
+                         # the physical one and this is the contract's unit
+                         "frac_survey_contract": points_read * 24.125 / (ms_kernel * 1e-3) / 1e9 / hbm,
+                         "survey_contract_note": "SURVEY.md 8(d): achieved = pairs/s x 24 B (+0.125 B "
+                                                 "mask) / peak; 60% target = 62 us per C2 pass"},
             "cpu_baseline": cpu,
             "e2e": {"value": Z_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
