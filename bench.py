@@ -876,7 +876,10 @@ def run_ours(args, spec, world, rank, local):
             "config": {**workload_config(args, spec, world, P, Z),
                        "evaluated_point_pairs_per_step": int(Z_all),
                        "evaluated_note": "the pass skips the points of pairs the first prune "
-                                         "dropped entirely; value counts evaluated point pairs"},
+                                         "dropped entirely; value counts evaluated point pairs",
+                       **({"pass_scalars_exchange": type(comm).__name__ + " ({L1, Z, kept} of "
+                           "every pass summed over the ranks inside the timed step)"}
+                          if world > 1 else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(args.config, args.precision),
                          "kernel_ms": ms_kernel,
