@@ -963,6 +963,18 @@ def strong_bench(args, device, stream, world, rank, cfg_name="c5", steps=10, sin
            "parity_check": {k: chk[k] for k in ("pairs", "points", "ok", "masks", "counts",
                                                  "W_max_rel_err")},
            "parity_sample": "200 image pairs spread evenly over the (rank-0) range"}
+    # per-GPU roofline of the step (this rank's shard; pass + totals [+ the
+    # scalar exchange at N > 1]); the C5 kernel's ncu traffic when committed
+    P_r = store.n_pairs
+    dropped = (eng.buf.n_active[0][:P_r] == 0).cpu().numpy()
+    pts = int(store.n_points - np.asarray(store.len_caller)[dropped].sum())
+    hbm, hbm_kind = peaks()
+    b = pass_bytes(pts, P_r, args.precision)
+    out["roofline_per_gpu"] = {"bound": "hbm", "achieved": b / (ms * 1e-3) / 1e9, "peak": hbm,
+                               "unit": "GB/s", "frac": b / (ms * 1e-3) / 1e9 / hbm,
+                               "peak_kind": hbm_kind, "algorithmic_bytes_per_launch": b,
+                               "traffic": ncu_traffic(cfg_name, args.precision) if world == 1 else None,
+                               "note": "bytes of this rank's shard / the step time (max over ranks)"}
     if world == 1:
         # the whole irls_refine schedule on the full config (one GPU): the
         # point passes dominate here, the Adam steps at C2
