@@ -211,7 +211,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // so 15 packed FFMA2 + 3 FADD2 cover the 36 moments -- plus the shifted-model
 // linearisation terms vgrad = sum w r t and s0 = sum w r^2.
 #ifndef FM_HOT_RING
-#define FM_HOT_RING 5
+#define FM_HOT_RING 4
 #endif
 #ifndef FM_HOT_UNROLL
 #define FM_HOT_UNROLL 1
@@ -435,16 +435,18 @@ struct LaneStage {
   float4 c[4][32];
   uint32_t m[32];
 };
-struct LaneRing {
-  LaneStage s[kRing];
+template <int RING>
+struct LaneRingT {
+  LaneStage s[RING];
 };
+using LaneRing = LaneRingT<kRing>;
 
 // L = 4 S lanes per work item: S sub-groups of 4 lanes; iteration `it`
 // covers blocks S*it .. S*it + S - 1 of the item, sub-group sg takes block
 // S*it + sg, and its lane h the 16-byte chunks h and h + 4 of each column
 // (slots {2h, 2h+1, 2h+8, 2h+9}): every copy instruction of a sub-group reads
 // whole 32-byte sectors.
-template <unsigned MODE, bool MOM64, int L>
+template <unsigned MODE, bool MOM64, int L, int RING = kRing>
 __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* __restrict__ ghat,
                                          const double thr, const int32_t* __restrict__ prev_active,
                                          const fm_pass_out& out, const PartialBufs& part,
@@ -463,7 +465,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  LaneRing& ring = reinterpret_cast<LaneRing*>(smem_raw)[wib];
+  LaneRingT<RING>& ring = reinterpret_cast<LaneRingT<RING>*>(smem_raw)[wib];
 #ifdef FM_HOT_TRACE
   const unsigned long long t_start = globaltimer();
 #endif
@@ -499,7 +501,7 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   constexpr uint32_t kStageB = sizeof(LaneStage);
   // this lane's chunk-0 slot of stage 0; its mask slot of a stage is mdelta on
   const uint32_t ring0 = smem_u32(&ring.s[0].c[0][lane]);
-  const uint32_t ring_last = ring0 + (kRing - 1) * kStageB;
+  const uint32_t ring_last = ring0 + (RING - 1) * kStageB;
   const uint32_t mdelta = 4 * kChunkB - 12 * lane;
   auto issue = [&](int it, uint32_t dst) {
     if (!FM_HOT_NOLOAD && S * it + sg < nblk) {
@@ -515,23 +517,23 @@ __device__ __forceinline__ void hot_body(const fm_point_store& s, const double* 
   };
   {  // stale stage bytes must be finite: zero this lane's ring slots once
 #pragma unroll
-    for (int st = 0; st < kRing; ++st)
+    for (int st = 0; st < RING; ++st)
 #pragma unroll
       for (int c = 0; c < 4; ++c) ring.s[st].c[c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncwarp();
 #pragma unroll
-  for (int it = 0; it < kRing - 1; ++it) issue(it, ring0 + it * kStageB);
+  for (int it = 0; it < RING - 1; ++it) issue(it, ring0 + it * kStageB);
 
   HotAcc<kPrune, kL1, kMom, MOM64> acc;
   acc.zero();
   // cur: the stage read this iteration; prv: the one read last iteration,
-  // refilled now (kRing - 1 iterations ahead)
+  // refilled now (RING - 1 iterations ahead)
   uint32_t cur = ring0, prv = ring_last;
 #pragma unroll kUnroll
   for (int it = 0; it < warp_it; ++it) {
-    issue(it + kRing - 1, prv);
-    cp_async_wait<kRing - 1>();  // this lane's copies of iteration `it` have landed
+    issue(it + RING - 1, prv);
+    cp_async_wait<RING - 1>();  // this lane's copies of iteration `it` have landed
     // a block past the item end reads mask 0: nothing counts, nothing is
     // pruned, weights are +0 (its stale ring bytes are finite)
     const int pos = half0 + kBlkSlots * S * it;  // block's first bit, relative to word lo/32
@@ -741,16 +743,16 @@ point_pass_hot(const fm_point_store s, const double* __restrict__ ghat, const do
 // efficient width, in whole waves), the rest with L2 > L1 lanes per item in
 // the blocks the scheduler dispatches last -- a tail item then takes
 // L1/L2 of the time, so the low-occupancy end of the launch shrinks.
-template <unsigned MODE, bool MOM64, int L1, int L2>
+template <unsigned MODE, bool MOM64, int L1, int L2, int RING>
 __global__ void __launch_bounds__(kGrpWarps * 32, MOM64 ? FM_HOT_MINB64 : FM_HOT_MINB)
 point_pass_hot_mixed(const fm_point_store s, const double* __restrict__ ghat, const double thr,
                      const int32_t* __restrict__ prev_active, const fm_pass_out out,
                      const PartialBufs part, const int64_t nb1, const int64_t n1) {
   if ((int64_t)blockIdx.x < nb1)
-    hot_body<MODE, MOM64, L1>(s, ghat, thr, prev_active, out, part,
+    hot_body<MODE, MOM64, L1, RING>(s, ghat, thr, prev_active, out, part,
                               (int64_t)blockIdx.x * kGrpWarps + (threadIdx.x >> 5), 0, s.n_items);
   else
-    hot_body<MODE, MOM64, L2>(s, ghat, thr, prev_active, out, part,
+    hot_body<MODE, MOM64, L2, RING>(s, ghat, thr, prev_active, out, part,
                               ((int64_t)blockIdx.x - nb1) * kGrpWarps + (threadIdx.x >> 5), n1, s.n_items);
 }
 
@@ -989,20 +991,20 @@ int launch_hot_l(const fm_point_store& s, double thr, const double* ghat, const 
   return FM_OK;
 }
 
-template <unsigned MODE, bool MOM64, int L1, int L2>
+template <unsigned MODE, bool MOM64, int L1, int L2, int RING>
 int launch_hot_mixed(const fm_point_store& s, double thr, const double* ghat,
                      const int32_t* prev_active, const fm_pass_out& out, const PartialBufs& part,
                      cudaStream_t stream, int64_t n1) {
-  const size_t smem = kGrpWarps * sizeof(LaneRing);
+  const size_t smem = kGrpWarps * sizeof(LaneRingT<RING>);
   static bool attr = false;
   if (!attr) {
-    FM_CUDA(cudaFuncSetAttribute(point_pass_hot_mixed<MODE, MOM64, L1, L2>,
+    FM_CUDA(cudaFuncSetAttribute(point_pass_hot_mixed<MODE, MOM64, L1, L2, RING>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   const int64_t nb1 = n1 / (kGrpWarps * (32 / L1));
   const int64_t nb2 = ceil_div(ceil_div(s.n_items - n1, 32 / L2), kGrpWarps);
-  point_pass_hot_mixed<MODE, MOM64, L1, L2><<<(unsigned)(nb1 + nb2), kGrpWarps * 32, smem, stream>>>(
+  point_pass_hot_mixed<MODE, MOM64, L1, L2, RING><<<(unsigned)(nb1 + nb2), kGrpWarps * 32, smem, stream>>>(
       s, ghat, thr, prev_active, out, part, nb1, n1);
   FM_LAUNCHED(point_pass_hot_mixed);
   if (s.n_items > s.n_pairs) {
@@ -1056,7 +1058,18 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     constexpr bool kMomPass = (MODE & FM_PASS_MOMENTS) && (MODE & FM_PASS_IRLS);
     if (kMomPass && mix && !getenv("FM_HOT_L") && n1 > 0 &&
         s.n_items > n1 && mean_blk >= 8)
-      return launch_hot_mixed<MODE, MOM64, 4, 16>(s, thr, ghat, prev_active, out, part, stream, n1);
+    {
+      // Ring depth (measured, ncu): a launch of at most two L = 4 waves
+      // (C2: one) runs faster with 3 stages per lane (less prologue per item,
+      // more L1 beside the smaller shared-memory ring: C2 47.5 -> 46.0 us
+      // from 5), long launches with 4 (C4 350.5 -> 348.0 us, C5 3156 ->
+      // 3152 us; 3 stages: 350.8 / 3183)
+      const char* env_r = getenv("FM_HOT_RING_PICK");  // tuning override: 3 or 4
+      const int ring = env_r ? atoi(env_r) : (n1 / G4 <= 2 ? 3 : 4);
+      if (ring == 3)
+        return launch_hot_mixed<MODE, MOM64, 4, 16, 3>(s, thr, ghat, prev_active, out, part, stream, n1);
+      return launch_hot_mixed<MODE, MOM64, 4, 16, 4>(s, thr, ghat, prev_active, out, part, stream, n1);
+    }
   }
   if (const char* env = getenv("FM_HOT_L")) pick = atoi(env);  // tuning override
   if (pick == 32) return launch_hot_l<MODE, MOM64, 32>(s, thr, ghat, prev_active, out, part, stream);

@@ -19,7 +19,7 @@ params = torch.as_tensor(scenes.initial_params(sc, ids), device=dev)
 eng = E.IrlsEngine(store, graph, params, HotPathConfig(), precision=prec)
 eng._ghat()
 eng.buf.n_active[0].fill_(1)
-for _ in range(4):
+for _ in range(int(os.environ.get("FM_PASSES", "4"))):
     eng.point_pass(modes[mode], 0.01, 0, 0)
 torch.cuda.synchronize()
 print("done")
