@@ -1047,7 +1047,7 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
       pick = L;
     }
   }
-  // Whole waves of L = 4 items, the rest of the launch at L = 16 (see
+  // Whole waves of L = 4 items, the rest of the launch at L = 8 or 16 (see
   // point_pass_hot_mixed) when that rest is under one wave.
   {
     const int64_t G4 = (int64_t)bps[0] * sm_count() * kGrpWarps * 8;  // items per L=4 wave
@@ -1059,15 +1059,17 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
     if (kMomPass && mix && !getenv("FM_HOT_L") && n1 > 0 &&
         s.n_items > n1 && mean_blk >= 8)
     {
-      // Ring depth (measured, ncu): a launch of at most two L = 4 waves
-      // (C2: one) runs faster with 3 stages per lane (less prologue per item,
-      // more L1 beside the smaller shared-memory ring: C2 47.5 -> 46.0 us
-      // from 5), long launches with 4 (C4 350.5 -> 348.0 us, C5 3156 ->
-      // 3152 us; 3 stages: 350.8 / 3183)
-      const char* env_r = getenv("FM_HOT_RING_PICK");  // tuning override: 3 or 4
-      const int ring = env_r ? atoi(env_r) : (n1 / G4 <= 2 ? 3 : 4);
-      if (ring == 3)
-        return launch_hot_mixed<MODE, MOM64, 4, 16, 3>(s, thr, ghat, prev_active, out, part, stream, n1);
+      // Short launches (at most two L = 4 waves; C2: one) run faster with 3
+      // ring stages per lane (less prologue per item, more L1 beside the
+      // smaller shared-memory ring) and the remainder at L = 8; long ones
+      // with 4 stages and the remainder at L = 16.  Measured (ncu medians,
+      // C2 / C4 / C5): 5 stages + L = 16 47.5 / 350.5 / 3156 us; 4 + 16
+      // 46.6 / 348.0 / 3152; 3 + 16 46.0 / 350.8 / 3183; 3 + 8 44.8 at C2;
+      // 4 + 8 348.3 / 3133 against 4 + 16 347.1 / 3130 on the same box.
+      const char* env_r = getenv("FM_HOT_SHORT");  // tuning override: 1 short form, 0 long form
+      const bool short_launch = env_r ? atoi(env_r) != 0 : n1 / G4 <= 2;
+      if (short_launch)
+        return launch_hot_mixed<MODE, MOM64, 4, 8, 3>(s, thr, ghat, prev_active, out, part, stream, n1);
       return launch_hot_mixed<MODE, MOM64, 4, 16, 4>(s, thr, ghat, prev_active, out, part, stream, n1);
     }
   }
