@@ -216,6 +216,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #ifndef FM_HOT_UNROLL
 #define FM_HOT_UNROLL 1
 #endif
+#ifndef FM_SHORT_RING
+#define FM_SHORT_RING 3  // ring stages of short mixed launches (see launch_hot)
+#endif
 #ifndef FM_HOT_MINB
 #define FM_HOT_MINB 4
 #endif
@@ -1069,7 +1072,7 @@ int launch_hot(const fm_point_store& s, double thr, const double* ghat, const in
       const char* env_r = getenv("FM_HOT_SHORT");  // tuning override: 1 short form, 0 long form
       const bool short_launch = env_r ? atoi(env_r) != 0 : n1 / G4 <= 2;
       if (short_launch)
-        return launch_hot_mixed<MODE, MOM64, 4, 8, 3>(s, thr, ghat, prev_active, out, part, stream, n1);
+        return launch_hot_mixed<MODE, MOM64, 4, 8, FM_SHORT_RING>(s, thr, ghat, prev_active, out, part, stream, n1);
       return launch_hot_mixed<MODE, MOM64, 4, 16, 4>(s, thr, ghat, prev_active, out, part, stream, n1);
     }
   }
