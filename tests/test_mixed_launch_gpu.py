@@ -5,8 +5,9 @@ wave plus a remainder).  FM_HOT_SHORT selects the short form (3 ring stages,
 remainder at L = 8; what C2 picks) or the long form (4 stages, remainder at
 L = 16; what C4/C5 pick).  Image pairs are sampled from the first wave and
 from the remainder; masks and counts bit-exact, L1 / shifted-model terms
-within 1e-5, W within 2e-5 of the pair's scale (bench.check_pairs, the
-in-bench check of the timed pass)."""
+within 1e-5, W within 2e-5 of the pair's scale (fp64 moments: 3e-7;
+bench.check_pairs, the in-bench check of the timed pass).  Both moment
+precisions."""
 
 import numpy as np
 import pytest
@@ -14,8 +15,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("short", ["1", "0"])
-def test_mixed_launch_forms_match_oracle(short, monkeypatch):
+def test_mixed_launch_forms_match_oracle(short, precision, monkeypatch):
     import torch
 
     import bench
@@ -26,7 +28,8 @@ def test_mixed_launch_forms_match_oracle(short, monkeypatch):
 
     class Args:
         cfg = HotPathConfig()
-        precision = "fp32"
+
+    Args.precision = precision
 
     dev = torch.device("cuda")
     spec = scenes.SceneSpec(n_images=400, band=50, points_per_pair=128, seed=5)
